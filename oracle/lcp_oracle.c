@@ -1,0 +1,658 @@
+/*
+ * lcp_oracle.c -- plain, slow, obviously correct FP64 CPU oracle.
+ *
+ * TEST INFRASTRUCTURE ONLY (see lcp_oracle.h).  Shares no code with the CUDA
+ * path.  Build: gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC.
+ *
+ * Conventions (C0): cell size h_d = (hi_d - lo_d) / cells_d;
+ * vertex (i,j,k) sits at lo + (i,j,k) h; cell id = i + nx (j + ny k);
+ * corner c = c0 + 2 c1 + 4 c2 is vertex (i+c0, j+c1, k+c2);
+ * the octree lives on a virtual cube of 2^Lfull cells per axis anchored at lo.
+ *
+ * Parallelism: only `#pragma omp parallel for` over independent buckets,
+ * nodes or cells; every per-item computation is the sequential definition.
+ */
+#include "lcp_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_EINVAL 1
+#define ORC_EFACTOR 3
+#define ORC_ENUMERIC 4
+
+static const double ORC_SQRT2 = 1.4142135623730951;
+static const double ORC_PI = 3.141592653589793;
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+void orc_free(void* p) { free(p); }
+
+/* ------------------------------------------------------------------ C1 --- */
+/* SE: sigma^2 exp(-|x1-x2|^2 / (2 l^2)), per-axis l (BASELINE c3).
+ * Matern-5/2 (BASELINE c4, c5): r = |(x1-x2)/l|, sigma^2 (1 + sqrt5 r + 5/3 r^2) e^{-sqrt5 r}. */
+double orc_kernel(const orc_kernel_t* kern, const double* a, const double* b) {
+    double r2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        double t = (a[d] - b[d]) / kern->lengthscale[d];
+        r2 += t * t;
+    }
+    if (kern->kind == 0) return kern->variance * exp(-0.5 * r2);
+    double r = sqrt(r2);
+    double s5 = sqrt(5.0);
+    return kern->variance * (1.0 + s5 * r + (5.0 / 3.0) * r2) * exp(-s5 * r);
+}
+
+/* ------------------------------------------------------ dense helpers --- */
+/* Cholesky A = L L^T of an n x n row-major SPD matrix (lower written into L). */
+static int chol_plain(const double* A, double* L, int n) {
+    memset(L, 0, sizeof(double) * (size_t)n * n);
+    for (int j = 0; j < n; ++j) {
+        double s = A[(size_t)j * n + j];
+        for (int p = 0; p < j; ++p) s -= L[(size_t)j * n + p] * L[(size_t)j * n + p];
+        if (!(s > 0.0)) return ORC_EFACTOR;
+        double ljj = sqrt(s);
+        L[(size_t)j * n + j] = ljj;
+        for (int i = j + 1; i < n; ++i) {
+            double t = A[(size_t)i * n + j];
+            for (int p = 0; p < j; ++p) t -= L[(size_t)i * n + p] * L[(size_t)j * n + p];
+            L[(size_t)i * n + j] = t / ljj;
+        }
+    }
+    return ORC_OK;
+}
+
+/* K_y = K + sigma_n^2 I; on failure retry with jitter 1e-10, 1e-9, 1e-8 x sigma_f^2 (R15). */
+static int chol_jitter(double* A, double* L, int n, double variance) {
+    if (chol_plain(A, L, n) == ORC_OK) return ORC_OK;
+    double jit = 1e-10 * variance, added = 0.0;
+    for (int t = 0; t < 3; ++t, jit *= 10.0) {
+        for (int i = 0; i < n; ++i) A[(size_t)i * n + i] += jit - added;
+        added = jit;
+        if (chol_plain(A, L, n) == ORC_OK) return ORC_OK;
+    }
+    return ORC_EFACTOR;
+}
+
+/* forward substitution L v = b */
+static void forward_sub(const double* L, int n, const double* b, double* v) {
+    for (int i = 0; i < n; ++i) {
+        double t = b[i];
+        for (int p = 0; p < i; ++p) t -= L[(size_t)i * n + p] * v[p];
+        v[i] = t / L[(size_t)i * n + i];
+    }
+}
+
+/* backward substitution L^T v = b */
+static void backward_sub(const double* L, int n, const double* b, double* v) {
+    for (int i = n - 1; i >= 0; --i) {
+        double t = b[i];
+        for (int p = i + 1; p < n; ++p) t -= L[(size_t)p * n + i] * v[p];
+        v[i] = t / L[(size_t)i * n + i];
+    }
+}
+
+/* ------------------------------------------------------------------ C2 --- */
+/* Exact GP regression posterior = Eq. 1 with M = X,
+ * mu_M = K (K + s_n^2 I)^-1 y, A_M = s_n^2 K (K + s_n^2 I)^-1 (R1):
+ *   mu(I)    = m0 + K_IX alpha,            alpha = K_y^-1 (y - m0)
+ *   Sigma(I) = K_II - V^T V,               V = L^-1 K_XI,  K_y = L L^T          */
+int orc_gp_exact(const orc_kernel_t* kern, const double* X, const double* y, int64_t m,
+                 const double* Q, int64_t nq, double* mu, double* cov) {
+    int n = (int)m;
+    double* A = malloc(sizeof(double) * n * n);
+    double* L = malloc(sizeof(double) * n * n);
+    double* r = malloc(sizeof(double) * n);
+    double* w = malloc(sizeof(double) * n);
+    double* alpha = malloc(sizeof(double) * n);
+    double* V = malloc(sizeof(double) * n * (nq > 0 ? nq : 1));
+    double* kq = malloc(sizeof(double) * n);
+    int st = ORC_OK;
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            A[a * n + b] = orc_kernel(kern, X + 3 * a, X + 3 * b) + (a == b ? kern->nugget : 0.0);
+    st = chol_jitter(A, L, n, kern->variance);
+    if (st == ORC_OK) {
+        for (int a = 0; a < n; ++a) r[a] = y[a] - kern->prior_mean;
+        forward_sub(L, n, r, w);
+        backward_sub(L, n, w, alpha);
+        for (int64_t q = 0; q < nq; ++q) {
+            double s = 0.0;
+            for (int a = 0; a < n; ++a) {
+                kq[a] = orc_kernel(kern, X + 3 * a, Q + 3 * q);
+                s += kq[a] * alpha[a];
+            }
+            mu[q] = kern->prior_mean + s;
+            forward_sub(L, n, kq, V + (size_t)q * n);
+        }
+        if (cov) {
+            for (int64_t p = 0; p < nq; ++p)
+                for (int64_t q = 0; q < nq; ++q) {
+                    double s = orc_kernel(kern, Q + 3 * p, Q + 3 * q);
+                    for (int a = 0; a < n; ++a) s -= V[(size_t)p * n + a] * V[(size_t)q * n + a];
+                    cov[p * nq + q] = s;
+                }
+        }
+    }
+    free(A); free(L); free(r); free(w); free(alpha); free(V); free(kq);
+    return st;
+}
+
+/* --------------------------------------------------------------- C3-C4 --- */
+struct orc_model {
+    orc_kernel_t kern;
+    orc_grid_t grid;
+    double h[3];          /* cell size */
+    double w[3];          /* k-NN metric weights 1 / l_d */
+    int32_t lfull, b, bs, h_full;
+    int32_t nb[3], nbuckets;
+    int32_t m, k;
+    double* X;            /* m x 3 */
+    double* y;            /* m */
+    int32_t* S;           /* nbuckets x k, ascending observation index */
+    double* L;            /* nbuckets x k x k, lower factor of K_y(S_B) */
+    double* alpha;        /* nbuckets x k */
+    double* mu_obs;       /* m: local marginal at x_i from bucket(x_i) (R10) */
+    double* var_obs;      /* m (floored) */
+    int32_t* obs_cell;    /* m x 3 finest cell of x_i (clamped) */
+};
+
+static int32_t clampi(int64_t v, int32_t lo, int32_t hi) {
+    return (int32_t)(v < lo ? lo : (v > hi ? hi : v));
+}
+
+int32_t orc_model_nbuckets(const orc_model_t* M) { return M->nbuckets; }
+int32_t orc_model_lfull(const orc_model_t* M) { return M->lfull; }
+
+/* R3: point -> bucket floor((x - lo) / s_B) clamped, s_B = bs * h. */
+int32_t orc_point_bucket(const orc_model_t* M, const double* x) {
+    int32_t idx[3];
+    for (int d = 0; d < 3; ++d) {
+        double sB = (double)M->bs * M->h[d];
+        double t = floor((x[d] - M->grid.lo[d]) / sB);
+        idx[d] = clampi((int64_t)(t < -1.0 ? -1.0 : (t > 2e9 ? 2e9 : t)), 0, M->nb[d] - 1);
+    }
+    return idx[0] + M->nb[0] * (idx[1] + M->nb[1] * idx[2]);
+}
+
+/* R3: vertex (i,j,k) -> bucket min(i / bs, nb - 1) per axis. */
+int32_t orc_vertex_bucket(const orc_model_t* M, int32_t i, int32_t j, int32_t k) {
+    int32_t v[3] = {i, j, k}, idx[3];
+    for (int d = 0; d < 3; ++d) idx[d] = clampi(v[d] / M->bs, 0, M->nb[d] - 1);
+    return idx[0] + M->nb[0] * (idx[1] + M->nb[1] * idx[2]);
+}
+
+/* R3: cell -> bucket containing it (bucket boundaries are cell boundaries). */
+int32_t orc_cell_bucket(const orc_model_t* M, int64_t cell) {
+    int64_t nx = M->grid.cells[0], ny = M->grid.cells[1];
+    int32_t i = (int32_t)(cell % nx), j = (int32_t)((cell / nx) % ny), k = (int32_t)(cell / (nx * ny));
+    return orc_vertex_bucket(M, i, j, k);
+}
+
+void orc_model_bucket_set(const orc_model_t* M, int32_t b, int32_t* idx_out) {
+    memcpy(idx_out, M->S + (size_t)b * M->k, sizeof(int32_t) * M->k);
+}
+
+typedef struct { double d2; int32_t idx; } knn_item;
+
+static int knn_cmp(const void* pa, const void* pb) {
+    const knn_item* a = pa; const knn_item* b = pb;
+    if (a->d2 < b->d2) return -1;
+    if (a->d2 > b->d2) return 1;
+    return (a->idx > b->idx) - (a->idx < b->idx);
+}
+
+static int int_cmp(const void* pa, const void* pb) {
+    int32_t a = *(const int32_t*)pa, b = *(const int32_t*)pb;
+    return (a > b) - (a < b);
+}
+
+static void vertex_pos(const orc_model_t* M, int32_t i, int32_t j, int32_t k, double* x) {
+    x[0] = M->grid.lo[0] + (double)i * M->h[0];
+    x[1] = M->grid.lo[1] + (double)j * M->h[1];
+    x[2] = M->grid.lo[2] + (double)k * M->h[2];
+}
+
+int orc_local_marginal(const orc_model_t* M, int32_t b, const double* x, double* mu, double* var) {
+    int k = M->k;
+    const int32_t* S = M->S + (size_t)b * k;
+    const double* L = M->L + (size_t)b * k * k;
+    const double* al = M->alpha + (size_t)b * k;
+    double* kv = malloc(sizeof(double) * k);
+    double* v = malloc(sizeof(double) * k);
+    double s = 0.0;
+    for (int a = 0; a < k; ++a) {
+        kv[a] = orc_kernel(&M->kern, M->X + 3 * (size_t)S[a], x);
+        s += kv[a] * al[a];
+    }
+    *mu = M->kern.prior_mean + s;
+    forward_sub(L, k, kv, v);
+    double q = orc_kernel(&M->kern, x, x);
+    for (int a = 0; a < k; ++a) q -= v[a] * v[a];
+    *var = q;
+    free(kv); free(v);
+    return ORC_OK;
+}
+
+/* R16: variance floor 1e-12 sigma_f^2, error below -1e-8 sigma_f^2. */
+static int floor_var(const orc_model_t* M, double var, double* out) {
+    if (var < -1e-8 * M->kern.variance) return ORC_ENUMERIC;
+    double f = 1e-12 * M->kern.variance;
+    *out = var > f ? var : f;
+    return ORC_OK;
+}
+
+int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
+                     const double* y, int64_t m, int32_t k, int32_t bucket_log2,
+                     int32_t h_full, orc_model_t** out) {
+    *out = NULL;
+    if (m < 1 || k < 1 || k > m || bucket_log2 < 0 || h_full < 0) return ORC_EINVAL;
+    if (kern->variance <= 0 || kern->nugget < 0) return ORC_EINVAL;
+    for (int d = 0; d < 3; ++d)
+        if (grid->cells[d] < 1 || !(grid->hi[d] > grid->lo[d]) || kern->lengthscale[d] <= 0)
+            return ORC_EINVAL;
+    orc_model_t* M = calloc(1, sizeof(orc_model_t));
+    M->kern = *kern;
+    M->grid = *grid;
+    int32_t cmax = grid->cells[0];
+    if (grid->cells[1] > cmax) cmax = grid->cells[1];
+    if (grid->cells[2] > cmax) cmax = grid->cells[2];
+    int32_t lf = 0;
+    while ((1 << lf) < cmax) ++lf;
+    M->lfull = lf;
+    if (bucket_log2 > lf) { free(M); return ORC_EINVAL; }
+    M->b = bucket_log2;
+    M->bs = 1 << (lf - bucket_log2);
+    M->h_full = h_full;
+    for (int d = 0; d < 3; ++d) {
+        M->h[d] = (grid->hi[d] - grid->lo[d]) / (double)grid->cells[d];
+        M->w[d] = 1.0 / kern->lengthscale[d];
+        M->nb[d] = (grid->cells[d] + M->bs - 1) / M->bs;
+    }
+    M->nbuckets = M->nb[0] * M->nb[1] * M->nb[2];
+    M->m = (int32_t)m;
+    M->k = k;
+    M->X = malloc(sizeof(double) * 3 * m);
+    M->y = malloc(sizeof(double) * m);
+    memcpy(M->X, X, sizeof(double) * 3 * m);
+    memcpy(M->y, y, sizeof(double) * m);
+    M->S = malloc(sizeof(int32_t) * (size_t)M->nbuckets * k);
+    M->L = malloc(sizeof(double) * (size_t)M->nbuckets * k * k);
+    M->alpha = malloc(sizeof(double) * (size_t)M->nbuckets * k);
+    int status = ORC_OK;
+
+#pragma omp parallel for schedule(dynamic)
+    for (int32_t bkt = 0; bkt < M->nbuckets; ++bkt) {
+        int32_t bi[3] = {bkt % M->nb[0], (bkt / M->nb[0]) % M->nb[1], bkt / (M->nb[0] * M->nb[1])};
+        double c[3];
+        for (int d = 0; d < 3; ++d) c[d] = grid->lo[d] + ((double)bi[d] + 0.5) * ((double)M->bs * M->h[d]);
+        /* k nearest in the metric sum_d ((x_d - c_d) w_d)^2, ties -> lower index (R2) */
+        knn_item* it = malloc(sizeof(knn_item) * m);
+        for (int64_t i = 0; i < m; ++i) {
+            double t0 = (X[3 * i + 0] - c[0]) * M->w[0];
+            double t1 = (X[3 * i + 1] - c[1]) * M->w[1];
+            double t2 = (X[3 * i + 2] - c[2]) * M->w[2];
+            it[i].d2 = t0 * t0 + t1 * t1 + t2 * t2;
+            it[i].idx = (int32_t)i;
+        }
+        qsort(it, m, sizeof(knn_item), knn_cmp);
+        int32_t* S = M->S + (size_t)bkt * k;
+        for (int a = 0; a < k; ++a) S[a] = it[a].idx;
+        qsort(S, k, sizeof(int32_t), int_cmp);
+        free(it);
+        /* K_y = K(S,S) + sigma_n^2 I; L = chol(K_y); alpha = K_y^-1 (y_S - m0)  (Eq. 1, R1) */
+        double* A = malloc(sizeof(double) * k * k);
+        double* Lb = M->L + (size_t)bkt * k * k;
+        for (int a = 0; a < k; ++a)
+            for (int b2 = 0; b2 < k; ++b2)
+                A[a * k + b2] = orc_kernel(kern, X + 3 * (size_t)S[a], X + 3 * (size_t)S[b2]) +
+                                (a == b2 ? kern->nugget : 0.0);
+        int st = chol_jitter(A, Lb, k, kern->variance);
+        if (st != ORC_OK) {
+#pragma omp critical
+            status = st;
+        } else {
+            double* r = malloc(sizeof(double) * k);
+            double* w = malloc(sizeof(double) * k);
+            for (int a = 0; a < k; ++a) r[a] = y[S[a]] - kern->prior_mean;
+            forward_sub(Lb, k, r, w);
+            backward_sub(Lb, k, w, M->alpha + (size_t)bkt * k);
+            free(r); free(w);
+        }
+        free(A);
+    }
+    if (status != ORC_OK) { orc_model_destroy(M); return status; }
+
+    /* a4: observation marginals and finest cells (R10) */
+    M->mu_obs = malloc(sizeof(double) * m);
+    M->var_obs = malloc(sizeof(double) * m);
+    M->obs_cell = malloc(sizeof(int32_t) * 3 * m);
+    for (int64_t i = 0; i < m; ++i) {
+        double var;
+        orc_local_marginal(M, orc_point_bucket(M, X + 3 * i), X + 3 * i, &M->mu_obs[i], &var);
+        if (floor_var(M, var, &M->var_obs[i]) != ORC_OK) status = ORC_ENUMERIC;
+        for (int d = 0; d < 3; ++d) {
+            double t = floor((X[3 * i + d] - grid->lo[d]) / M->h[d]);
+            M->obs_cell[3 * i + d] = clampi((int64_t)(t < -1.0 ? -1.0 : (t > 2e9 ? 2e9 : t)), 0, grid->cells[d] - 1);
+        }
+    }
+    if (status != ORC_OK) { orc_model_destroy(M); return status; }
+    *out = M;
+    return ORC_OK;
+}
+
+void orc_model_destroy(orc_model_t* M) {
+    if (!M) return;
+    free(M->X); free(M->y); free(M->S); free(M->L); free(M->alpha);
+    free(M->mu_obs); free(M->var_obs); free(M->obs_cell);
+    free(M);
+}
+
+/* ------------------------------------------------------------------ C8 --- */
+int orc_cell_posterior(const orc_model_t* M, int64_t cell, double* mu, double* cov) {
+    int k = M->k;
+    int64_t nx = M->grid.cells[0], ny = M->grid.cells[1];
+    int32_t ci = (int32_t)(cell % nx), cj = (int32_t)((cell / nx) % ny), ck = (int32_t)(cell / (nx * ny));
+    int32_t b = orc_vertex_bucket(M, ci, cj, ck);
+    const int32_t* S = M->S + (size_t)b * k;
+    const double* L = M->L + (size_t)b * k * k;
+    const double* al = M->alpha + (size_t)b * k;
+    double xc[8][3];
+    for (int c = 0; c < 8; ++c) vertex_pos(M, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2), xc[c]);
+    double* K = malloc(sizeof(double) * k);
+    double* V = malloc(sizeof(double) * 8 * k);
+    for (int c = 0; c < 8; ++c) {
+        double s = 0.0;
+        for (int a = 0; a < k; ++a) {
+            K[a] = orc_kernel(&M->kern, M->X + 3 * (size_t)S[a], xc[c]);
+            s += K[a] * al[a];
+        }
+        mu[c] = M->kern.prior_mean + s;
+        forward_sub(L, k, K, V + (size_t)c * k);
+    }
+    int st = ORC_OK;
+    for (int c = 0; c < 8; ++c)
+        for (int e = 0; e < 8; ++e) {
+            double s = orc_kernel(&M->kern, xc[c], xc[e]);
+            for (int a = 0; a < k; ++a) s -= V[(size_t)c * k + a] * V[(size_t)e * k + a];
+            cov[c * 8 + e] = s;
+        }
+    for (int c = 0; c < 8; ++c)
+        if (cov[c * 8 + c] < -1e-8 * M->kern.variance) st = ORC_ENUMERIC;
+    free(K); free(V);
+    return st;
+}
+
+/* ------------------------------------------------------------------ C9 --- */
+/* Cholesky of the 8x8 corner covariance; a pivot <= 1e-12 max_diag is clamped:
+ * L_jj = 0 and the column below is zeroed (PSD clamp, never fails; R14). */
+void orc_chol8(const double* S, double* L) {
+    double md = 0.0;
+    for (int c = 0; c < 8; ++c) if (S[c * 8 + c] > md) md = S[c * 8 + c];
+    double tol = 1e-12 * md;
+    memset(L, 0, sizeof(double) * 64);
+    for (int j = 0; j < 8; ++j) {
+        double s = S[j * 8 + j];
+        for (int p = 0; p < j; ++p) s -= L[j * 8 + p] * L[j * 8 + p];
+        if (s <= tol) continue;  /* column stays zero */
+        double ljj = sqrt(s);
+        L[j * 8 + j] = ljj;
+        for (int i = j + 1; i < 8; ++i) {
+            double t = S[i * 8 + j];
+            for (int p = 0; p < j; ++p) t -= L[i * 8 + p] * L[j * 8 + p];
+            L[i * 8 + j] = t / ljj;
+        }
+    }
+}
+
+/* ----------------------------------------------------------------- C10 --- */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): 10 rounds of
+ *   (hi0, lo0) = M0 * c0, (hi1, lo1) = M1 * c2,
+ *   c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0),
+ * with the key bumped by the Weyl constants between rounds.                   */
+void orc_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        uint32_t n1 = (uint32_t)p1;
+        uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        uint32_t n3 = (uint32_t)p0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    memcpy(out, c, sizeof(c));
+}
+
+/* uniform from the low 23 bits: u = (r mod 2^23 + 1/2) 2^-23 in [2^-24, 1 - 2^-24] (R13) */
+static double u23(uint32_t r) { return ((double)(r & 0x7FFFFFu) + 0.5) * (1.0 / 8388608.0); }
+
+/* counter = (2s + j, cell lo32, cell hi32, iso_index), key = (seed lo32, seed hi32);
+ * Box-Muller pairs (u_a, u_b): R = sqrt(-2 ln u_a), (R cos 2 pi u_b, R sin 2 pi u_b). */
+void orc_normals8(uint64_t seed, int64_t cell, uint32_t iso_index, int64_t s, double* z) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int j = 0; j < 2; ++j) {
+        uint32_t ctr[4] = {(uint32_t)(2 * s + j), (uint32_t)(uint64_t)cell,
+                           (uint32_t)((uint64_t)cell >> 32), iso_index};
+        uint32_t r[4];
+        orc_philox4x32_10(ctr, key, r);
+        for (int p = 0; p < 2; ++p) {
+            double ua = u23(r[2 * p]), ub = u23(r[2 * p + 1]);
+            double R = sqrt(-2.0 * log(ua));
+            z[4 * j + 2 * p] = R * cos(2.0 * ORC_PI * ub);
+            z[4 * j + 2 * p + 1] = R * sin(2.0 * ORC_PI * ub);
+        }
+    }
+}
+
+/* ----------------------------------------------------------------- C11 --- */
+/* y = mu + L z; crossing = not(all y < theta) and not(all y > theta)
+ * (the displayed sum at :130 is the NOT-crossed mass, R5). */
+int64_t orc_mc_count(const double* mu, const double* L, double theta, int64_t n_samples,
+                     uint64_t seed, int64_t cell, uint32_t iso_index) {
+    int64_t count = 0;
+    for (int64_t s = 0; s < n_samples; ++s) {
+        double z[8], y[8];
+        orc_normals8(seed, cell, iso_index, s, z);
+        int below = 1, above = 1;
+        for (int c = 0; c < 8; ++c) {
+            y[c] = mu[c];
+            for (int e = 0; e <= c; ++e) y[c] += L[c * 8 + e] * z[e];
+            below = below && (y[c] < theta);
+            above = above && (y[c] > theta);
+        }
+        if (!below && !above) ++count;
+    }
+    return count;
+}
+
+int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double theta,
+                  int64_t n_samples, uint64_t seed, uint32_t iso_index, double* lcp_out) {
+    if (n_samples < 1) return ORC_EINVAL;
+    int status = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < n; ++q) {
+        double mu[8], cov[64], L[64];
+        int st = orc_cell_posterior(M, cells[q], mu, cov);
+        if (st != ORC_OK) {
+#pragma omp critical
+            status = st;
+        }
+        orc_chol8(cov, L);
+        lcp_out[q] = (double)orc_mc_count(mu, L, theta, n_samples, seed, cells[q], iso_index) /
+                     (double)n_samples;
+    }
+    return status;
+}
+
+/* ------------------------------------------------------------------ C6 --- */
+/* P(Y < theta) = Phi((theta - mu) / sigma) (Sigma read as sigma, R4),
+ * evaluated as erfc so that both tails keep full relative precision. */
+void orc_tail_probs(double mu, double var, double theta, double* p_lo, double* p_hi) {
+    double sd2 = sqrt(var) * ORC_SQRT2;
+    *p_lo = 0.5 * erfc((mu - theta) / sd2);
+    *p_hi = 0.5 * erfc((theta - mu) / sd2);
+}
+
+int orc_eval_node(const orc_model_t* M, double theta, double alpha, int32_t level,
+                  int32_t i, int32_t j, int32_t k, orc_node_rec_t* rec) {
+    int32_t h = M->lfull - level;
+    int64_t side = (int64_t)1 << h;
+    int32_t a[3] = {i, j, k};
+    int64_t base[3], vmax[3];
+    for (int d = 0; d < 3; ++d) {
+        base[d] = (int64_t)a[d] * side;
+        vmax[d] = base[d] + side < M->grid.cells[d] ? base[d] + side : M->grid.cells[d];
+    }
+    rec->level = level; rec->i = i; rec->j = j; rec->k = k;
+    /* Alg. 1 lines 3-5: M~ = observations inside the node, p1 = max P(Y_i < theta),
+     * p2 = max P(Y_i > theta) */
+    int any = 0;
+    double p1 = -1.0, p2 = -1.0;
+    for (int32_t o = 0; o < M->m; ++o) {
+        const int32_t* oc = M->obs_cell + 3 * o;
+        int in = 1;
+        for (int d = 0; d < 3; ++d) in = in && oc[d] >= base[d] && oc[d] < base[d] + side;
+        if (!in) continue;
+        double pl, ph;
+        orc_tail_probs(M->mu_obs[o], M->var_obs[o], theta, &pl, &ph);
+        if (!any || pl > p1) p1 = pl;
+        if (!any || ph > p2) p2 = ph;
+        any = 1;
+    }
+    rec->p1 = p1; rec->p2 = p2;
+    if (any && p1 > alpha && p2 > alpha) {            /* case 1 (lines 6-7) */
+        rec->ncase = 1; rec->U = 1.0; rec->refine = 1;
+        return ORC_OK;
+    }
+    int ncase = !any ? 0 : (p2 <= alpha ? 2 : 3);     /* R8, R9 */
+    /* B_l = min_D P(Y < theta), B_u = min_D P(Y > theta) over the candidate lattice
+     * (R6): Q_lo = 1 - B_l, Q_hi = 1 - B_u. */
+    int32_t st = h - M->h_full > 0 ? h - M->h_full : 0;
+    int64_t stride = (int64_t)1 << st;
+    int64_t lst[3][1 << 12];
+    int nl[3];
+    for (int d = 0; d < 3; ++d) {
+        nl[d] = 0;
+        for (int64_t v = base[d]; v < vmax[d]; v += stride) lst[d][nl[d]++] = v;
+        lst[d][nl[d]++] = vmax[d];
+    }
+    double q_lo = 0.0, q_hi = 0.0;
+    int status = ORC_OK;
+    for (int z = 0; z < nl[2]; ++z)
+        for (int y = 0; y < nl[1]; ++y)
+            for (int x = 0; x < nl[0]; ++x) {
+                int32_t vi = (int32_t)lst[0][x], vj = (int32_t)lst[1][y], vk = (int32_t)lst[2][z];
+                double xv[3], mu, var, vf = 0.0, pl, ph;
+                vertex_pos(M, vi, vj, vk, xv);
+                orc_local_marginal(M, orc_vertex_bucket(M, vi, vj, vk), xv, &mu, &var);
+                if (floor_var(M, var, &vf) != ORC_OK) status = ORC_ENUMERIC;
+                orc_tail_probs(mu, vf, theta, &pl, &ph);
+                if (ph > q_lo) q_lo = ph;
+                if (pl > q_hi) q_hi = pl;
+            }
+    /* d = inclusive vertex count of the (clipped) node (Alg. 1 line 10, R7) */
+    double dcount = (double)(vmax[0] - base[0] + 1) * (double)(vmax[1] - base[1] + 1) *
+                    (double)(vmax[2] - base[2] + 1);
+    double U;
+    if (ncase == 2) {
+        U = -expm1(dcount * log1p(-q_lo));                       /* 1 - B_l^d */
+    } else if (ncase == 3) {
+        U = -expm1(dcount * log1p(-q_hi));                       /* 1 - B_u^d */
+    } else {
+        U = -expm1(dcount * log1p(-q_lo)) - exp(dcount * log1p(-q_hi));   /* Eq. 4 */
+        if (U < 0.0) U = 0.0;
+        if (U > 1.0) U = 1.0;
+    }
+    rec->ncase = ncase; rec->U = U; rec->refine = U > alpha;
+    return status;
+}
+
+/* ------------------------------------------------------------------ C7 --- */
+typedef struct { int32_t i, j, k; } node3;
+
+static int cmp64(const void* a, const void* b) {
+    int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return (x > y) - (x < y);
+}
+
+int orc_octree(const orc_model_t* M, double theta, double alpha, int32_t max_depth,
+               int32_t sub_level, int32_t si, int32_t sj, int32_t sk,
+               orc_node_rec_t** recs_out, int64_t* n_recs, int64_t** leaves_out, int64_t* n_leaves) {
+    if (!(alpha > 0.0 && alpha < 0.5) || max_depth < 0 || max_depth > M->lfull) return ORC_EINVAL;
+    int32_t L0 = sub_level >= 0 ? sub_level : 0;
+    if (L0 > max_depth) return ORC_EINVAL;
+    node3* front = malloc(sizeof(node3));
+    int64_t nf = 1;
+    front[0].i = sub_level >= 0 ? si : 0;
+    front[0].j = sub_level >= 0 ? sj : 0;
+    front[0].k = sub_level >= 0 ? sk : 0;
+    int64_t cap_r = 1024, nr = 0, cap_l = 1024, nlv = 0;
+    orc_node_rec_t* recs = malloc(sizeof(orc_node_rec_t) * cap_r);
+    int64_t* leaves = malloc(sizeof(int64_t) * cap_l);
+    int status = ORC_OK;
+    const int32_t* cells = M->grid.cells;
+    for (int32_t level = L0; level <= max_depth && nf > 0; ++level) {
+        orc_node_rec_t* lr = malloc(sizeof(orc_node_rec_t) * nf);
+#pragma omp parallel for schedule(dynamic)
+        for (int64_t q = 0; q < nf; ++q) {
+            int st = orc_eval_node(M, theta, alpha, level, front[q].i, front[q].j, front[q].k, &lr[q]);
+            if (st != ORC_OK) {
+#pragma omp critical
+                status = st;
+            }
+        }
+        if (nr + nf > cap_r) {
+            while (nr + nf > cap_r) cap_r *= 2;
+            recs = realloc(recs, sizeof(orc_node_rec_t) * cap_r);
+        }
+        memcpy(recs + nr, lr, sizeof(orc_node_rec_t) * nf);
+        nr += nf;
+        int32_t h = M->lfull - level;
+        int64_t nn = 0;
+        node3* next = malloc(sizeof(node3) * 8 * nf);
+        for (int64_t q = 0; q < nf; ++q) {
+            if (!lr[q].refine) continue;
+            if (level < max_depth) {           /* Alg. 1 lines 14-21: 8 children */
+                for (int c = 0; c < 8; ++c) {
+                    node3 ch = {2 * front[q].i + (c & 1), 2 * front[q].j + ((c >> 1) & 1),
+                                2 * front[q].k + (c >> 2)};
+                    int64_t cs = (int64_t)1 << (h - 1);
+                    if ((int64_t)ch.i * cs < cells[0] && (int64_t)ch.j * cs < cells[1] &&
+                        (int64_t)ch.k * cs < cells[2])
+                        next[nn++] = ch;
+                }
+            } else {                           /* lines 12-13: max depth, return the box's cells */
+                int64_t side = (int64_t)1 << h;
+                for (int64_t z = (int64_t)front[q].k * side; z < ((int64_t)front[q].k + 1) * side && z < cells[2]; ++z)
+                    for (int64_t y = (int64_t)front[q].j * side; y < ((int64_t)front[q].j + 1) * side && y < cells[1]; ++y)
+                        for (int64_t x = (int64_t)front[q].i * side; x < ((int64_t)front[q].i + 1) * side && x < cells[0]; ++x) {
+                            if (nlv == cap_l) { cap_l *= 2; leaves = realloc(leaves, sizeof(int64_t) * cap_l); }
+                            leaves[nlv++] = x + (int64_t)cells[0] * (y + (int64_t)cells[1] * z);
+                        }
+            }
+        }
+        free(lr);
+        free(front);
+        front = next;
+        nf = nn;
+    }
+    free(front);
+    qsort(leaves, nlv, sizeof(int64_t), cmp64);
+    *recs_out = recs; *n_recs = nr; *leaves_out = leaves; *n_leaves = nlv;
+    return status;
+}
+

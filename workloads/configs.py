@@ -1,0 +1,97 @@
+"""Configuration records for the synthetic workloads.
+
+c1..c5 follow BASELINE.json `configs[0..4]`; values BASELINE.json leaves open
+are the readings listed in DESIGN.md §3.  t1/t2 are
+small ragged parity cases (non-power-of-two grids, max_depth < full depth,
+bucket grids that do not divide the grid) that the oracle finishes in seconds.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional, Tuple
+
+KERNEL_SE = 0
+KERNEL_MATERN52 = 1
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    lo: Tuple[float, float, float]
+    hi: Tuple[float, float, float]
+    cells: Tuple[int, int, int]
+    m: int
+    # field recipe
+    n_bumps: int
+    width_lo: float
+    width_hi: float
+    width_log: bool              # log-uniform widths (c5)
+    ramp_z: float                # + ramp_z * z
+    texture_sin4pix: float       # + texture * sin(4 pi x)
+    tangle_like: bool            # c1: sin(2 pi x) cos(2 pi y) + 0.5 z
+    noise_std: float
+    placement: str               # "uniform" | "grad" | "mixed"
+    # GP kernel (lcp_kernel_t)
+    kernel: int
+    variance: float
+    lengthscale: Tuple[float, float, float]
+    nugget: float
+    prior_mean: float
+    # method parameters
+    thetas: Tuple[Optional[float], ...]   # None = median of f on the vertex lattice
+    k: int
+    bucket_log2: int
+    h_full: int
+    n_samples: int
+    alpha: float
+    max_depth: int
+    precision: str               # "fp64" | "fp32" (posterior precision)
+    gen_seed: int
+    mc_seed: int
+
+
+def _cube(n):
+    return (n, n, n)
+
+
+CONFIGS = {
+    # BASELINE.json configs[0]: Tangle-sized tiny case, exact GP (k = m, one bucket).
+    "c1": Config("c1", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(16), 50,
+                 0, 0.0, 0.0, False, 0.0, 0.0, True, 0.01, "uniform",
+                 KERNEL_SE, 1.0, (0.2, 0.2, 0.2), 1e-4, 0.0,
+                 (0.0,), 50, 0, 4, 1000, 1e-3, 4, "fp64", 1001, 2001),
+    # configs[1]
+    "c2": Config("c2", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(64), 200,
+                 8, 0.05, 0.2, False, 0.0, 0.0, False, 0.02, "uniform",
+                 KERNEL_SE, 1.0, (0.15, 0.15, 0.15), 4e-4, 0.0,
+                 (0.1,), 32, 3, 2, 2000, 1e-3, 6, "fp32", 1002, 2002),
+    # configs[2]: the paper's m = 500 at 128^3; theta = median of f on the 129^3 vertices
+    "c3": Config("c3", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(128), 500,
+                 16, 0.05, 0.2, False, 0.5, 0.0, False, 0.01, "uniform",
+                 KERNEL_SE, 0.5, (0.1, 0.15, 0.2), 1e-4, 0.0,
+                 (None,), 64, 3, 2, 4096, 1e-4, 7, "fp64", 1003, 2003),
+    # configs[3]: 256x256x128 cubic cells of side 1/256 (domain z in [0, 0.5])
+    "c4": Config("c4", (0.0, 0.0, 0.0), (1.0, 1.0, 0.5), (256, 256, 128), 2000,
+                 64, 0.05, 0.2, False, 0.0, 0.2, False, 1e-5 ** 0.5, "grad",
+                 KERNEL_MATERN52, 1.0, (0.08, 0.08, 0.08), 1e-5, 0.0,
+                 (-0.2, 0.0, 0.3), 64, 4, 2, 10000, 1e-4, 8, "fp64", 1004, 2004),
+    # configs[4]: the 512^3 multi-GPU workload
+    "c5": Config("c5", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(512), 20000,
+                 256, 0.01, 0.2, True, 0.0, 0.0, False, 0.01, "mixed",
+                 KERNEL_MATERN52, 1.0, (0.03, 0.03, 0.03), 1e-4, 0.0,
+                 (0.0,), 128, 5, 2, 4096, 1e-5, 9, "fp64", 1005, 2005),
+    # ragged parity case: non-power-of-two grid, bucket grid not dividing it
+    "t1": Config("t1", (0.0, 0.0, 0.0), (0.92, 0.68, 0.44), (23, 17, 11), 60,
+                 6, 0.05, 0.2, False, 0.0, 0.0, False, 0.01, "uniform",
+                 KERNEL_SE, 1.0, (0.15, 0.15, 0.15), 1e-4, 0.0,
+                 (0.05,), 24, 2, 1, 777, 1e-3, 5, "fp64", 1101, 2101),
+    # ragged parity case 2: Matern, anisotropic grid, max_depth < full depth, k < m
+    "t2": Config("t2", (-1.0, 0.5, 2.0), (0.6, 0.86, 3.32), (40, 9, 33), 90,
+                 10, 0.1, 0.4, False, 0.3, 0.0, False, 0.02, "grad",
+                 KERNEL_MATERN52, 0.8, (0.25, 0.2, 0.3), 2e-4, 0.1,
+                 (0.2, -0.1), 40, 2, 2, 333, 1e-3, 5, "fp64", 1102, 2102),
+}
+
+
+def get_config(name: str) -> Config:
+    return CONFIGS[name]
