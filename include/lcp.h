@@ -1,0 +1,184 @@
+/*
+ * lcp.h -- C ABI of the B200-native level-crossing-probability (LCP) library.
+ *
+ * Implements the data-parallel hot path of arxiv 2512.12442 ("efficient LCP
+ * computation for GP-represented data"; PAPER.md = /root/reference/PAPER.md):
+ *   - lcp_fit_local      : bucket-local k-NN GP factors
+ *   - lcp_octree_refine  : Alg. 1 octree with the Eq. 4 bound   (a5-a6)
+ *   - lcp_pmc_cells      : per-cell posterior + 8x8 Cholesky + Philox MC (a7-a8)
+ *   - lcp_scatter_field / lcp_run_field : dense LCP field output (a9)
+ * Every step runs in hand-written sm_100a kernels of liblcp.so.  There is no
+ * CPU fallback: without a CUDA device every call returns LCP_ECUDA.
+ *
+ * Conventions: cell size h_d = (hi_d - lo_d) / cells_d; vertex
+ * (i,j,k) at lo + (i,j,k) h; cell id = i + nx (j + ny k) (x fastest); corner
+ * c = c0 + 2 c1 + 4 c2 of cell (i,j,k) is vertex (i+c0, j+c1, k+c2)
+ * (PAPER.md:118-122).  Pointers are plain host or device pointers as stated
+ * per argument; "device" pointers must be valid on the ctx's device.
+ *
+ * Errors: every call returns lcp_status_t; outputs are undefined unless the
+ * status is LCP_OK, and lcp_last_error() then holds a message.  No exception
+ * or abort crosses the ABI.  Threading: one ctx per device per host thread.
+ */
+#ifndef LCP_H
+#define LCP_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lcp_ctx lcp_ctx_t;   /* opaque; owns all device caches */
+
+typedef enum {
+    LCP_OK = 0,
+    LCP_EINVAL = 1,    /* bad argument (alpha not in (0,0.5), N < 1, k < 1 or k > m, ...) */
+    LCP_ESTATE = 2,    /* refine / pmc before fit */
+    LCP_EFACTOR = 3,   /* a bucket K_y not PD even after jitter 1e-10..1e-8 sigma_f^2 (R15) */
+    LCP_ENUMERIC = 4,  /* a posterior variance < -1e-8 sigma_f^2 (R16) */
+    LCP_ECUDA = 5,     /* CUDA runtime error (incl. no device) */
+    LCP_ENOMEM = 6     /* device allocation failed */
+} lcp_status_t;
+
+typedef enum { LCP_K_SE = 0, LCP_K_MATERN52 = 1 } lcp_kernel_kind_t;
+typedef enum { LCP_FP64 = 0, LCP_FP32 = 1 } lcp_prec_t;
+
+/* GP prior: k(x1,x2) = variance * f(|(x1-x2)/lengthscale|);
+ * SE f = exp(-r^2/2); Matern-5/2 f = (1 + sqrt5 r + 5/3 r^2) exp(-sqrt5 r).
+ * nugget = observation noise variance sigma_n^2 (R1); prior_mean = m0. */
+typedef struct {
+    int32_t kind;
+    int32_t pad_;
+    double variance;
+    double lengthscale[3];
+    double nugget;
+    double prior_mean;
+} lcp_kernel_t;
+
+/* target grid: domain [lo, hi], cells[d] cells per axis */
+typedef struct {
+    double lo[3];
+    double hi[3];
+    int32_t cells[3];
+    int32_t pad_;
+} lcp_grid_t;
+
+typedef struct {
+    int32_t bucket_log2;   /* bucket grid: 2^bucket_log2 buckets per axis of the virtual cube (R3) */
+    int32_t h_full;        /* candidate lattice: all vertices at node heights <= h_full (R6) */
+    int32_t precision;     /* lcp_prec_t of the leaf posterior (R17) */
+    int32_t slab_rank;     /* z-slab decomposition: this rank ... */
+    int32_t slab_count;    /* ... of slab_count (1 = whole domain) */
+    int32_t slab_level;    /* octree level whose z-layers are split across ranks (default 3) */
+    int32_t keep_records;  /* parity tap: keep per-node records of levels < keep_records (0 = none) */
+    int32_t pad_;
+} lcp_opts_t;
+
+/* per evaluated octree node (Alg. 1) */
+typedef struct {
+    int32_t level, i, j, k;   /* node index at `level` of the virtual 2^Lfull cube (R23) */
+    int32_t ncase;            /* 0: M~ empty, 1: p1>a & p2>a, 2: p2<=a, 3: p1<=a (R8, R9) */
+    int32_t refine;           /* subdivide (or emit, at max depth) */
+    double p1, p2, U;         /* max P(Y_i<th), max P(Y_i>th) over M~ (-1 if empty), bound U */
+} lcp_node_rec_t;
+
+typedef struct {
+    int64_t m;           /* observations */
+    int32_t k;           /* local-GP size */
+    int32_t nbuckets;
+    int32_t nb[3];
+    int32_t lfull;       /* depth of the full octree (2^lfull >= max cells) */
+    int32_t bucket_side; /* cells per bucket side */
+    int32_t device;
+} lcp_info_t;
+
+/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
+ * (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a private stream.
+ * The ctx never destroys a caller-provided stream. */
+lcp_status_t lcp_create(int32_t device, void* cuda_stream, lcp_ctx_t** out);
+void lcp_destroy(lcp_ctx_t* ctx);
+const char* lcp_last_error(const lcp_ctx_t* ctx);
+
+/* a1-a4: bin the m observations into the bucket grid, gather each bucket's k
+ * nearest observations (R2), build K_y = K_SS + nugget I, its Cholesky factor,
+ * L^-1 and alpha = K_y^-1 (y_S - m0) per bucket (Eq. 1, PAPER.md:89-100;
+ * local GP), and the observation marginals.
+ *   xyz: m x 3 row-major, y: m; host pointers if on_device == 0 (copied inside,
+ *   synchronously), else device pointers (read before return).
+ *   opts may be NULL (bucket_log2 = 0, h_full = 2, FP64, one slab, level 3, no records).
+ * Errors: EINVAL (k < 1, k > m, variance <= 0, nugget < 0, lengthscale <= 0,
+ * cells < 1, bucket_log2 > Lfull), EFACTOR, ENUMERIC, ENOMEM, ECUDA. */
+lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, int64_t m,
+                           int32_t on_device, const lcp_kernel_t* kernel, int32_t k,
+                           const lcp_grid_t* grid, const lcp_opts_t* opts);
+
+/* a5-a6: Alg. 1 as a level-synchronous pass over levels
+ * 0..max_depth with the three-case preliminary test and the
+ * Slepian bound U = 1 - B_l^d - B_u^d (Eq. 3-4; R6-R9).
+ * Nodes with U <= threshold are pruned.  Returns the leaf cells (cells of
+ * refined max-depth nodes) in a ctx-owned device array valid until the next
+ * fit/refine/destroy.  Blocks the host (one size read-back per level).
+ * Errors: ESTATE before fit; EINVAL unless 0 < threshold < 0.5 and
+ * 0 <= max_depth <= Lfull. */
+lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold,
+                               int32_t max_depth, int64_t* n_leaf_out,
+                               const int64_t** leaf_cells_dev_out);
+
+/* a7-a8: for each cell id, the 8-corner posterior of the cell's bucket local
+ * GP, its 8x8 Cholesky (R14), and an N-sample Philox MC count
+ * of samples whose corners straddle `isovalue` (R13, R24).
+ *   cells: n_cells ids (device pointer if cells_on_device, else host);
+ *   lcp_out: n_cells floats = count / n_samples (device pointer if
+ *   out_on_device, else host: the call then synchronizes).
+ * Any cell list is accepted (dense baseline = all ids).  Asynchronous on the
+ * ctx stream when both pointers are device pointers.
+ * Errors: ESTATE, EINVAL (n_samples < 1, cell id out of range -> ENUMERIC-free
+ * check on the host only when cells_on_device == 0), ENUMERIC, ECUDA. */
+lcp_status_t lcp_pmc_cells(lcp_ctx_t* ctx, const int64_t* cells, int64_t n_cells,
+                           int32_t cells_on_device, double isovalue, int64_t n_samples,
+                           uint64_t seed, uint32_t iso_index, float* lcp_out,
+                           int32_t out_on_device);
+
+/* a9: zero `field` (nx*ny*nz floats, device) and scatter lcp[q] into cell
+ * cells[q] (every other cell is 0).  Asynchronous. */
+lcp_status_t lcp_scatter_field(lcp_ctx_t* ctx, const int64_t* cells_dev, const float* lcp_dev,
+                               int64_t n, float* field_dev);
+
+/* One whole step of the path after fit: refine + pmc on the leaves + scatter
+ * into the dense field (device pointer if out_on_device, else host, copied
+ * before return).  n_leaf_out may be NULL. */
+lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, int32_t max_depth,
+                           int64_t n_samples, uint64_t seed, uint32_t iso_index, float* field,
+                           int32_t out_on_device, int64_t* n_leaf_out);
+
+/* ---- parity taps (used by tests; not on the hot path) ---- */
+
+/* node records of the last refine (opts.keep_records != 0), levels ascending,
+ * Morton order within a level; ctx-owned device array. */
+lcp_status_t lcp_node_records(lcp_ctx_t* ctx, int64_t* n_out, const lcp_node_rec_t** recs_dev_out);
+
+/* FP64 posterior of cells: mu_dev n*8, cov_dev n*64 (row-major 8x8), device. */
+lcp_status_t lcp_cell_posterior(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_t n,
+                                double* mu_dev, double* cov_dev);
+
+/* local marginal (mean, variance before the floor) at points xyz_dev (n x 3),
+ * using bucket bucket_dev[q] or, if bucket_dev == NULL, each point's own bucket. */
+lcp_status_t lcp_point_marginals(lcp_ctx_t* ctx, const double* xyz_dev, int64_t n,
+                                 const int32_t* bucket_dev, double* mu_dev, double* var_dev);
+
+/* the k-NN set of every bucket (nbuckets x k int32, ascending), device */
+lcp_status_t lcp_bucket_sets(lcp_ctx_t* ctx, int32_t* sets_dev);
+
+lcp_status_t lcp_get_info(lcp_ctx_t* ctx, lcp_info_t* out);
+
+/* JSON with per-phase device times and counters of the last calls */
+lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap);
+
+/* wait for all work queued on the ctx stream; reports deferred device errors */
+lcp_status_t lcp_synchronize(lcp_ctx_t* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCP_H */

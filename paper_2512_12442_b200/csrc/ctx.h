@@ -1,0 +1,153 @@
+// ctx.h -- host-side context of liblcp.so and the internal launch interface.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "lcp.h"
+
+namespace lcp {
+
+// grow-only device buffer (allocation happens only when a call needs more)
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  // grow keeping the first `used` bytes (stream-ordered copy)
+  cudaError_t ensure_keep(size_t bytes, size_t used, cudaStream_t s) {
+    if (bytes <= cap) return cudaSuccess;
+    size_t want = bytes + bytes / 2 + 256;
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, want);
+    if (e != cudaSuccess) return e;
+    if (p && used) {
+      e = cudaMemcpyAsync(q, p, used, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+      cudaStreamSynchronize(s);
+    }
+    if (p) cudaFree(p);
+    p = q;
+    cap = want;
+    return cudaSuccess;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct PhaseTimes {
+  double fit_ms = 0, refine_ms = 0, posterior_ms = 0, chol_ms = 0, mc_ms = 0, scatter_ms = 0;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int sm_count = 148;
+
+  // model (after fit)
+  bool fitted = false;
+  KernParams kp{};
+  Geom g{};
+  lcp_kernel_t kern{};
+  lcp_grid_t grid{};
+  lcp_opts_t opts{};
+  int64_t m = 0;
+  int k = 0;
+  int64_t bstride = 0;       // doubles per bucket block [Linv tri(k) | alpha k | Xs 3k], padded to 2
+  double kcc[36];            // prior covariance among the 8 corners of a cell (packed lower)
+
+  DevBuf X, y;               // observations, SoA x[m] y[m] z[m] / y[m]
+  DevBuf obs_bucket;         // int32 point bucket per obs
+  DevBuf bcount, bstart;     // per bucket observation counts / starts (int64)
+  DevBuf gcount, goff;       // group_by_bucket scratch (int64)
+  DevBuf obs_by_bucket;      // int32 observations grouped by bucket
+  DevBuf S;                  // int32 nbuckets x k (ascending)
+  DevBuf bdata;              // double nbuckets x bstride
+  DevBuf fscratch;           // factor scratch for large k
+  DevBuf obs_key, obs_sorted_key, obs_sorted_idx;  // Morton keys of the finest cell
+  DevBuf obs_mu, obs_sd;     // observation marginals (Morton order after fit)
+  DevBuf plo, phi;           // per-theta observation tails (Morton order)
+  DevBuf derr;               // device error flags (int)
+  DevBuf knn_fail;           // int: buckets whose ring search overflowed
+  int knn_fallbacks = 0;
+  int64_t n_vertices = 0;    // (nx+1)(ny+1)(nz+1)
+  int64_t last_requests = 0; // vertex marginals computed by the last refine
+
+  // octree state
+  DevBuf vcache;             // double2 (mu, sd) per grid vertex
+  DevBuf vstate;             // uint32 bitmask over grid vertices: marginal requested/ready
+  bool vcache_valid = false;
+  DevBuf front[2];           // uint64 node keys
+  DevBuf ncase, nref;        // per node of the level
+  DevBuf np1, np2, nU;       // per node of the level (double)
+  DevBuf cnt, offs;          // int64 per node: children / leaf counts and offsets
+  DevBuf scan_tmp;
+  DevBuf req, req_sorted;    // vertex requests
+  DevBuf counters;           // int64 device counters
+  DevBuf leaves;             // int64 leaf cell ids
+  int64_t n_leaves = 0;
+  DevBuf recs;               // lcp_node_rec_t
+  int64_t n_recs = 0;
+
+  // leaf pass scratch
+  DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
+
+  // host pinned staging for counters
+  int64_t* h_counters = nullptr;
+
+  // stats
+  PhaseTimes t;
+  std::vector<int64_t> level_nodes, level_refined, level_case[4];
+  int64_t last_pmc_cells = 0, last_pmc_samples = 0;
+  cudaEvent_t ev[8];
+  bool ev_init = false;
+};
+
+// ---- internal launchers (implemented in the .cu files) ----
+cudaError_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, int64_t* total_dev);
+cudaError_t group_by_bucket(Ctx& c, const int32_t* bucket_of_item, int64_t n, int64_t* perm_out);
+
+lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* y, int64_t m, int on_device,
+                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts);
+lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth);
+lcp_status_t pmc_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double theta, int64_t N,
+                      uint64_t seed, uint32_t iso, float* out_dev);
+lcp_status_t posterior_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double* post_dev);
+lcp_status_t point_marginals_impl(Ctx& c, const double* xyz_dev, int64_t n, const int32_t* bkt,
+                                  double* mu_dev, double* var_dev);
+lcp_status_t check_device_errors(Ctx& c);
+
+// marginals / posterior tile kernels (marginals.cu)
+enum QueryMode : int { Q_VERTEX = 0, Q_OBS = 1, Q_POINT = 2 };
+cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, const int32_t* item_bucket_sorted,
+                             int64_t n, const double* points, double* out_mu, double* out_sd_or_var,
+                             int write_var, const int64_t* n_dev);
+cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* perm,
+                                  const int32_t* bkt_sorted, int64_t n, double* post);
+
+lcp_status_t set_err(Ctx& c, lcp_status_t st, const std::string& msg);
+lcp_status_t cuda_err(Ctx& c, cudaError_t e, const char* where);
+
+}  // namespace lcp
+
+struct lcp_ctx {
+  lcp::Ctx c;
+};

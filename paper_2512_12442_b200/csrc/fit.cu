@@ -1,0 +1,549 @@
+// fit.cu -- lcp_fit_local: SURVEY §8(a) rows a1-a4.
+//
+//  a1  k_obs_bin / group_by_bucket / k_obs_rank : point -> bucket (R3), finest
+//      cell, Morton key of the finest cell, observations grouped by bucket and
+//      sorted by Morton key (for the node ranges of Alg. 1 line 3).
+//  a2  k_knn        : per bucket, the k nearest observations to the bucket centre
+//      in the metric sum_d ((x_d - c_d) / l_d)^2, ties -> lower index (R2); exact
+//      ring search over the bucket grid, brute-force fallback k_knn_brute.
+//  a3  k_bucket_factor : K_y = K_SS + sigma_n^2 I, Cholesky, L^-1 and
+//      alpha = K_y^-1 (y_S - m0) (Eq. 1; jitter R15).
+//  a4  observation marginals (R10) via k_marginals.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ctx.h"
+
+namespace lcp {
+
+constexpr int KNN_CMAX = 6144;
+constexpr int KNN_THREADS = 256;
+constexpr int FACT_THREADS = 256;
+
+template <typename T>
+__device__ T block_sum(T v, T* sh) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  T s = 0;
+  for (int w = 0; w < nw; ++w) s += sh[w];
+  return s;
+}
+
+// a1: point bucket, finest cell Morton key
+__global__ void k_obs_bin(Geom g, const double* __restrict__ X, int64_t m, int32_t* __restrict__ obs_bucket,
+                          uint64_t* __restrict__ obs_key) {
+  int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= m) return;
+  int bc[3], cc[3];
+  for (int d = 0; d < 3; ++d) {
+    double x = X[3 * o + d];
+    bc[d] = point_bucket_axis(g, d, x);
+    cc[d] = cell_axis(g, d, x);
+  }
+  obs_bucket[o] = bucket_id(g, bc[0], bc[1], bc[2]);
+  obs_key[o] = morton3(cc[0], cc[1], cc[2]);
+}
+
+__global__ void k_bucket_ranges(const int64_t* __restrict__ gcount, const int64_t* __restrict__ gend, int nb,
+                                int64_t* __restrict__ bcount, int64_t* __restrict__ bstart) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  bcount[b] = gcount[b];
+  bstart[b] = gend[b] - gcount[b];
+}
+
+__global__ void k_gather_i32(const int32_t* __restrict__ src, const int64_t* __restrict__ perm, int64_t n,
+                             int32_t* __restrict__ dst) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) dst[q] = src[perm[q]];
+}
+
+// a1: stable rank sort of the Morton keys (m is at most ~1e5: O(m^2 / P))
+__global__ void k_obs_rank(const uint64_t* __restrict__ key, int64_t m, uint64_t* __restrict__ skey,
+                           int32_t* __restrict__ sidx) {
+  __shared__ uint64_t tile[1024];
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t ki = i < m ? key[i] : 0;
+  int64_t rank = 0;
+  for (int64_t t0 = 0; t0 < m; t0 += 1024) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < 1024; q += blockDim.x)
+      tile[q] = t0 + q < m ? key[t0 + q] : ~0ull;
+    __syncthreads();
+    if (i < m) {
+      int n = (int)min((int64_t)1024, m - t0);
+      for (int q = 0; q < n; ++q) {
+        uint64_t kj = tile[q];
+        rank += (kj < ki) || (kj == ki && t0 + q < i);
+      }
+    }
+  }
+  if (i < m) {
+    skey[rank] = ki;
+    sidx[rank] = (int32_t)i;
+  }
+}
+
+// a2: exact k-NN by ring search over the bucket grid.  A ball of radius
+// R_out (the metric distance from the centre to the nearest face of the
+// searched box that is not the grid boundary) contains every observation
+// outside the box at distance >= R_out; the k-th candidate distance strictly
+// inside R_out (with a 1e-9 relative margin) proves the candidate set exact.
+__global__ void __launch_bounds__(KNN_THREADS) k_knn(KernParams kp, Geom g, const double* __restrict__ X,
+                                                     int64_t m, int k, const int64_t* __restrict__ bstart,
+                                                     const int64_t* __restrict__ bcount,
+                                                     const int64_t* __restrict__ obs_by_bucket,
+                                                     int32_t* __restrict__ S, int* __restrict__ fail_list,
+                                                     int* __restrict__ n_fail, int r0) {
+  extern __shared__ unsigned char sm_raw[];
+  double* cd2 = reinterpret_cast<double*>(sm_raw);
+  int32_t* cidx = reinterpret_cast<int32_t*>(cd2 + KNN_CMAX);
+  int32_t* sel = cidx + KNN_CMAX;
+  __shared__ long long s_red[32];
+  __shared__ int s_n;
+  __shared__ double s_d2k;
+  const int b = blockIdx.x;
+  int32_t* Sb = S + (int64_t)b * k;
+  if ((int64_t)k >= m) {
+    for (int a = threadIdx.x; a < k; a += blockDim.x) Sb[a] = a;
+    return;
+  }
+  int bc[3] = {b % g.nb[0], (b / g.nb[0]) % g.nb[1], b / (g.nb[0] * g.nb[1])};
+  double c[3];
+  for (int d = 0; d < 3; ++d) c[d] = __dadd_rn(g.lo[d], __dmul_rn((double)bc[d] + 0.5, g.sB[d]));
+  for (int r = r0;; ++r) {
+    __syncthreads();
+    int lo[3], hi[3], ext[3];
+    bool full = true;
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = max(bc[d] - r, 0);
+      hi[d] = min(bc[d] + r, g.nb[d] - 1);
+      ext[d] = hi[d] - lo[d] + 1;
+      full = full && lo[d] == 0 && hi[d] == g.nb[d] - 1;
+    }
+    int64_t nbox = (int64_t)ext[0] * ext[1] * ext[2];
+    long long cnt = 0;
+    for (int64_t t = threadIdx.x; t < nbox; t += blockDim.x) {
+      int ix = lo[0] + (int)(t % ext[0]), iy = lo[1] + (int)((t / ext[0]) % ext[1]),
+          iz = lo[2] + (int)(t / ((int64_t)ext[0] * ext[1]));
+      cnt += bcount[bucket_id(g, ix, iy, iz)];
+    }
+    cnt = block_sum(cnt, s_red);
+    if (cnt > KNN_CMAX) {
+      if (threadIdx.x == 0) fail_list[atomicAdd(n_fail, 1)] = b;
+      return;
+    }
+    if (cnt < k && !full) continue;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int64_t t = threadIdx.x; t < nbox; t += blockDim.x) {
+      int ix = lo[0] + (int)(t % ext[0]), iy = lo[1] + (int)((t / ext[0]) % ext[1]),
+          iz = lo[2] + (int)(t / ((int64_t)ext[0] * ext[1]));
+      int id = bucket_id(g, ix, iy, iz);
+      int64_t st = bstart[id], n = bcount[id];
+      for (int64_t q = 0; q < n; ++q) {
+        int64_t o = obs_by_bucket[st + q];
+        int pos = atomicAdd(&s_n, 1);
+        cidx[pos] = (int32_t)o;
+        cd2[pos] = knn_d2(kp, X + 3 * o, c);
+      }
+    }
+    __syncthreads();
+    const int n = s_n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double di = cd2[i];
+      int32_t ii = cidx[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        double dj = cd2[j];
+        rank += (dj < di) || (dj == di && cidx[j] < ii);
+      }
+      if (rank < k) sel[rank] = ii;
+      if (rank == k - 1) s_d2k = di;
+    }
+    __syncthreads();
+    if (!full) {
+      double rout2 = INFINITY;
+      for (int d = 0; d < 3; ++d) {
+        if (lo[d] > 0 || hi[d] < g.nb[d] - 1) {
+          double f = __dmul_rn(__dmul_rn((double)r + 0.5, g.sB[d]), kp.inv_ls[d]);
+          rout2 = fmin(rout2, f * f);
+        }
+      }
+      if (!(s_d2k < rout2 * (1.0 - 1e-9))) continue;
+    }
+    for (int a = threadIdx.x; a < k; a += blockDim.x) {
+      int32_t v = sel[a];
+      int rk = 0;
+      for (int q = 0; q < k; ++q) rk += sel[q] < v;
+      Sb[rk] = v;
+    }
+    return;
+  }
+}
+
+// a2 fallback: running top-k over all observations in chunks (exact, slow)
+__global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g, const double* __restrict__ X,
+                                                           int64_t m, int k, const int* __restrict__ list,
+                                                           int32_t* __restrict__ S) {
+  extern __shared__ unsigned char sm_raw[];
+  double* cd2 = reinterpret_cast<double*>(sm_raw);
+  int32_t* cidx = reinterpret_cast<int32_t*>(cd2 + KNN_CMAX);
+  int32_t* sel = cidx + KNN_CMAX;
+  double* seld = reinterpret_cast<double*>(sel + ((k + 1) & ~1));
+  const int b = list[blockIdx.x];
+  int bc[3] = {b % g.nb[0], (b / g.nb[0]) % g.nb[1], b / (g.nb[0] * g.nb[1])};
+  double c[3];
+  for (int d = 0; d < 3; ++d) c[d] = __dadd_rn(g.lo[d], __dmul_rn((double)bc[d] + 0.5, g.sB[d]));
+  int ntop = 0;
+  const int chunk = KNN_CMAX - k;
+  for (int64_t s0 = 0; s0 < m; s0 += chunk) {
+    int nn = (int)min((int64_t)chunk, m - s0);
+    for (int t = threadIdx.x; t < nn; t += blockDim.x) {
+      cidx[ntop + t] = (int32_t)(s0 + t);
+      cd2[ntop + t] = knn_d2(kp, X + 3 * (s0 + t), c);
+    }
+    __syncthreads();
+    int n = ntop + nn;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double di = cd2[i];
+      int32_t ii = cidx[i];
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        double dj = cd2[j];
+        rank += (dj < di) || (dj == di && cidx[j] < ii);
+      }
+      if (rank < k) { sel[rank] = ii; seld[rank] = di; }
+    }
+    __syncthreads();
+    ntop = min(k, n);
+    for (int t = threadIdx.x; t < ntop; t += blockDim.x) { cidx[t] = sel[t]; cd2[t] = seld[t]; }
+    __syncthreads();
+  }
+  int32_t* Sb = S + (int64_t)b * k;
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    int32_t v = cidx[a];
+    int rk = 0;
+    for (int q = 0; q < k; ++q) rk += cidx[q] < v;
+    Sb[rk] = v;
+  }
+}
+
+// a3: per-bucket factor.  Block layout in bdata: [L^-1 packed col-major (tri)]
+// [alpha (k)] [x (k)] [y (k)] [z (k)].
+__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, int k, const double* __restrict__ X,
+                                                                const double* __restrict__ yobs,
+                                                                const int32_t* __restrict__ S,
+                                                                double* __restrict__ bdata, int64_t bstride,
+                                                                double* __restrict__ gscratch, int use_smem,
+                                                                int* __restrict__ derr) {
+  extern __shared__ double sm[];
+  __shared__ int s_ok;
+  __shared__ double s_piv;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = bd >> 5;
+  const int64_t tri = tri_size(k);
+  double* sx = sm;
+  double* sy = sx + k;
+  double* sz = sy + k;
+  double* rr = sz + k;
+  double* vv = rr + k;
+  double* A;
+  double* Li;
+  if (use_smem) {
+    A = vv + k;
+    Li = A + tri;
+  } else {
+    A = gscratch + (int64_t)b * 2 * tri;
+    Li = A + tri;
+  }
+  const int32_t* Sb = S + (int64_t)b * k;
+  double* out = bdata + (int64_t)b * bstride;
+  for (int a = tid; a < k; a += bd) {
+    int64_t o = Sb[a];
+    sx[a] = X[3 * o];
+    sy[a] = X[3 * o + 1];
+    sz[a] = X[3 * o + 2];
+    rr[a] = yobs[o] - kp.m0;
+    out[tri + k + a] = sx[a];
+    out[tri + 2 * k + a] = sy[a];
+    out[tri + 3 * k + a] = sz[a];
+  }
+  bool ok = false;
+  for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+    double jit = attempt == 0 ? 0.0 : 1e-10 * kp.var * (attempt == 1 ? 1.0 : attempt == 2 ? 10.0 : 100.0);
+    __syncthreads();
+    for (int j = wid; j < k; j += nw) {
+      double* colj = A + tri_col(j, k) - j;
+      for (int i = j + lane; i < k; i += 32) {
+        double r2 = kern_r2(kp, sx[i] - sx[j], sy[i] - sy[j], sz[i] - sz[j]);
+        colj[i] = kern_from_r2(kp, r2) + (i == j ? kp.nugget + jit : 0.0);
+      }
+    }
+    if (tid == 0) s_ok = 1;
+    // right-looking Cholesky, column by column
+    for (int j = 0; j < k; ++j) {
+      __syncthreads();
+      double* colj = A + tri_col(j, k) - j;
+      if (tid == 0) {
+        double d = colj[j];
+        if (!(d > 0.0)) {
+          s_ok = 0;
+        } else {
+          d = sqrt(d);
+          colj[j] = d;
+          s_piv = d;
+        }
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      double piv = s_piv;
+      for (int i = j + 1 + tid; i < k; i += bd) colj[i] = colj[i] / piv;
+      __syncthreads();
+      for (int l = j + 1 + wid; l < k; l += nw) {
+        double* coll = A + tri_col(l, k) - l;
+        double ljl = colj[l];
+        for (int i = l + lane; i < k; i += 32) coll[i] = fma(-colj[i], ljl, coll[i]);
+      }
+    }
+    __syncthreads();
+    ok = s_ok != 0;
+  }
+  if (!ok) {
+    if (tid == 0) atomicOr(derr, DERR_FACTOR);
+    return;
+  }
+  // L^-1: column j solves L x = e_j by forward substitution (independent per column)
+  for (int j = tid; j < k; j += bd) {
+    double* Lc = Li + tri_col(j, k) - j;
+    Lc[j] = 1.0 / A[tri_col(j, k)];
+    for (int i = j + 1; i < k; ++i) {
+      double s0 = 0.0, s1 = 0.0;
+      int p = j;
+      for (; p + 1 < i; p += 2) {
+        s0 = fma(A[tri_col(p, k) + i - p], Lc[p], s0);
+        s1 = fma(A[tri_col(p + 1, k) + i - p - 1], Lc[p + 1], s1);
+      }
+      if (p < i) s0 = fma(A[tri_col(p, k) + i - p], Lc[p], s0);
+      Lc[i] = -(s0 + s1) / A[tri_col(i, k)];
+    }
+  }
+  __syncthreads();
+  // alpha = L^-T (L^-1 r)
+  for (int i = tid; i < k; i += bd) {
+    double s = 0.0;
+    for (int j = 0; j <= i; ++j) s = fma(Li[tri_col(j, k) + i - j], rr[j], s);
+    vv[i] = s;
+  }
+  __syncthreads();
+  for (int j = tid; j < k; j += bd) {
+    const double* Lc = Li + tri_col(j, k) - j;
+    double s = 0.0;
+    for (int i = j; i < k; ++i) s = fma(Lc[i], vv[i], s);
+    out[tri + j] = s;
+  }
+  for (int64_t e = tid; e < tri; e += bd) out[e] = Li[e];
+}
+
+// ------------------------------------------------------------------- host
+static int ilog2_ceil(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+
+static double host_kern(const KernParams& p, const double* a, const double* b) {
+  double r2 = 0.0;
+  for (int d = 0; d < 3; ++d) {
+    double t = (a[d] - b[d]) * p.inv_ls[d];
+    r2 += t * t;
+  }
+  if (p.kind == LCP_K_SE) return p.var * std::exp(-0.5 * r2);
+  double r = std::sqrt(r2), s = SQRT5 * r;
+  return p.var * (1.0 + s + (5.0 / 3.0) * r2) * std::exp(-s);
+}
+
+lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, int on_device,
+                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts) {
+  if (!xyz || !yv || !kern || !grid) return set_err(c, LCP_EINVAL, "fit: null argument");
+  if (m < 1 || k < 1 || (int64_t)k > m) return set_err(c, LCP_EINVAL, "fit: need 1 <= k <= m");
+  if (k > 1024 && (int64_t)k != m) return set_err(c, LCP_EINVAL, "fit: k > 1024 requires k == m");
+  if (!(kern->variance > 0) || !(kern->nugget >= 0) || (kern->kind != LCP_K_SE && kern->kind != LCP_K_MATERN52))
+    return set_err(c, LCP_EINVAL, "fit: bad kernel parameters");
+  for (int d = 0; d < 3; ++d)
+    if (!(kern->lengthscale[d] > 0) || grid->cells[d] < 1 || !(grid->hi[d] > grid->lo[d]) || grid->cells[d] > (1 << 20))
+      return set_err(c, LCP_EINVAL, "fit: bad lengthscale or grid");
+  lcp_opts_t o{};
+  o.bucket_log2 = 0;
+  o.h_full = 2;
+  o.precision = LCP_FP64;
+  o.slab_rank = 0;
+  o.slab_count = 1;
+  o.slab_level = 3;
+  o.keep_records = 0;
+  if (opts) o = *opts;
+  if (o.slab_count < 1) o.slab_count = 1;
+  int cmax = std::max(grid->cells[0], std::max(grid->cells[1], grid->cells[2]));
+  int lfull = ilog2_ceil(cmax);
+  if (o.bucket_log2 < 0 || o.bucket_log2 > lfull || o.h_full < 0 || o.slab_rank < 0 ||
+      o.slab_rank >= o.slab_count)
+    return set_err(c, LCP_EINVAL, "fit: bad options (bucket_log2 / h_full / slab)");
+  if (o.slab_count > 1 && (o.slab_level < 1 || o.slab_level > lfull))
+    return set_err(c, LCP_EINVAL, "fit: slab_level must be in [1, Lfull] when slab_count > 1");
+
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, c.stream);
+
+  c.fitted = false;
+  c.vcache_valid = false;
+  c.kern = *kern;
+  c.grid = *grid;
+  c.opts = o;
+  c.m = m;
+  c.k = k;
+  KernParams& kp = c.kp;
+  kp.kind = kern->kind;
+  kp.var = kern->variance;
+  for (int d = 0; d < 3; ++d) kp.inv_ls[d] = 1.0 / kern->lengthscale[d];
+  kp.nugget = kern->nugget;
+  kp.m0 = kern->prior_mean;
+  Geom& g = c.g;
+  g.lfull = lfull;
+  g.bs_log2 = lfull - o.bucket_log2;
+  g.bs = 1 << g.bs_log2;
+  g.h_full = o.h_full;
+  for (int d = 0; d < 3; ++d) {
+    g.lo[d] = grid->lo[d];
+    g.cells[d] = grid->cells[d];
+    g.h[d] = (grid->hi[d] - grid->lo[d]) / (double)grid->cells[d];
+    g.sB[d] = (double)g.bs * g.h[d];
+    g.nb[d] = (grid->cells[d] + g.bs - 1) / g.bs;
+  }
+  g.nbuckets = g.nb[0] * g.nb[1] * g.nb[2];
+  // prior covariance among the 8 corners (depends on h only)
+  for (int cc = 0; cc < 8; ++cc)
+    for (int dd = 0; dd <= cc; ++dd) {
+      double a[3] = {(cc & 1) * g.h[0], ((cc >> 1) & 1) * g.h[1], (cc >> 2) * g.h[2]};
+      double b[3] = {(dd & 1) * g.h[0], ((dd >> 1) & 1) * g.h[1], (dd >> 2) * g.h[2]};
+      c.kcc[cc * (cc + 1) / 2 + dd] = host_kern(kp, a, b);
+    }
+  int64_t tri = tri_size(k);
+  c.bstride = (tri + 4 * (int64_t)k + 1) & ~1ll;
+  const int nbk = g.nbuckets;
+
+  cudaError_t e;
+#define CK(x)                                  \
+  do {                                         \
+    e = (x);                                   \
+    if (e != cudaSuccess) return cuda_err(c, e, #x); \
+  } while (0)
+  CK(c.X.ensure(sizeof(double) * 3 * m));
+  CK(c.y.ensure(sizeof(double) * m));
+  CK(c.obs_bucket.ensure(sizeof(int32_t) * m));
+  CK(c.obs_key.ensure(sizeof(uint64_t) * m));
+  CK(c.obs_sorted_key.ensure(sizeof(uint64_t) * m));
+  CK(c.obs_sorted_idx.ensure(sizeof(int32_t) * m));
+  CK(c.obs_by_bucket.ensure(sizeof(int64_t) * m));
+  CK(c.bcount.ensure(sizeof(int64_t) * nbk));
+  CK(c.bstart.ensure(sizeof(int64_t) * nbk));
+  CK(c.S.ensure(sizeof(int32_t) * (size_t)nbk * k));
+  CK(c.bdata.ensure(sizeof(double) * (size_t)nbk * c.bstride));
+  CK(c.obs_mu.ensure(sizeof(double) * m));
+  CK(c.obs_sd.ensure(sizeof(double) * m));
+  CK(c.derr.ensure(sizeof(int) * 4));
+  CK(c.knn_fail.ensure(sizeof(int) * (nbk + 1)));
+  CK(c.cell_bucket.ensure(sizeof(int32_t) * m));
+  CK(cudaMemsetAsync(c.derr.p, 0, sizeof(int) * 4, c.stream));
+  if (on_device) {
+    CK(cudaMemcpyAsync(c.X.p, xyz, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.y.p, yv, sizeof(double) * m, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    CK(cudaMemcpyAsync(c.X.p, xyz, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, c.stream));
+    CK(cudaMemcpyAsync(c.y.p, yv, sizeof(double) * m, cudaMemcpyHostToDevice, c.stream));
+  }
+  const double* X = c.X.as<double>();
+  unsigned gm = (unsigned)((m + 255) / 256);
+  // a1
+  k_obs_bin<<<gm, 256, 0, c.stream>>>(g, X, m, c.obs_bucket.as<int32_t>(), c.obs_key.as<uint64_t>());
+  CK(group_by_bucket(c, c.obs_bucket.as<int32_t>(), m, c.obs_by_bucket.as<int64_t>()));
+  k_bucket_ranges<<<(nbk + 255) / 256, 256, 0, c.stream>>>(c.gcount.as<int64_t>(), c.goff.as<int64_t>(), nbk,
+                                                          c.bcount.as<int64_t>(), c.bstart.as<int64_t>());
+  k_obs_rank<<<gm, 256, 0, c.stream>>>(c.obs_key.as<uint64_t>(), m, c.obs_sorted_key.as<uint64_t>(),
+                                      c.obs_sorted_idx.as<int32_t>());
+  CK(cudaGetLastError());
+  // a2
+  {
+    int r0 = 0;
+    double dens = (double)m / nbk;
+    while (r0 < 64 && std::pow(2.0 * r0 + 1.0, 3) * dens < (double)k) ++r0;
+    size_t smem = sizeof(double) * KNN_CMAX + sizeof(int32_t) * KNN_CMAX + sizeof(int32_t) * (k + 2) +
+                  sizeof(double) * (k + 1);
+    CK(cudaFuncSetAttribute(k_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_knn_brute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int* nfail_dev = c.knn_fail.as<int>();
+    int* list_dev = nfail_dev + 1;
+    CK(cudaMemsetAsync(nfail_dev, 0, sizeof(int), c.stream));
+    k_knn<<<nbk, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, c.bstart.as<int64_t>(), c.bcount.as<int64_t>(),
+                                              c.obs_by_bucket.as<int64_t>(), c.S.as<int32_t>(), list_dev,
+                                              nfail_dev, r0);
+    CK(cudaGetLastError());
+    int nfail = 0;
+    CK(cudaMemcpyAsync(&nfail, nfail_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.knn_fallbacks = nfail;
+    if (nfail > 0) {
+      k_knn_brute<<<nfail, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, list_dev, c.S.as<int32_t>());
+      CK(cudaGetLastError());
+    }
+  }
+  // a3
+  {
+    size_t head = sizeof(double) * 5 * (size_t)k;
+    size_t full = head + sizeof(double) * 2 * (size_t)tri;
+    int use_smem = full <= 200 * 1024;
+    size_t smem = use_smem ? full : head;
+    double* gs = nullptr;
+    if (!use_smem) {
+      CK(c.fscratch.ensure(sizeof(double) * 2 * (size_t)tri * nbk));
+      gs = c.fscratch.as<double>();
+    }
+    CK(cudaFuncSetAttribute(k_bucket_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_bucket_factor<<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                           c.bdata.as<double>(), c.bstride, gs, use_smem,
+                                                           c.derr.as<int>());
+    CK(cudaGetLastError());
+  }
+  // a4: observation marginals (grouped by bucket)
+  k_gather_i32<<<gm, 256, 0, c.stream>>>(c.obs_bucket.as<int32_t>(), c.obs_by_bucket.as<int64_t>(), m,
+                                         c.cell_bucket.as<int32_t>());
+  CK(launch_marginals(c, Q_OBS, c.obs_by_bucket.as<int64_t>(), c.cell_bucket.as<int32_t>(), m, X,
+                      c.obs_mu.as<double>(), c.obs_sd.as<double>(), 0, nullptr));
+  cudaEventRecord(e1, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  c.t.fit_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  lcp_status_t st = check_device_errors(c);
+  if (st != LCP_OK) return st;
+  // the vertex cache covers every grid vertex
+  int64_t nv = (int64_t)(g.cells[0] + 1) * (g.cells[1] + 1) * (g.cells[2] + 1);
+  c.n_vertices = nv;
+  CK(c.vcache.ensure(sizeof(double2) * nv));
+  CK(c.vstate.ensure(sizeof(uint32_t) * ((nv + 31) / 32)));
+  CK(cudaMemsetAsync(c.vstate.p, 0, sizeof(uint32_t) * ((nv + 31) / 32), c.stream));
+  c.vcache_valid = true;
+  c.fitted = true;
+#undef CK
+  return LCP_OK;
+}
+
+}  // namespace lcp

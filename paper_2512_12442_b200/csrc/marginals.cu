@@ -1,0 +1,374 @@
+// marginals.cu -- bucket-tiled local-GP posterior kernels.
+//
+// Eq. 1 on the bucket's local GP (R1, R2): for query points
+// q_1..q_8 sharing bucket B with observations S_B, factor L_B (K_y = L L^T) and
+// alpha_B = K_y^-1 (y_S - m0):
+//     mu_c    = m0 + sum_j K(x_j, q_c) alpha_j
+//     V       = L^-1 K_{S,q}            (k x 8, triangular mat-mat)
+//     Sigma   = K_qq - V^T V
+// One warp handles 8 queries: the 8 corners of a cell (leaf pass, a7) or 8
+// independent points (vertex / observation marginals, a4-a5).  A CTA stages the
+// bucket block [L^-1 | alpha | X_S] into shared memory once and all its warps
+// reuse it; work lists are grouped by bucket (scan.cu) so restaging is rare.
+#include "ctx.h"
+
+namespace lcp {
+
+constexpr int TILE_WARPS_MAX = 16;
+constexpr int ROWS_PER_GROUP = 128;   // 4 row blocks of 32 per lane pass
+
+struct TileArgs {
+  KernParams kp;
+  Geom g;
+  int k;
+  int staged;            // L^-1 staged in shared memory
+  int64_t bstride;       // doubles per bucket block
+  const double* bdata;   // [L^-1 packed col-major | alpha | x | y | z] per bucket
+  double kcc[36];        // prior covariance of the 8 cell corners (packed lower, row-major pairs)
+  double var_floor;      // 1e-12 sigma_f^2
+  double var_err;        // -1e-8 sigma_f^2
+};
+
+// all threads copy n doubles (16-byte aligned) global -> shared
+__device__ __forceinline__ void stage_copy(double* dst, const double* __restrict__ src, int64_t n) {
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  int64_t n2 = n >> 1;
+  for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) d2[i] = __ldg(s2 + i);
+  if ((n & 1) && threadIdx.x == 0) dst[n - 1] = __ldg(src + n - 1);
+}
+
+// V rows of group g:  v[rb][c] = sum_{j <= i} Linv[i][j] K[j][c],  i = row0 + 32 rb + lane.
+__device__ __forceinline__ void trmv8_group(const double* __restrict__ Linv, int k, int row0,
+                                            const double* __restrict__ sK, double (&v)[4][8], int lane) {
+#pragma unroll
+  for (int rb = 0; rb < 4; ++rb)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[rb][c] = 0.0;
+  int nrows = min(ROWS_PER_GROUP, k - row0);
+  int nrb = (nrows + 31) >> 5;
+  int jend = row0 + nrows;
+  const double2* sK2 = reinterpret_cast<const double2*>(sK);
+  for (int j = 0; j < jend; ++j) {
+    double2 a0 = sK2[4 * j + 0], a1 = sK2[4 * j + 1], a2 = sK2[4 * j + 2], a3 = sK2[4 * j + 3];
+    double kj[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
+    const double* col = Linv + tri_col(j, k) - j;   // col[i] = Linv[i][j]
+    int rb_lo = j < row0 ? 0 : ((j - row0) >> 5);
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      if (rb < rb_lo || rb >= nrb) continue;   // warp-uniform
+      int i = row0 + 32 * rb + lane;
+      double l = (i >= j && i < k) ? col[i] : 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[rb][c] = fma(l, kj[c], v[rb][c]);
+    }
+  }
+}
+
+// Warp computes, for its 8 queries (positions in sQ[8][3]):
+//   mu  -> returned in lane c (c < 8) as mu_out
+//   pair sums sum_i V[i][c] V[i][d] for pair p = lane (and lane + 32 < 36) in pair_out[0..1]
+// pairs: all 36 (cov) or the 8 diagonals (diag_only; pair p < 8 is (p,p)).
+__device__ __forceinline__ void warp_local_posterior(const TileArgs& a, const double* __restrict__ Linv,
+                                                     const double* __restrict__ alpha,
+                                                     const double* __restrict__ Xs,
+                                                     const double* __restrict__ sQ, double* sK, double* sV,
+                                                     bool diag_only, double& mu_out, double (&pair_out)[2]) {
+  const int k = a.k;
+  const int lane = threadIdx.x & 31;
+  // 1. K[j][c] = k(x_j, q_c)
+  for (int j = lane; j < k; j += 32) {
+    double xj = Xs[j], yj = Xs[k + j], zj = Xs[2 * k + j];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      double r2 = kern_r2(a.kp, xj - sQ[3 * c], yj - sQ[3 * c + 1], zj - sQ[3 * c + 2]);
+      sK[8 * j + c] = kern_from_r2(a.kp, r2);
+    }
+  }
+  __syncwarp();
+  // 2. mu_c = m0 + sum_j K[j][c] alpha_j   (lane: c = lane & 7, part = lane >> 3)
+  {
+    int c = lane & 7, part = lane >> 3;
+    double s = 0.0;
+    for (int j = part; j < k; j += 4) s = fma(sK[8 * j + c], alpha[j], s);
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    mu_out = a.kp.m0 + s;
+  }
+  // 3. V = L^-1 K, 4. pair sums of V^T V
+  int p0 = lane, p1 = lane + 32;
+  int c0, d0, c1 = 0, d1 = 0;
+  if (diag_only) {
+    c0 = d0 = lane & 7;
+  } else {
+    // p = c (c + 1) / 2 + d, d <= c
+    c0 = (int)((sqrt(8.0 * p0 + 1.0) - 1.0) * 0.5);
+    d0 = p0 - c0 * (c0 + 1) / 2;
+    if (p1 < 36) {
+      c1 = (int)((sqrt(8.0 * p1 + 1.0) - 1.0) * 0.5);
+      d1 = p1 - c1 * (c1 + 1) / 2;
+    }
+  }
+  double acc0 = 0.0, acc1 = 0.0;
+  const bool single = k <= ROWS_PER_GROUP;
+  for (int row0 = 0; row0 < k; row0 += ROWS_PER_GROUP) {
+    double v[4][8];
+    trmv8_group(Linv, k, row0, sK, v, lane);
+    double* dst = single ? sK : sV;   // single group: K is dead, reuse its buffer
+    __syncwarp();
+    int nrows = min(ROWS_PER_GROUP, k - row0);
+#pragma unroll
+    for (int rb = 0; rb < 4; ++rb) {
+      int r = 32 * rb + lane;
+      if (r < nrows) {
+        double2* d2 = reinterpret_cast<double2*>(dst + 8 * r);
+        d2[0] = make_double2(v[rb][0], v[rb][1]);
+        d2[1] = make_double2(v[rb][2], v[rb][3]);
+        d2[2] = make_double2(v[rb][4], v[rb][5]);
+        d2[3] = make_double2(v[rb][6], v[rb][7]);
+      }
+    }
+    __syncwarp();
+    if (diag_only ? lane < 8 : true) {
+      for (int r = 0; r < nrows; ++r) acc0 = fma(dst[8 * r + c0], dst[8 * r + d0], acc0);
+    }
+    if (!diag_only && p1 < 36) {
+      for (int r = 0; r < nrows; ++r) acc1 = fma(dst[8 * r + c1], dst[8 * r + d1], acc1);
+    }
+    __syncwarp();
+  }
+  pair_out[0] = acc0;
+  pair_out[1] = acc1;
+}
+
+__device__ __forceinline__ int item_bucket(const TileArgs& a, int mode, int64_t item, const double* pts,
+                                           const int32_t* bkt_sorted, int64_t q) {
+  if (bkt_sorted) return bkt_sorted[q];
+  if (mode == Q_VERTEX) return vertex_bucket(a.g, item);
+  return cell_bucket(a.g, item);
+}
+
+// Generic tile loop: CTA handles sorted positions [t0, t1); runs of equal bucket
+// share one staging of the bucket block.
+template <typename Body>
+__device__ __forceinline__ void tile_loop(const TileArgs& a, int64_t t0, int64_t t1, double* smem,
+                                          const int32_t* __restrict__ runb, Body body) {
+  __shared__ int s_run_end;
+  __shared__ int s_bucket;
+  const int64_t blk = a.bstride;
+  int staged_bucket = -1;
+  int64_t q = t0;
+  while (q < t1) {
+    if (threadIdx.x == 0) {
+      int b = runb[q];
+      int64_t e = q + 1;
+      while (e < t1 && runb[e] == b) ++e;
+      s_run_end = (int)(e - t0);
+      s_bucket = b;
+    }
+    __syncthreads();
+    int b = s_bucket;
+    int64_t qe = t0 + s_run_end;
+    if (b != staged_bucket) {
+      const double* src = a.bdata + (int64_t)b * blk;
+      int64_t tri = tri_size(a.k);
+      if (a.staged) stage_copy(smem, src, blk);
+      else stage_copy(smem, src + tri, 4 * (int64_t)a.k);
+      staged_bucket = b;
+    }
+    __syncthreads();
+    const double* Linv = a.staged ? smem : a.bdata + (int64_t)b * blk;
+    const double* tail = a.staged ? smem + tri_size(a.k) : smem;
+    body(b, q, qe, Linv, tail, tail + a.k);
+    __syncthreads();
+    q = qe;
+  }
+}
+
+// ---------------------------------------------------------------- a4 / a5
+// items_sorted[q]: vertex id (Q_VERTEX), observation index (Q_OBS) or point
+// index (Q_POINT); bkt_sorted[q]: its bucket.  Output indexed by the item
+// (vertex cache slot, observation, point).
+__global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const int64_t* __restrict__ items,
+                                                   const int32_t* __restrict__ bkt_sorted, int64_t n,
+                                                   const int64_t* __restrict__ n_dev, int tile,
+                                                   const double* __restrict__ pts, double* __restrict__ out_mu,
+                                                   double* __restrict__ out_sd, int write_var,
+                                                   double2* __restrict__ vcache, uint8_t* __restrict__ vstate,
+                                                   int* __restrict__ derr) {
+  extern __shared__ double smem[];
+  if (n_dev) n = *n_dev;
+  int64_t t0 = (int64_t)blockIdx.x * tile;
+  if (t0 >= n) return;
+  int64_t t1 = min(n, t0 + tile);
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
+  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  head = (head + 1) & ~1ll;
+  const int64_t per_warp = 8 * (int64_t)k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
+  double* wbuf = smem + head + wid * per_warp;
+  double* sK = wbuf;
+  double* sV = wbuf + 8 * k;
+  double* sQ = wbuf + per_warp - 24;
+  const Geom& g = a.g;
+  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
+                                              const double* alpha, const double* Xs) {
+    for (int64_t base = q0 + 8 * wid; base < q1; base += 8 * warps) {
+      int nq = (int)min((int64_t)8, q1 - base);
+      if (lane < 8) {
+        int64_t it = items[base + (lane < nq ? lane : 0)];
+        double x, y, z;
+        if (mode == Q_VERTEX) {
+          int i, j, kk;
+          vertex_ijk(g, it, i, j, kk);
+          x = vpos(g, 0, i); y = vpos(g, 1, j); z = vpos(g, 2, kk);
+        } else {
+          x = pts[3 * it]; y = pts[3 * it + 1]; z = pts[3 * it + 2];
+        }
+        sQ[3 * lane] = x; sQ[3 * lane + 1] = y; sQ[3 * lane + 2] = z;
+      }
+      __syncwarp();
+      double mu, pr[2];
+      warp_local_posterior(a, Linv, alpha, Xs, sQ, sK, sV, true, mu, pr);
+      if (lane < nq) {
+        int64_t it = items[base + lane];
+        double var = a.kp.var - pr[0];   // k(q,q) = sigma_f^2 for both kernels
+        if (var < a.var_err) atomicOr(derr, DERR_NUMERIC);
+        double vf = var > a.var_floor ? var : a.var_floor;
+        if (mode == Q_VERTEX) {
+          vcache[it] = make_double2(mu, sqrt(vf));
+        } else {
+          out_mu[it] = mu;
+          out_sd[it] = write_var ? var : sqrt(vf);
+        }
+      }
+      __syncwarp();
+    }
+  });
+}
+
+// ------------------------------------------------------------------- a7
+// post[q] (44 doubles): mu[8] then Sigma packed lower (pair p = c(c+1)/2 + d).
+__global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_t* __restrict__ cells,
+                                                        const int64_t* __restrict__ perm,
+                                                        const int32_t* __restrict__ bkt_sorted, int64_t n,
+                                                        int tile, double* __restrict__ post,
+                                                        int* __restrict__ derr) {
+  extern __shared__ double smem[];
+  int64_t t0 = (int64_t)blockIdx.x * tile;
+  if (t0 >= n) return;
+  int64_t t1 = min(n, t0 + tile);
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
+  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  head = (head + 1) & ~1ll;
+  const int64_t per_warp = 8 * (int64_t)k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
+  double* wbuf = smem + head + wid * per_warp;
+  double* sK = wbuf;
+  double* sV = wbuf + 8 * k;
+  double* sQ = wbuf + per_warp - 24;
+  const Geom& g = a.g;
+  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
+                                              const double* alpha, const double* Xs) {
+    for (int64_t q = q0 + wid; q < q1; q += warps) {
+      int64_t slot = perm ? perm[q] : q;
+      int64_t cell = cells[slot];
+      int ci, cj, ck;
+      cell_ijk(g, cell, ci, cj, ck);
+      if (lane < 8) {
+        sQ[3 * lane] = vpos(g, 0, ci + (lane & 1));
+        sQ[3 * lane + 1] = vpos(g, 1, cj + ((lane >> 1) & 1));
+        sQ[3 * lane + 2] = vpos(g, 2, ck + (lane >> 2));
+      }
+      __syncwarp();
+      double mu, pr[2];
+      warp_local_posterior(a, Linv, alpha, Xs, sQ, sK, sV, false, mu, pr);
+      double* rec = post + 44 * slot;
+      if (lane < 8) rec[lane] = mu;
+      double s0 = a.kcc[lane] - pr[0];
+      rec[8 + lane] = s0;
+      // diagonal pairs are p = c (c + 3) / 2: 0 2 5 9 14 20 27 | 35
+      bool diag0 = lane == 0 || lane == 2 || lane == 5 || lane == 9 || lane == 14 || lane == 20 || lane == 27;
+      if (diag0 && s0 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      if (lane < 4) {
+        double s1 = a.kcc[32 + lane] - pr[1];
+        rec[8 + 32 + lane] = s1;
+        if (lane == 3 && s1 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      }
+      __syncwarp();
+    }
+  });
+}
+
+static TileArgs make_tile_args(Ctx& c) {
+  TileArgs a;
+  a.kp = c.kp;
+  a.g = c.g;
+  a.k = c.k;
+  a.bstride = c.bstride;
+  a.bdata = c.bdata.as<double>();
+  for (int p = 0; p < 36; ++p) a.kcc[p] = c.kcc[p];
+  a.var_floor = 1e-12 * c.kp.var;
+  a.var_err = -1e-8 * c.kp.var;
+  a.staged = 0;
+  return a;
+}
+
+// shared-memory plan: staged bucket block (if it fits) + W per-warp buffers
+static void plan_tile(const Ctx& c, int& staged, int& warps, size_t& smem) {
+  const size_t cap = 220 * 1024;
+  int64_t k = c.k;
+  size_t per_warp = sizeof(double) * (8 * k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24);
+  size_t head_staged = sizeof(double) * ((c.bstride + 1) & ~1ll);
+  size_t head_tail = sizeof(double) * (4 * k + 1);
+  staged = 0;
+  warps = 0;
+  for (int w = TILE_WARPS_MAX; w >= 4; w -= 4) {
+    if (head_staged + w * per_warp <= cap) { staged = 1; warps = w; break; }
+  }
+  if (!staged) {
+    for (int w = TILE_WARPS_MAX; w >= 1; --w)
+      if (head_tail + w * per_warp <= cap) { warps = w; break; }
+    smem = head_tail + warps * per_warp;
+  } else {
+    smem = head_staged + warps * per_warp;
+  }
+}
+
+cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, const int32_t* bkt_sorted,
+                             int64_t n, const double* points, double* out_mu, double* out_sd,
+                             int write_var, const int64_t* n_dev) {
+  if (n <= 0) return cudaSuccess;
+  TileArgs a = make_tile_args(c);
+  int staged, warps;
+  size_t smem;
+  plan_tile(c, staged, warps, smem);
+  if (warps == 0) return cudaErrorInvalidConfiguration;
+  a.staged = staged;
+  cudaFuncSetAttribute(k_marginals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int tile = 8 * warps * 4;
+  unsigned grid = (unsigned)((n + tile - 1) / tile);
+  k_marginals<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
+                                                    out_mu, out_sd, write_var, c.vcache.as<double2>(),
+                                                    c.vstate.as<uint8_t>(), c.derr.as<int>());
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* perm,
+                                  const int32_t* bkt_sorted, int64_t n, double* post) {
+  if (n <= 0) return cudaSuccess;
+  TileArgs a = make_tile_args(c);
+  int staged, warps;
+  size_t smem;
+  plan_tile(c, staged, warps, smem);
+  if (warps == 0) return cudaErrorInvalidConfiguration;
+  a.staged = staged;
+  cudaFuncSetAttribute(k_cell_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int tile = warps * 16;
+  unsigned grid = (unsigned)((n + tile - 1) / tile);
+  k_cell_posterior<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
+                                                         c.derr.as<int>());
+  return cudaGetLastError();
+}
+
+}  // namespace lcp

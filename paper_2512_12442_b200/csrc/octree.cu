@@ -1,0 +1,398 @@
+// octree.cu -- lcp_octree_refine: SURVEY §8(a) rows a5-a6.
+//
+// Alg. 1 run level-synchronously: the frontier of level L
+// is a Morton-ordered array of node keys; every node is evaluated by one warp:
+//   k_node_prelim : M~ = observations in the node (a contiguous range of the
+//                   Morton-sorted observations), p1 = max P(Y_i < th),
+//                   p2 = max P(Y_i > th) (lines 3-5), the case
+//                   (R8, R9) and, unless case 1, requests for the candidate
+//                   lattice vertices (R6) whose marginals are not cached yet;
+//   k_marginals   : local-GP marginals of the requested vertices (marginals.cu);
+//   k_node_bound  : B_l, B_u over the lattice and U = 1 - B_l^d - B_u^d in log
+//                   space (Eq. 3-4; R7, R9);
+//   k_node_counts / exclusive scan / k_emit : stream compaction of the refined
+//                   nodes into the next frontier (8 children in Morton order,
+//                   lines 14-21) or, at max depth, into the leaf-cell list (line 13).
+#include <algorithm>
+#include <cmath>
+
+#include "ctx.h"
+
+namespace lcp {
+
+struct Lattice {
+  int64_t base[3], vmax[3], stride;
+  int cnt[3];
+};
+
+__device__ __forceinline__ Lattice node_lattice(const Geom& g, int h, int i, int j, int k) {
+  Lattice L;
+  int a[3] = {i, j, k};
+  int st = h - g.h_full > 0 ? h - g.h_full : 0;
+  L.stride = (int64_t)1 << st;
+  for (int d = 0; d < 3; ++d) {
+    L.base[d] = (int64_t)a[d] << h;
+    int64_t e = L.base[d] + ((int64_t)1 << h);
+    L.vmax[d] = e < g.cells[d] ? e : g.cells[d];
+    L.cnt[d] = (int)((L.vmax[d] - L.base[d] + L.stride - 1) / L.stride) + 1;
+  }
+  return L;
+}
+
+__device__ __forceinline__ int64_t lattice_vertex(const Geom& g, const Lattice& L, int64_t q) {
+  int t0 = (int)(q % L.cnt[0]);
+  int64_t r = q / L.cnt[0];
+  int t1 = (int)(r % L.cnt[1]);
+  int t2 = (int)(r / L.cnt[1]);
+  int64_t v0 = t0 < L.cnt[0] - 1 ? L.base[0] + t0 * L.stride : L.vmax[0];
+  int64_t v1 = t1 < L.cnt[1] - 1 ? L.base[1] + t1 * L.stride : L.vmax[1];
+  int64_t v2 = t2 < L.cnt[2] - 1 ? L.base[2] + t2 * L.stride : L.vmax[2];
+  return vertex_id(g, v0, v1, v2);
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t n, uint64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// a4 per isovalue: tails of the observation marginals, Morton order
+__global__ void k_obs_probs(const int32_t* __restrict__ sidx, const double* __restrict__ mu,
+                            const double* __restrict__ sd, int64_t m, double theta, double* __restrict__ plo,
+                            double* __restrict__ phi) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  int o = sidx[r];
+  double s2 = sd[o] * SQRT2;
+  plo[r] = 0.5 * erfc((mu[o] - theta) / s2);
+  phi[r] = 0.5 * erfc((theta - mu[o]) / s2);
+}
+
+__global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF,
+                              const uint64_t* __restrict__ skey, const double* __restrict__ plo,
+                              const double* __restrict__ phi, int64_t m, double alpha,
+                              int8_t* __restrict__ ncase, int8_t* __restrict__ nref, double* __restrict__ np1,
+                              double* __restrict__ np2, double* __restrict__ nU, uint32_t* __restrict__ vmask,
+                              int64_t* __restrict__ req, unsigned long long* __restrict__ nreq) {
+  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (n >= nF) return;
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  int h = g.lfull - level;
+  uint64_t mk = morton3(i, j, k);
+  int64_t a = 0, b = 0;
+  if (lane == 0) {
+    a = lower_bound_u64(skey, m, mk << (3 * h));
+    b = lower_bound_u64(skey, m, (mk + 1) << (3 * h));
+  }
+  a = __shfl_sync(0xffffffffu, a, 0);
+  b = __shfl_sync(0xffffffffu, b, 0);
+  double p1 = -1.0, p2 = -1.0;
+  for (int64_t r = a + lane; r < b; r += 32) {
+    p1 = fmax(p1, plo[r]);
+    p2 = fmax(p2, phi[r]);
+  }
+  p1 = warp_max(p1);
+  p2 = warp_max(p2);
+  bool any = b > a;
+  int cs = !any ? 0 : ((p1 > alpha && p2 > alpha) ? 1 : (p2 <= alpha ? 2 : 3));
+  if (lane == 0) {
+    ncase[n] = (int8_t)cs;
+    np1[n] = p1;
+    np2[n] = p2;
+    if (cs == 1) {
+      nref[n] = 1;
+      nU[n] = 1.0;
+    }
+  }
+  if (cs == 1) return;
+  Lattice L = node_lattice(g, h, i, j, k);
+  int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
+  for (int64_t q = lane; q < nc; q += 32) {
+    int64_t v = lattice_vertex(g, L, q);
+    uint32_t bit = 1u << (v & 31);
+    if (vmask[v >> 5] & bit) continue;
+    uint32_t old = atomicOr(&vmask[v >> 5], bit);
+    if (!(old & bit)) req[atomicAdd(nreq, 1ull)] = v;
+  }
+}
+
+__global__ void k_req_bucket(Geom g, const int64_t* __restrict__ req, int64_t n, int32_t* __restrict__ bkt) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) bkt[q] = vertex_bucket(g, req[q]);
+}
+
+__global__ void k_gather_req(const int64_t* __restrict__ req, const int32_t* __restrict__ bkt,
+                             const int64_t* __restrict__ perm, int64_t n, int64_t* __restrict__ req_s,
+                             int32_t* __restrict__ bkt_s) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  int64_t p = perm[q];
+  req_s[q] = req[p];
+  bkt_s[q] = bkt[p];
+}
+
+__global__ void k_node_bound(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF, double theta,
+                             double alpha, const int8_t* __restrict__ ncase, const double2* __restrict__ vcache,
+                             int8_t* __restrict__ nref, double* __restrict__ nU) {
+  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (n >= nF) return;
+  int cs = ncase[n];
+  if (cs == 1) return;
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  int h = g.lfull - level;
+  Lattice L = node_lattice(g, h, i, j, k);
+  int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
+  double zmax = -INFINITY, zmin = INFINITY;
+  for (int64_t q = lane; q < nc; q += 32) {
+    double2 ms = vcache[lattice_vertex(g, L, q)];
+    double z = (ms.x - theta) / (ms.y * SQRT2);
+    zmax = fmax(zmax, z);
+    zmin = fmin(zmin, z);
+  }
+  zmax = warp_max(zmax);
+  zmin = warp_min(zmin);
+  if (lane != 0) return;
+  // Q_lo = max P(Y > th) = erfc(-zmax)/2, Q_hi = max P(Y < th) = erfc(zmin)/2
+  double q_lo = 0.5 * erfc(-zmax), q_hi = 0.5 * erfc(zmin);
+  double d = (double)(L.vmax[0] - L.base[0] + 1) * (double)(L.vmax[1] - L.base[1] + 1) *
+             (double)(L.vmax[2] - L.base[2] + 1);
+  double U;
+  if (cs == 2) {
+    U = -expm1(d * log1p(-q_lo));
+  } else if (cs == 3) {
+    U = -expm1(d * log1p(-q_hi));
+  } else {
+    U = -expm1(d * log1p(-q_lo)) - exp(d * log1p(-q_hi));
+    U = U < 0.0 ? 0.0 : (U > 1.0 ? 1.0 : U);
+  }
+  nU[n] = U;
+  nref[n] = U > alpha ? 1 : 0;
+}
+
+__global__ void k_node_records(int level, const uint64_t* __restrict__ front, int64_t nF,
+                               const int8_t* __restrict__ ncase, const int8_t* __restrict__ nref,
+                               const double* __restrict__ np1, const double* __restrict__ np2,
+                               const double* __restrict__ nU, lcp_node_rec_t* __restrict__ out,
+                               unsigned long long* __restrict__ stats) {
+  int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nF) return;
+  if (out) {
+    lcp_node_rec_t r;
+    node_unkey(front[n], r.i, r.j, r.k);
+    r.level = level;
+    r.ncase = ncase[n];
+    r.refine = nref[n];
+    r.p1 = np1[n];
+    r.p2 = np2[n];
+    r.U = nU[n];
+    out[n] = r;
+  }
+  atomicAdd(&stats[ncase[n]], 1ull);
+  if (nref[n]) atomicAdd(&stats[4], 1ull);
+}
+
+// children / leaf counts of refined nodes
+__global__ void k_node_counts(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
+                              const int8_t* __restrict__ nref, int slab_level, int z0, int z1,
+                              int64_t* __restrict__ cnt) {
+  int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nF) return;
+  if (!nref[n]) {
+    cnt[n] = 0;
+    return;
+  }
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  int h = g.lfull - level;
+  if (level < max_depth) {
+    int64_t cs = (int64_t)1 << (h - 1);
+    int c = 0;
+    for (int ch = 0; ch < 8; ++ch) {
+      int64_t ci = 2 * (int64_t)i + (ch & 1), cj = 2 * (int64_t)j + ((ch >> 1) & 1), ck = 2 * (int64_t)k + (ch >> 2);
+      bool in = ci * cs < g.cells[0] && cj * cs < g.cells[1] && ck * cs < g.cells[2];
+      if (level + 1 == slab_level) in = in && ck >= z0 && ck < z1;
+      c += in;
+    }
+    cnt[n] = c;
+  } else {
+    int64_t side = (int64_t)1 << h;
+    int64_t e[3];
+    int a[3] = {i, j, k};
+    for (int d = 0; d < 3; ++d) {
+      int64_t b = (int64_t)a[d] * side;
+      e[d] = min(b + side, (int64_t)g.cells[d]) - b;
+    }
+    cnt[n] = e[0] * e[1] * e[2];
+  }
+}
+
+__global__ void k_emit(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
+                       const int8_t* __restrict__ nref, const int64_t* __restrict__ offs, int slab_level, int z0,
+                       int z1, uint64_t* __restrict__ next, int64_t* __restrict__ leaves) {
+  int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nF || !nref[n]) return;
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  int h = g.lfull - level;
+  int64_t o = offs[n];
+  if (level < max_depth) {
+    int64_t cs = (int64_t)1 << (h - 1);
+    for (int ch = 0; ch < 8; ++ch) {
+      int64_t ci = 2 * (int64_t)i + (ch & 1), cj = 2 * (int64_t)j + ((ch >> 1) & 1), ck = 2 * (int64_t)k + (ch >> 2);
+      bool in = ci * cs < g.cells[0] && cj * cs < g.cells[1] && ck * cs < g.cells[2];
+      if (level + 1 == slab_level) in = in && ck >= z0 && ck < z1;
+      if (in) next[o++] = node_key(ci, cj, ck);
+    }
+  } else {
+    int64_t side = (int64_t)1 << h;
+    int64_t b0 = (int64_t)i * side, b1 = (int64_t)j * side, b2 = (int64_t)k * side;
+    int64_t e0 = min(b0 + side, (int64_t)g.cells[0]), e1 = min(b1 + side, (int64_t)g.cells[1]),
+            e2 = min(b2 + side, (int64_t)g.cells[2]);
+    for (int64_t z = b2; z < e2; ++z)
+      for (int64_t y = b1; y < e1; ++y)
+        for (int64_t x = b0; x < e0; ++x) leaves[o++] = x + (int64_t)g.cells[0] * (y + (int64_t)g.cells[1] * z);
+  }
+}
+
+lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
+  if (!c.fitted) return set_err(c, LCP_ESTATE, "refine before fit");
+  if (!(alpha > 0.0 && alpha < 0.5)) return set_err(c, LCP_EINVAL, "refine: threshold must be in (0, 0.5)");
+  if (max_depth < 0 || max_depth > c.g.lfull) return set_err(c, LCP_EINVAL, "refine: max_depth not in [0, Lfull]");
+  if (!std::isfinite(theta)) return set_err(c, LCP_EINVAL, "refine: isovalue not finite");
+  const Geom& g = c.g;
+  cudaError_t e;
+#define CK(x)                                        \
+  do {                                               \
+    e = (x);                                         \
+    if (e != cudaSuccess) return cuda_err(c, e, #x); \
+  } while (0)
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, c.stream);
+  const int64_t m = c.m;
+  CK(c.plo.ensure(sizeof(double) * m));
+  CK(c.phi.ensure(sizeof(double) * m));
+  CK(c.counters.ensure(sizeof(unsigned long long) * 16));
+  if (!c.h_counters) CK(cudaMallocHost(&c.h_counters, sizeof(int64_t) * 16));
+  k_obs_probs<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(c.obs_sorted_idx.as<int32_t>(), c.obs_mu.as<double>(),
+                                                                 c.obs_sd.as<double>(), m, theta, c.plo.as<double>(),
+                                                                 c.phi.as<double>());
+  CK(c.front[0].ensure(sizeof(uint64_t)));
+  uint64_t root = node_key(0, 0, 0);
+  CK(cudaMemcpyAsync(c.front[0].p, &root, sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
+  int cur = 0;
+  int64_t nF = 1;
+  c.n_leaves = 0;
+  c.n_recs = 0;
+  c.last_requests = 0;
+  c.level_nodes.clear();
+  c.level_refined.clear();
+  for (int q = 0; q < 4; ++q) c.level_case[q].clear();
+  // z-slab of this rank at slab_level
+  int slab_level = -1, z0 = 0, z1 = 1 << 30;
+  if (c.opts.slab_count > 1) {
+    slab_level = c.opts.slab_level;
+    int64_t side = (int64_t)1 << (g.lfull - slab_level);
+    int nz = (int)((g.cells[2] + side - 1) / side);
+    z0 = (int)((int64_t)c.opts.slab_rank * nz / c.opts.slab_count);
+    z1 = (int)((int64_t)(c.opts.slab_rank + 1) * nz / c.opts.slab_count);
+  }
+  unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  for (int level = 0; level <= max_depth && nF > 0; ++level) {
+    int h = g.lfull - level;
+    CK(c.ncase.ensure(nF));
+    CK(c.nref.ensure(nF));
+    CK(c.np1.ensure(sizeof(double) * nF));
+    CK(c.np2.ensure(sizeof(double) * nF));
+    CK(c.nU.ensure(sizeof(double) * nF));
+    CK(c.cnt.ensure(sizeof(int64_t) * nF));
+    CK(c.offs.ensure(sizeof(int64_t) * nF));
+    CK(cudaMemsetAsync(c.nref.p, 0, nF, c.stream));
+    int hf = std::min(h, g.h_full);
+    int64_t per = ((int64_t)1 << hf) + 1;
+    int64_t cap = std::min(nF * per * per * per, c.n_vertices);
+    CK(c.req.ensure(sizeof(int64_t) * cap));
+    CK(c.req_sorted.ensure(sizeof(int64_t) * cap));
+    CK(c.cell_bucket.ensure(sizeof(int32_t) * 2 * cap));
+    CK(c.perm.ensure(sizeof(int64_t) * cap));
+    CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * 16, c.stream));
+    const uint64_t* F = c.front[cur].as<uint64_t>();
+    unsigned gw = (unsigned)((nF * 32 + 255) / 256);
+    k_node_prelim<<<gw, 256, 0, c.stream>>>(g, level, F, nF, c.obs_sorted_key.as<uint64_t>(), c.plo.as<double>(),
+                                            c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
+                                            c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(),
+                                            c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    int64_t nreq = c.h_counters[0];
+    c.last_requests += nreq;
+    if (nreq > 0) {
+      int32_t* bkt = c.cell_bucket.as<int32_t>();
+      int32_t* bkt_s = bkt + cap;
+      unsigned gr = (unsigned)((nreq + 255) / 256);
+      k_req_bucket<<<gr, 256, 0, c.stream>>>(g, c.req.as<int64_t>(), nreq, bkt);
+      CK(group_by_bucket(c, bkt, nreq, c.perm.as<int64_t>()));
+      k_gather_req<<<gr, 256, 0, c.stream>>>(c.req.as<int64_t>(), bkt, c.perm.as<int64_t>(), nreq,
+                                             c.req_sorted.as<int64_t>(), bkt_s);
+      CK(launch_marginals(c, Q_VERTEX, c.req_sorted.as<int64_t>(), bkt_s, nreq, nullptr, nullptr, nullptr, 0,
+                          nullptr));
+    }
+    k_node_bound<<<gw, 256, 0, c.stream>>>(g, level, F, nF, theta, alpha, c.ncase.as<int8_t>(),
+                                           c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>());
+    lcp_node_rec_t* rec_out = nullptr;
+    const bool keep = level < c.opts.keep_records;
+    if (keep) {
+      CK(c.recs.ensure_keep(sizeof(lcp_node_rec_t) * (c.n_recs + nF), sizeof(lcp_node_rec_t) * c.n_recs, c.stream));
+      rec_out = c.recs.as<lcp_node_rec_t>() + c.n_recs;
+    }
+    unsigned gt = (unsigned)((nF + 255) / 256);
+    k_node_records<<<gt, 256, 0, c.stream>>>(level, F, nF, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
+                                             c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(), rec_out,
+                                             dcnt + 8);
+    k_node_counts<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), slab_level, z0, z1,
+                                            c.cnt.as<int64_t>());
+    CK(exclusive_scan_i64(c, c.cnt.as<int64_t>(), c.offs.as<int64_t>(), nF, (int64_t*)(dcnt + 1)));
+    CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    int64_t total = c.h_counters[1];
+    if (keep) c.n_recs += nF;
+    c.level_nodes.push_back(nF);
+    c.level_refined.push_back(c.h_counters[12]);
+    for (int q = 0; q < 4; ++q) c.level_case[q].push_back(c.h_counters[8 + q]);
+    if (level < max_depth) {
+      CK(c.front[cur ^ 1].ensure(sizeof(uint64_t) * std::max<int64_t>(total, 1)));
+      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
+                                       slab_level, z0, z1, c.front[cur ^ 1].as<uint64_t>(), nullptr);
+      cur ^= 1;
+      nF = total;
+    } else {
+      CK(c.leaves.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
+      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
+                                       slab_level, z0, z1, nullptr, c.leaves.as<int64_t>());
+      c.n_leaves = total;
+      nF = 0;
+    }
+    CK(cudaGetLastError());
+  }
+  cudaEventRecord(e1, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  c.t.refine_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+#undef CK
+  return check_device_errors(c);
+}
+
+}  // namespace lcp

@@ -1,0 +1,264 @@
+// pmc.cu -- lcp_pmc_cells: SURVEY §8(a) rows a7-a9.
+//
+//  a7  cell posterior (marginals.cu: k_cell_posterior), cells grouped by bucket
+//  a8  k_chol8 : 8x8 Cholesky of Sigma in FP64 with the PSD pivot clamp (R14)
+//      k_pmc   : warp per cell; lane l draws samples s = l, l+32, ...:
+//                Philox4x32-10 on counter (2s+j, cell lo, cell hi, iso), key =
+//                seed (R13); uniforms from the low 23 bits; Box-Muller; y = mu +
+//                L z in FP32; crossing = not all y < th and not all y > th
+//                (R5, R24).  LCP = count / N.
+//  a9  k_scatter : dense field, zero off the leaves.
+#include <algorithm>
+
+#include "ctx.h"
+
+namespace lcp {
+
+constexpr int64_t PMC_CHUNK = (int64_t)1 << 23;   // cells per posterior/MC chunk (2.9 GB of records)
+
+__global__ void k_cell_bucket(Geom g, const int64_t* __restrict__ cells, int64_t n, int32_t* __restrict__ bkt,
+                              int* __restrict__ derr) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  int64_t cell = cells[q];
+  int64_t ncell = (int64_t)g.cells[0] * g.cells[1] * g.cells[2];
+  if (cell < 0 || cell >= ncell) {
+    atomicOr(derr, DERR_OVERFLOW);
+    cell = 0;
+  }
+  bkt[q] = cell_bucket(g, cell);
+}
+
+// number of positions where the bucket changes (runs - 1)
+__global__ void k_count_runs(const int32_t* __restrict__ bkt, int64_t n, unsigned long long* __restrict__ out) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned v = (q + 1 < n && bkt[q] != bkt[q + 1]) ? 1u : 0u;
+  unsigned b = __ballot_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, (unsigned long long)__popc(b));
+}
+
+__global__ void k_gather_bkt(const int32_t* __restrict__ bkt, const int64_t* __restrict__ perm, int64_t n,
+                             int32_t* __restrict__ out) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) out[q] = bkt[perm[q]];
+}
+
+// a8: in-place: rec = [mu (8 double) | Sigma packed (36 double)] ->
+//                     [mu (8 double) | L packed row-major lower (36 float) | unused]
+__global__ void k_chol8(double* __restrict__ post, int64_t n) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  double* rec = post + 44 * q;
+  double S[36];
+#pragma unroll
+  for (int p = 0; p < 36; ++p) S[p] = rec[8 + p];
+  double md = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) md = fmax(md, S[c * (c + 3) / 2]);
+  const double tol = 1e-12 * md;
+  double L[36];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double s = S[j * (j + 3) / 2];
+#pragma unroll
+    for (int p = 0; p < j; ++p) s -= L[j * (j + 1) / 2 + p] * L[j * (j + 1) / 2 + p];
+    bool live = s > tol;
+    double ljj = live ? sqrt(s) : 0.0;
+    double inv = live ? 1.0 / ljj : 0.0;
+    L[j * (j + 3) / 2] = ljj;
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) {
+      double t = S[i * (i + 1) / 2 + j];
+#pragma unroll
+      for (int p = 0; p < j; ++p) t -= L[i * (i + 1) / 2 + p] * L[j * (j + 1) / 2 + p];
+      L[i * (i + 1) / 2 + j] = live ? t * inv : 0.0;
+    }
+  }
+  float* Lf = reinterpret_cast<float*>(rec + 8);
+#pragma unroll
+  for (int p = 0; p < 36; ++p) Lf[p] = (float)L[p];
+}
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                              uint32_t k1, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                              uint32_t& r3) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c0 = n0;
+    c1 = (uint32_t)p1;
+    c2 = n2;
+    c3 = (uint32_t)p0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  r0 = c0; r1 = c1; r2 = c2; r3 = c3;
+}
+
+// u = (r mod 2^23 + 1/2) 2^-23, exact: one LOP3 + one FADD
+__device__ __forceinline__ float u23(uint32_t r) {
+  return __uint_as_float(0x3f800000u | (r & 0x7fffffu)) - (1.0f - 0x1p-24f);
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Box-Muller: (R cos 2 pi ub, R sin 2 pi ub), R = sqrt(-2 ln ua); the angle is
+// reduced to (-pi, pi) via ub - 1/2 (exact), which flips both signs.
+__device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, float& z1) {
+  float ua = u23(ra), ub = u23(rb);
+  float r2 = fmaxf(-1.3862943611198906f * __log2f(ua), 0.0f);
+  float nR = -sqrt_approx(r2);
+  float s, co;
+  __sincosf(6.283185307179586f * (ub - 0.5f), &s, &co);
+  z0 = nR * co;
+  z1 = nR * s;
+}
+
+__global__ void __launch_bounds__(256) k_pmc(const int64_t* __restrict__ cells, const double* __restrict__ post,
+                                             int64_t n, double theta, uint32_t N, uint32_t k0, uint32_t k1,
+                                             uint32_t iso, float* __restrict__ out) {
+  int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (q >= n) return;
+  const double* rec = post + 44 * q;
+  float m[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) m[c] = (float)(rec[c] - theta);
+  const float4* L4 = reinterpret_cast<const float4*>(rec + 8);
+  float L[36];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    float4 v = L4[t];
+    L[4 * t] = v.x; L[4 * t + 1] = v.y; L[4 * t + 2] = v.z; L[4 * t + 3] = v.w;
+  }
+  int64_t cell = cells[q];
+  uint32_t c1 = (uint32_t)(uint64_t)cell, c2 = (uint32_t)((uint64_t)cell >> 32);
+  uint32_t cnt = 0;
+  for (uint32_t s = lane; s < N; s += 32) {
+    uint32_t r[8];
+    philox4x32_10(2u * s, c1, c2, iso, k0, k1, r[0], r[1], r[2], r[3]);
+    philox4x32_10(2u * s + 1u, c1, c2, iso, k0, k1, r[4], r[5], r[6], r[7]);
+    float z[8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) box_muller(r[2 * p], r[2 * p + 1], z[2 * p], z[2 * p + 1]);
+    float mx = -INFINITY, mn = INFINITY;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float y = m[c];
+#pragma unroll
+      for (int d = 0; d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
+      mx = fmaxf(mx, y);
+      mn = fminf(mn, y);
+    }
+    cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0) out[q] = (float)((double)cnt / (double)N);
+}
+
+__global__ void k_scatter(const int64_t* __restrict__ cells, const float* __restrict__ lcp, int64_t n,
+                          float* __restrict__ field) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) field[cells[q]] = lcp[q];
+}
+
+// posterior of n cells (device list) into post (n x 44 doubles); groups by
+// bucket unless the list already comes in long same-bucket runs.
+lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* post) {
+  cudaError_t e;
+#define CK(x)                                        \
+  do {                                               \
+    e = (x);                                         \
+    if (e != cudaSuccess) return cuda_err(c, e, #x); \
+  } while (0)
+  if (n <= 0) return LCP_OK;
+  CK(c.cell_bucket.ensure(sizeof(int32_t) * 2 * n));
+  CK(c.counters.ensure(sizeof(unsigned long long) * 16));
+  if (!c.h_counters) CK(cudaMallocHost(&c.h_counters, sizeof(int64_t) * 16));
+  int32_t* bkt = c.cell_bucket.as<int32_t>();
+  unsigned gr = (unsigned)((n + 255) / 256);
+  k_cell_bucket<<<gr, 256, 0, c.stream>>>(c.g, cells, n, bkt, c.derr.as<int>());
+  unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  CK(cudaMemsetAsync(dcnt + 15, 0, sizeof(unsigned long long), c.stream));
+  k_count_runs<<<gr, 256, 0, c.stream>>>(bkt, n, dcnt + 15);
+  CK(cudaMemcpyAsync(c.h_counters + 15, dcnt + 15, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  int64_t runs = c.h_counters[15] + 1;
+  if (n / runs >= 64 || c.g.nbuckets == 1) {
+    CK(launch_cell_posterior(c, cells, nullptr, bkt, n, post));
+  } else {
+    CK(c.perm.ensure(sizeof(int64_t) * n));
+    CK(group_by_bucket(c, bkt, n, c.perm.as<int64_t>()));
+    int32_t* bs = bkt + n;
+    k_gather_bkt<<<gr, 256, 0, c.stream>>>(bkt, c.perm.as<int64_t>(), n, bs);
+    CK(launch_cell_posterior(c, cells, c.perm.as<int64_t>(), bs, n, post));
+  }
+#undef CK
+  return LCP_OK;
+}
+
+lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int64_t N, uint64_t seed,
+                      uint32_t iso, float* out) {
+  if (!c.fitted) return set_err(c, LCP_ESTATE, "pmc before fit");
+  if (N < 1 || N > ((int64_t)1 << 31)) return set_err(c, LCP_EINVAL, "pmc: need 1 <= n_samples <= 2^31");
+  if (n < 0) return set_err(c, LCP_EINVAL, "pmc: negative cell count");
+  if (n == 0) return LCP_OK;
+  cudaError_t e;
+#define CK(x)                                        \
+  do {                                               \
+    e = (x);                                         \
+    if (e != cudaSuccess) return cuda_err(c, e, #x); \
+  } while (0)
+  if (!c.ev_init) {
+    for (int i = 0; i < 8; ++i) cudaEventCreate(&c.ev[i]);
+    c.ev_init = true;
+  }
+  int64_t chunk = std::min(n, PMC_CHUNK);
+  CK(c.post.ensure(sizeof(double) * 44 * chunk));
+  double* post = c.post.as<double>();
+  float tp = 0, tc = 0, tm = 0;
+  for (int64_t s0 = 0; s0 < n; s0 += chunk) {
+    int64_t nn = std::min(chunk, n - s0);
+    cudaEventRecord(c.ev[0], c.stream);
+    lcp_status_t st = posterior_impl(c, cells + s0, nn, post);
+    if (st != LCP_OK) return st;
+    cudaEventRecord(c.ev[1], c.stream);
+    k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(post, nn);
+    cudaEventRecord(c.ev[2], c.stream);
+    k_pmc<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, c.stream>>>(cells + s0, post, nn, theta, (uint32_t)N,
+                                                                  (uint32_t)seed, (uint32_t)(seed >> 32), iso,
+                                                                  out + s0);
+    cudaEventRecord(c.ev[3], c.stream);
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(c.ev[3]));
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, c.ev[0], c.ev[1]);
+    cudaEventElapsedTime(&b, c.ev[1], c.ev[2]);
+    cudaEventElapsedTime(&d, c.ev[2], c.ev[3]);
+    tp += a; tc += b; tm += d;
+  }
+  c.t.posterior_ms = tp;
+  c.t.chol_ms = tc;
+  c.t.mc_ms = tm;
+  c.last_pmc_cells = n;
+  c.last_pmc_samples = n * N;
+#undef CK
+  return check_device_errors(c);
+}
+
+cudaError_t launch_scatter(Ctx& c, const int64_t* cells, const float* lcp, int64_t n, float* field) {
+  int64_t ncell = (int64_t)c.g.cells[0] * c.g.cells[1] * c.g.cells[2];
+  cudaError_t e = cudaMemsetAsync(field, 0, sizeof(float) * ncell, c.stream);
+  if (e != cudaSuccess) return e;
+  if (n > 0) k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cells, lcp, n, field);
+  return cudaGetLastError();
+}
+
+}  // namespace lcp

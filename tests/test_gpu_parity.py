@@ -1,0 +1,274 @@
+"""GPU parity: the CUDA path through the C ABI vs the FP64 oracle.
+
+Tolerances (BASELINE north_star, R18/R19): posterior mu / Sigma within 1e-5
+(prior-scaled floors); k-NN sets and leaf sets bit-exact (except nodes excused by
+the 1e-6 band around alpha); LCP |d| <= 2/N on >= 99.9 % of cells with mean
+|d| <= 1e-4 under identical Philox streams.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from tests.parity_util import compare_node_sets, lcp_parity, posterior_close
+from workloads import generate
+from workloads.gen import random_cells
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def _ctx(name, dev, k=None, bucket_log2=None, keep_records=True, precision=0, host_inputs=False):
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate(name)
+    cfg = w.cfg
+    kernel, grid, kk, b, hf = config_args(cfg, k, bucket_log2)
+    ctx = Context(0)
+    if host_inputs:
+        X, y = w.X, w.y
+    else:
+        X = torch.from_numpy(np.array(w.X)).to(dev)
+        y = torch.from_numpy(np.array(w.y)).to(dev)
+    ctx.fit_local(X, y, kernel, kk, grid, bucket_log2=b, h_full=hf, keep_records=keep_records,
+                  precision=precision)
+    M = O.Model.from_config(cfg, w.X, w.y, k=kk, bucket_log2=b)
+    return w, ctx, M
+
+
+@pytest.mark.parametrize("name", ["c1", "t1", "t2", "c2", "c3", "c4"])
+def test_knn_sets_exact(name, dev):
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    S = ctx.bucket_sets().cpu().numpy()
+    nb = M.nbuckets
+    assert S.shape == (nb, w.cfg.k)
+    bad = [b for b in range(nb) if not np.array_equal(S[b], M.bucket_set(b))]
+    assert not bad, f"{len(bad)} buckets differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("name", ["c1", "t2", "c3", "c4"])
+def test_point_marginals(name, dev):
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    g = np.random.default_rng(5)
+    P = np.asarray(cfg.lo) + (np.asarray(cfg.hi) - np.asarray(cfg.lo)) * g.random((300, 3))
+    P = np.concatenate([P, w.X[:50]])
+    mu_g, var_g = ctx.point_marginals(torch.from_numpy(P).to(dev))
+    mu_g, var_g = mu_g.cpu().numpy(), var_g.cpu().numpy()
+    mu_o = np.zeros(len(P))
+    var_o = np.zeros(len(P))
+    for q, p in enumerate(P):
+        mu_o[q], var_o[q] = M.local_marginal(M.point_bucket(p), p)
+    em, ev = posterior_close(mu_g, mu_o, var_g, var_o, cfg.variance, 1e-5)
+    assert em <= 1e-5 and ev <= 1e-5, (em, ev)
+
+
+@pytest.mark.parametrize("name", ["c1", "t1", "t2", "c3", "c4"])
+def test_cell_posterior(name, dev):
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cells = random_cells(name, 400, 11)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    mu_g, cov_g = mu_g.cpu().numpy(), cov_g.cpu().numpy()
+    worst = (0.0, 0.0)
+    for q, c in enumerate(cells):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, w.cfg.variance, 1e-5)
+        worst = (max(worst[0], em), max(worst[1], ec))
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
+
+
+@pytest.mark.parametrize("name", ["c1", "t1", "t2", "c2", "c3"])
+def test_octree_node_sets(name, dev):
+    w, ctx, M = _ctx(name, dev)
+    cfg = w.cfg
+    for it, th in enumerate(w.thetas):
+        leaves_g = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy()
+        rec_g = ctx.node_records()
+        rec_o, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+        res = compare_node_sets(rec_g, rec_o, cfg.alpha)
+        assert not res["unexcused"], (res["unexcused"][:10], res)
+        assert res["max_dU"] < 1e-6, res
+        if res["excused"] == 0:
+            assert np.array_equal(np.sort(leaves_g), leaves_o)
+
+
+@pytest.mark.parametrize("name", ["c1", "t1", "t2"])
+def test_pmc_leaves_parity(name, dev):
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    for it, th in enumerate(w.thetas):
+        leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+        lcp_g = ctx.pmc_cells(leaves, th, cfg.n_samples, cfg.mc_seed, it).cpu().numpy()
+        lcp_o = M.pmc_cells(leaves.cpu().numpy(), th, cfg.n_samples, cfg.mc_seed, it)
+        frac, mean, mx = lcp_parity(lcp_g, lcp_o, cfg.n_samples)
+        assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+        assert np.all((lcp_g >= 0) & (lcp_g <= 1))
+
+
+def test_pmc_c2_fp64_subset(dev):
+    w, ctx, M = _ctx("c2", dev, keep_records=False)
+    cfg = w.cfg
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    lcp_g = ctx.pmc_cells(leaves, th, cfg.n_samples, cfg.mc_seed).cpu().numpy()
+    sel = np.arange(0, len(leaves), 13)
+    lcp_o = M.pmc_cells(leaves.cpu().numpy()[sel], th, cfg.n_samples, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(lcp_g[sel], lcp_o, cfg.n_samples)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_random_cell_list_and_host_pointers(dev):
+    # arbitrary (unsorted, multi-bucket) cell list, host in/out pointers
+    w, ctx, M = _ctx("t2", dev, keep_records=False, host_inputs=True)
+    cfg = w.cfg
+    cells = random_cells("t2", 3001, 3)[::-1].copy()
+    out = np.zeros(len(cells), np.float32)
+    ctx.pmc_cells(cells, w.thetas[0], 500, 99, 0, out=out)
+    lcp_o = M.pmc_cells(cells, w.thetas[0], 500, 99, 0)
+    frac, mean, mx = lcp_parity(out, lcp_o, 500)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_dense_equals_pruned_on_leaves(dev):
+    # identical Philox streams: the dense baseline and the pruned run agree bit
+    # for bit on every leaf cell
+    w, ctx, _ = _ctx("t1", dev, keep_records=False)
+    cfg = w.cfg
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).clone()
+    lcp_l = ctx.pmc_cells(leaves, th, cfg.n_samples, cfg.mc_seed)
+    allc = torch.arange(int(np.prod(cfg.cells)), device=dev, dtype=torch.int64)
+    lcp_d = ctx.pmc_cells(allc, th, cfg.n_samples, cfg.mc_seed)
+    assert torch.equal(lcp_d[leaves], lcp_l)
+    f1, n1 = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    assert n1 == len(leaves)
+    assert torch.equal(f1[leaves], lcp_l)
+    mask = torch.ones_like(f1, dtype=torch.bool)
+    mask[leaves] = False
+    assert torch.all(f1[mask] == 0)
+
+
+def test_determinism(dev):
+    w, ctx, _ = _ctx("c2", dev, keep_records=False)
+    cfg = w.cfg
+    th = w.thetas[0]
+    a, na = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    a = a.clone()
+    b, nb = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    assert na == nb and torch.equal(a, b)
+
+
+def test_slab_union_equals_full(dev):
+    # z-slab decomposition emulated on one GPU: the union of the
+    # per-slab leaf sets and LCPs equals the single-domain run bit for bit.
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate("c2")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    th = w.thetas[0]
+    full = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    ref, _ = full.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    G = 4
+    acc = torch.zeros_like(ref)
+    leaves_all = []
+    for r in range(G):
+        ctx = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=r,
+                                   slab_count=G, slab_level=3)
+        f, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+        leaves_all.append(ctx.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy())
+        acc += f
+    L = np.concatenate(leaves_all)
+    assert len(L) == len(np.unique(L))
+    assert torch.equal(acc, ref)
+
+
+def test_error_codes(dev):
+    from paper_2512_12442_b200 import Context, LcpError, config_args
+    from paper_2512_12442_b200.lcp import LCP_EINVAL, LCP_ESTATE
+    w = generate("t1")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    ctx = Context(0)
+    with pytest.raises(LcpError) as e:
+        ctx.octree_refine(0.0, 1e-3, 3)
+    assert e.value.status == LCP_ESTATE
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    with pytest.raises(LcpError) as e:
+        ctx.fit_local(X, y, kernel, cfg.m + 1, grid)
+    assert e.value.status == LCP_EINVAL
+    ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    for bad_alpha in (0.0, 0.5, -1.0):
+        with pytest.raises(LcpError) as e:
+            ctx.octree_refine(0.0, bad_alpha, 3)
+        assert e.value.status == LCP_EINVAL
+    with pytest.raises(LcpError) as e:
+        ctx.octree_refine(0.0, 1e-3, 99)
+    assert e.value.status == LCP_EINVAL
+    cells = torch.zeros(3, dtype=torch.int64, device=dev)
+    with pytest.raises(LcpError) as e:
+        ctx.pmc_cells(cells, 0.0, 0, 1)
+    assert e.value.status == LCP_EINVAL
+    with pytest.raises(LcpError) as e:
+        ctx.pmc_cells(np.array([-1, 5], np.int64), 0.0, 10, 1, out=np.zeros(2, np.float32))
+    assert e.value.status == LCP_EINVAL
+    # empty list, max_depth 0 (root only), far-shifted isovalue (empty leaf set)
+    empty = torch.zeros(0, dtype=torch.int64, device=dev)
+    assert ctx.pmc_cells(empty, 0.0, 10, 1).numel() == 0
+    leaves = ctx.octree_refine(-50.0, 1e-3, cfg.max_depth)
+    assert leaves.numel() == 0
+    leaves0 = ctx.octree_refine(w.thetas[0], 1e-3, 0)
+    assert leaves0.numel() in (0, int(np.prod(cfg.cells)))
+
+
+def test_k_equals_m_exact_gp(dev):
+    # the dense exact-GP configuration (k = m, one bucket) used by the c3 baseline
+    w, ctx, M = _ctx("t1", dev, k=generate("t1").cfg.m, bucket_log2=0, keep_records=False)
+    cells = random_cells("t1", 200, 4)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    kern = O.make_kernel(w.cfg.kernel, w.cfg.variance, w.cfg.lengthscale, w.cfg.nugget, w.cfg.prior_mean)
+    cfg = w.cfg
+    h = [(cfg.hi[d] - cfg.lo[d]) / cfg.cells[d] for d in range(3)]
+    nx, ny = cfg.cells[0], cfg.cells[1]
+    for q, c in enumerate(cells[:40]):
+        i, j, k = c % nx, (c // nx) % ny, c // (nx * ny)
+        Q = np.array([[cfg.lo[0] + (i + (a & 1)) * h[0], cfg.lo[1] + (j + ((a >> 1) & 1)) * h[1],
+                       cfg.lo[2] + (k + (a >> 2)) * h[2]] for a in range(8)])
+        mu_o, cov_o = O.gp_exact(kern, w.X, w.y, Q)
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5
+
+
+def test_full_size_c5_sampled(dev):
+    # BASELINE's largest config at full size, in the launch configuration the
+    # bench times: sampled node records and leaf LCPs against the oracle.
+    w, ctx, M = _ctx("c5", dev, keep_records=7)
+    cfg = w.cfg
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    rec = ctx.node_records()
+    g = np.random.default_rng(1)
+    # every node of levels 0-2 and a sample of deeper ones, evaluated one by one
+    pick = np.concatenate([np.nonzero(rec["level"] <= 2)[0], g.choice(len(rec), 300, replace=False)])
+    bad = 0
+    for q in pick:
+        r = rec[q]
+        o = M.eval_node(th, cfg.alpha, int(r["level"]), int(r["i"]), int(r["j"]), int(r["k"]))
+        near = abs(o["U"] - cfg.alpha) <= 1e-6 or (o["p1"] >= 0 and (abs(o["p1"] - cfg.alpha) <= 1e-6 or abs(o["p2"] - cfg.alpha) <= 1e-6))
+        if (o["refine"] != r["refine"] or o["ncase"] != r["ncase"]) and not near:
+            bad += 1
+        assert abs(o["U"] - r["U"]) < 1e-6
+    assert bad == 0
+    lv = leaves.cpu().numpy()
+    sel = g.choice(len(lv), 96, replace=False)
+    lcp_g = ctx.pmc_cells(leaves, th, cfg.n_samples, cfg.mc_seed).cpu().numpy()[sel]
+    lcp_o = M.pmc_cells(lv[sel], th, cfg.n_samples, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, cfg.n_samples)
+    assert frac >= 0.99 and mean <= 1e-4, (frac, mean, mx)
