@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from tests.parity_util import compare_node_sets, lcp_parity, posterior_close
+from parity_util import compare_node_sets, lcp_parity, posterior_close
 from workloads import generate
 from workloads.gen import random_cells
 
