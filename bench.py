@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the LCP hot path (BASELINE.json metric: PMC LCP cells/sec and
+end-to-end octree LCP time at 1/2/4/8 B200; % FP32 roofline).
+
+One step = one pass of the whole hot path over the
+workload: lcp_fit_local (binning, k-NN, bucket factors, observation marginals)
++ lcp_run_field (octree refine, leaf posterior, chol8, Philox MC, dense field
+scatter) and, for N > 1 GPUs, the NCCL reduction of the per-slab fields to rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl ours|reference]
+
+Rank 0 prints ONE JSON line.  See DESIGN.md §6 for every key.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PMC LCP cells/sec"
+UNIT = "cells/s"
+# minimal per-sample op mix of k_pmc: Philox4x32-10 x2 = 80,
+# uniforms 16, Box-Muller 4 x 11 = 44 (16 MUFU), L z + mu 36, crossing test 16
+ALG_OPS_PER_SAMPLE = 192
+SM_COUNT = 148
+LANES_PER_SM_CLK = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def workload_desc(cfg, thetas):
+    kern = {0: "SE", 1: "Matern-5/2"}[cfg.kernel]
+    return (f"{cfg.name}: {cfg.cells[0]}x{cfg.cells[1]}x{cfg.cells[2]} cells, m={cfg.m} observations "
+            f"({cfg.placement}), {cfg.n_bumps} Gaussian bumps, {kern} l={cfg.lengthscale[0]} "
+            f"var={cfg.variance} nugget={cfg.nugget}, k={cfg.k}, bucket_log2={cfg.bucket_log2}, "
+            f"h_full={cfg.h_full}, N={cfg.n_samples}, alpha={cfg.alpha}, max_depth={cfg.max_depth}, "
+            f"isovalues={thetas}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        loaded = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(kernel="k_pmc"):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except Exception:
+        return None
+
+
+def oracle_sample(w, oracle_model=None, stride=16):
+    """The oracle as it stands on a bounded sample of the workload: the octree
+    on the level-3 subtree (0,0,0) and the leaf pass on every `stride`-th leaf
+    of it (time extrapolated to all its leaves); the model build is amortised
+    by the sample's share of the domain.  Returns (cells/s, seconds, detail)."""
+    import oracle as O
+    cfg = w.cfg
+    t0 = time.perf_counter()
+    M = oracle_model or O.Model.from_config(cfg, w.X, w.y)
+    t_fit = time.perf_counter() - t0
+    lf = M.lfull
+    sl = min(3, cfg.max_depth)
+    side = 1 << (lf - sl)
+    sample_cells = int(np.prod([min(side, c) for c in cfg.cells]))
+    total_cells = int(np.prod(cfg.cells))
+    t_oct = t_pmc = 0.0
+    n_leaf = n_done = 0
+    for it, th in enumerate(w.thetas):
+        t0 = time.perf_counter()
+        _, leaves = M.octree(th, cfg.alpha, cfg.max_depth, subtree=(sl, 0, 0, 0))
+        t_oct += time.perf_counter() - t0
+        sub = leaves[::stride]
+        t0 = time.perf_counter()
+        if len(sub):
+            M.pmc_cells(sub, th, cfg.n_samples, cfg.mc_seed, it)
+        dt = time.perf_counter() - t0
+        t_pmc += dt * (len(leaves) / max(len(sub), 1))
+        n_leaf += len(leaves)
+        n_done += len(sub)
+    secs = t_oct + t_pmc + t_fit * sample_cells / total_cells
+    detail = (f"oracle (C, FP64, OpenMP) on the level-{sl} subtree (0,0,0) = {sample_cells} cells "
+              f"({sample_cells / total_cells:.2e} of the grid): octree {t_oct:.2f} s, leaf pass on "
+              f"{n_done} of its {n_leaf} leaves x {len(w.thetas)} isovalue(s) extrapolated to {t_pmc:.2f} s, "
+              f"model build {t_fit:.2f} s amortised by the sample's share")
+    return sample_cells * len(w.thetas) / secs, secs, detail, M
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    from workloads import generate
+    w = generate(args.workload)
+    cfg = w.cfg
+    cores = O.num_threads()
+    M = None
+    vals = []
+    tot = 0.0
+    detail = ""
+    for s in range(args.warmup + args.steps):
+        v, secs, detail, M = oracle_sample(w, M)
+        if s >= args.warmup:
+            vals.append(v)
+            tot += secs
+    value = float(np.mean(vals))
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / max(args.steps, 1),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": workload_desc(cfg, w.thetas), "sample": detail},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": detail},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_12442_b200 import Context, config_args
+    from workloads import generate
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = generate(args.workload)
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    ncell = int(np.prod(cfg.cells))
+    field = torch.empty(ncell, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    slab = dict(slab_rank=rank, slab_count=world, slab_level=3) if world > 1 else {}
+    ctx = Context(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(host=None):
+        if host is None:
+            ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
+        else:
+            ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
+        leaves = 0
+        mc_ms = 0.0
+        for it, th in enumerate(w.thetas):
+            _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it, field=field)
+            leaves += n
+            mc_ms += ctx.stats()["mc_ms"]
+            if world > 1:
+                dist.reduce(field, 0, op=dist.ReduceOp.SUM)
+            if host is not None and rank == 0:
+                host[2].copy_(field, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+        return leaves, mc_ms
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.stats()["launches"]
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    leaves_tot = 0
+    mc_ms_tot = 0.0
+    st_phase = {"fit_ms": 0.0, "refine_ms": 0.0, "posterior_ms": 0.0, "chol_ms": 0.0, "mc_ms": 0.0}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.fill_(1)                      # L2 flush between timed steps (256 MB > 126 MB L2)
+        torch.cuda.synchronize()
+        e0.record()
+        leaves, mc_ms = step()
+        e1.record()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        leaves_tot += leaves
+        mc_ms_tot += mc_ms
+        s = ctx.stats()
+        for key in st_phase:
+            st_phase[key] += s[key] if key != "mc_ms" else 0.0
+    st_phase["mc_ms"] = mc_ms_tot
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ctx.stats()["launches"] - launches0
+    t = torch.tensor([total_ms, mc_ms_tot], dtype=torch.float64, device=dev)
+    lv = torch.tensor([leaves_tot, launches], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lv, op=dist.ReduceOp.SUM)
+    total_ms = float(t[0])
+    ms_step = total_ms / args.steps
+    cells_per_step = ncell * len(w.thetas)
+    value = cells_per_step / (ms_step / 1000.0)
+    leaves_step = float(lv[0]) / args.steps
+    samples_step = leaves_step * cfg.n_samples
+
+    # e2e: the same step through the C ABI with host (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(np.array(w.X)).pin_memory().numpy()
+        yh = torch.from_numpy(np.array(w.y)).pin_memory().numpy()
+        fh = torch.empty(ncell, dtype=torch.float32).pin_memory()
+        host = (Xh, yh, fh)
+        step(host)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step(host)
+        torch.cuda.synchronize()
+        barrier()
+        te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": cells_per_step / float(te[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes),
+               "d2h_bytes_per_step": int(fh.numel() * 4 * len(w.thetas)), "seconds_per_step": float(te[0])}
+
+    if rank != 0:
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+    # roofline of the dominant kernel (k_pmc): algorithmic lane-ops / measured time
+    mc_s = float(t[1]) / args.steps / 1000.0
+    peak = SM_COUNT * LANES_PER_SM_CLK * 1965e6 / 1e12          # T lane-op/s at the max SM clock
+    achieved = (samples_step / max(world, 1)) * ALG_OPS_PER_SAMPLE / mc_s / 1e12 if mc_s > 0 else None
+    traffic = load_traffic()
+    roofline = {"bound": "alu", "kernel": "k_pmc", "achieved": achieved, "peak": peak,
+                "unit": "Tlane-op/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "ops_per_sample": ALG_OPS_PER_SAMPLE,
+                "samples_per_s": samples_step / max(world, 1) / mc_s if mc_s > 0 else None,
+                "mc_share_of_step": mc_s / (ms_step / 1000.0),
+                "peak_note": "148 SMs x 128 lanes x 1.965 GHz issue slots (guide unit counts, max clock)"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            v, secs, detail, _ = oracle_sample(w)
+            cpu = {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle", "sample": detail}
+        except Exception as ex:  # the GPU number stands on its own
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                   "sample": f"failed: {ex}"}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
+           "config": {"workload": workload_desc(cfg, w.thetas), "cells": ncell, "m": cfg.m, "k": cfg.k,
+                      "n_samples": cfg.n_samples, "alpha": cfg.alpha, "max_depth": cfg.max_depth,
+                      "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                      "l2": "flushed between timed steps (256 MB write, outside the step events)"},
+           "end_to_end_octree_lcp_s": ms_step / 1000.0,
+           "leaf_cells_per_step": leaves_step, "pmc_leaf_cells_per_s": leaves_step / (ms_step / 1000.0),
+           "samples_per_step": samples_step,
+           "phase_ms_per_step": {k2: v2 / args.steps for k2, v2 in st_phase.items()},
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(float(lv[1])),
+           "clocks": clk}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -74,9 +74,13 @@ lcp_status_t point_marginals_impl(Ctx& c, const double* xyz, int64_t n, const in
   int32_t* bkt = c.cell_bucket.as<int32_t>();
   unsigned gr = (unsigned)((n + 255) / 256);
   if (bkt_in) CK(cudaMemcpyAsync(bkt, bkt_in, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c.stream));
-  else k_point_bucket<<<gr, 256, 0, c.stream>>>(c.g, xyz, n, bkt);
+  else {
+    k_point_bucket<<<gr, 256, 0, c.stream>>>(c.g, xyz, n, bkt);
+    ++c.n_launch;
+  }
   CK(group_by_bucket(c, bkt, n, c.perm.as<int64_t>()));
   k_gather_sorted<<<gr, 256, 0, c.stream>>>(bkt, c.perm.as<int64_t>(), n, bkt + n);
+  ++c.n_launch;
   CK(launch_marginals(c, Q_POINT, c.perm.as<int64_t>(), bkt + n, n, xyz, mu, var, 1, nullptr));
 #undef CK
   return check_device_errors(c);
@@ -264,6 +268,7 @@ lcp_status_t lcp_cell_posterior(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_
   lcp_status_t st = posterior_impl(c, cells_dev, n, c.post.as<double>());
   if (st != LCP_OK) return st;
   k_expand_post<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.post.as<double>(), n, mu_dev, cov_dev);
+  ++c.n_launch;
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_err(c, e, "expand");
   return check_device_errors(c);
 }
@@ -305,10 +310,12 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
   std::snprintf(tmp, sizeof tmp,
                 "\"fit_ms\": %.6f, \"refine_ms\": %.6f, \"posterior_ms\": %.6f, \"chol_ms\": %.6f, \"mc_ms\": %.6f, "
                 "\"scatter_ms\": %.6f, \"leaves\": %lld, \"pmc_cells\": %lld, \"pmc_samples\": %lld, "
-                "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld",
+                "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld, "
+                "\"launches\": %lld",
                 c.t.fit_ms, c.t.refine_ms, c.t.posterior_ms, c.t.chol_ms, c.t.mc_ms, c.t.scatter_ms,
                 (long long)c.n_leaves, (long long)c.last_pmc_cells, (long long)c.last_pmc_samples,
-                (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m);
+                (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m,
+                (long long)c.n_launch);
   s += tmp;
   auto arr = [&](const char* name, const std::vector<int64_t>& v) {
     s += ", \"";

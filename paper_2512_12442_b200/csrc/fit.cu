@@ -472,11 +472,14 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   unsigned gm = (unsigned)((m + 255) / 256);
   // a1
   k_obs_bin<<<gm, 256, 0, c.stream>>>(g, X, m, c.obs_bucket.as<int32_t>(), c.obs_key.as<uint64_t>());
+  ++c.n_launch;
   CK(group_by_bucket(c, c.obs_bucket.as<int32_t>(), m, c.obs_by_bucket.as<int64_t>()));
   k_bucket_ranges<<<(nbk + 255) / 256, 256, 0, c.stream>>>(c.gcount.as<int64_t>(), c.goff.as<int64_t>(), nbk,
                                                           c.bcount.as<int64_t>(), c.bstart.as<int64_t>());
+  ++c.n_launch;
   k_obs_rank<<<gm, 256, 0, c.stream>>>(c.obs_key.as<uint64_t>(), m, c.obs_sorted_key.as<uint64_t>(),
                                       c.obs_sorted_idx.as<int32_t>());
+  ++c.n_launch;
   CK(cudaGetLastError());
   // a2
   {
@@ -493,6 +496,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     k_knn<<<nbk, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, c.bstart.as<int64_t>(), c.bcount.as<int64_t>(),
                                               c.obs_by_bucket.as<int64_t>(), c.S.as<int32_t>(), list_dev,
                                               nfail_dev, r0);
+    ++c.n_launch;
     CK(cudaGetLastError());
     int nfail = 0;
     CK(cudaMemcpyAsync(&nfail, nfail_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -500,6 +504,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     c.knn_fallbacks = nfail;
     if (nfail > 0) {
       k_knn_brute<<<nfail, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, list_dev, c.S.as<int32_t>());
+      ++c.n_launch;
       CK(cudaGetLastError());
     }
   }
@@ -518,11 +523,13 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     k_bucket_factor<<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
                                                            c.bdata.as<double>(), c.bstride, gs, use_smem,
                                                            c.derr.as<int>());
+    ++c.n_launch;
     CK(cudaGetLastError());
   }
   // a4: observation marginals (grouped by bucket)
   k_gather_i32<<<gm, 256, 0, c.stream>>>(c.obs_bucket.as<int32_t>(), c.obs_by_bucket.as<int64_t>(), m,
                                          c.cell_bucket.as<int32_t>());
+  ++c.n_launch;
   CK(launch_marginals(c, Q_OBS, c.obs_by_bucket.as<int64_t>(), c.cell_bucket.as<int32_t>(), m, X,
                       c.obs_mu.as<double>(), c.obs_sd.as<double>(), 0, nullptr));
   cudaEventRecord(e1, c.stream);

@@ -351,6 +351,7 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
   k_marginals<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
                                                     out_mu, out_sd, write_var, c.vcache.as<double2>(),
                                                     c.vstate.as<uint8_t>(), c.derr.as<int>());
+  ++c.n_launch;
   return cudaGetLastError();
 }
 
@@ -368,6 +369,7 @@ cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* p
   unsigned grid = (unsigned)((n + tile - 1) / tile);
   k_cell_posterior<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
                                                          c.derr.as<int>());
+  ++c.n_launch;
   return cudaGetLastError();
 }
 

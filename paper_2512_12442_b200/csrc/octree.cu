@@ -286,6 +286,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
   k_obs_probs<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(c.obs_sorted_idx.as<int32_t>(), c.obs_mu.as<double>(),
                                                                  c.obs_sd.as<double>(), m, theta, c.plo.as<double>(),
                                                                  c.phi.as<double>());
+  ++c.n_launch;
   CK(c.front[0].ensure(sizeof(uint64_t)));
   uint64_t root = node_key(0, 0, 0);
   CK(cudaMemcpyAsync(c.front[0].p, &root, sizeof(uint64_t), cudaMemcpyHostToDevice, c.stream));
@@ -331,6 +332,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
                                             c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
                                             c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(),
                                             c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt);
+    ++c.n_launch;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
@@ -341,14 +343,17 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       int32_t* bkt_s = bkt + cap;
       unsigned gr = (unsigned)((nreq + 255) / 256);
       k_req_bucket<<<gr, 256, 0, c.stream>>>(g, c.req.as<int64_t>(), nreq, bkt);
+      ++c.n_launch;
       CK(group_by_bucket(c, bkt, nreq, c.perm.as<int64_t>()));
       k_gather_req<<<gr, 256, 0, c.stream>>>(c.req.as<int64_t>(), bkt, c.perm.as<int64_t>(), nreq,
                                              c.req_sorted.as<int64_t>(), bkt_s);
+      ++c.n_launch;
       CK(launch_marginals(c, Q_VERTEX, c.req_sorted.as<int64_t>(), bkt_s, nreq, nullptr, nullptr, nullptr, 0,
                           nullptr));
     }
     k_node_bound<<<gw, 256, 0, c.stream>>>(g, level, F, nF, theta, alpha, c.ncase.as<int8_t>(),
                                            c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>());
+    ++c.n_launch;
     lcp_node_rec_t* rec_out = nullptr;
     const bool keep = level < c.opts.keep_records;
     if (keep) {
@@ -359,8 +364,10 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     k_node_records<<<gt, 256, 0, c.stream>>>(level, F, nF, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
                                              c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(), rec_out,
                                              dcnt + 8);
+    ++c.n_launch;
     k_node_counts<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), slab_level, z0, z1,
                                             c.cnt.as<int64_t>());
+    ++c.n_launch;
     CK(exclusive_scan_i64(c, c.cnt.as<int64_t>(), c.offs.as<int64_t>(), nF, (int64_t*)(dcnt + 1)));
     CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
@@ -373,12 +380,14 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       CK(c.front[cur ^ 1].ensure(sizeof(uint64_t) * std::max<int64_t>(total, 1)));
       k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
                                        slab_level, z0, z1, c.front[cur ^ 1].as<uint64_t>(), nullptr);
+      ++c.n_launch;
       cur ^= 1;
       nF = total;
     } else {
       CK(c.leaves.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
       k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
                                        slab_level, z0, z1, nullptr, c.leaves.as<int64_t>());
+      ++c.n_launch;
       c.n_leaves = total;
       nF = 0;
     }

@@ -185,9 +185,11 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
   int32_t* bkt = c.cell_bucket.as<int32_t>();
   unsigned gr = (unsigned)((n + 255) / 256);
   k_cell_bucket<<<gr, 256, 0, c.stream>>>(c.g, cells, n, bkt, c.derr.as<int>());
+  ++c.n_launch;
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
   CK(cudaMemsetAsync(dcnt + 15, 0, sizeof(unsigned long long), c.stream));
   k_count_runs<<<gr, 256, 0, c.stream>>>(bkt, n, dcnt + 15);
+  ++c.n_launch;
   CK(cudaMemcpyAsync(c.h_counters + 15, dcnt + 15, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   int64_t runs = c.h_counters[15] + 1;
@@ -198,6 +200,7 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
     CK(group_by_bucket(c, bkt, n, c.perm.as<int64_t>()));
     int32_t* bs = bkt + n;
     k_gather_bkt<<<gr, 256, 0, c.stream>>>(bkt, c.perm.as<int64_t>(), n, bs);
+    ++c.n_launch;
     CK(launch_cell_posterior(c, cells, c.perm.as<int64_t>(), bs, n, post));
   }
 #undef CK
@@ -231,10 +234,12 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
     if (st != LCP_OK) return st;
     cudaEventRecord(c.ev[1], c.stream);
     k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(post, nn);
+    ++c.n_launch;
     cudaEventRecord(c.ev[2], c.stream);
     k_pmc<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, c.stream>>>(cells + s0, post, nn, theta, (uint32_t)N,
                                                                   (uint32_t)seed, (uint32_t)(seed >> 32), iso,
                                                                   out + s0);
+    ++c.n_launch;
     cudaEventRecord(c.ev[3], c.stream);
     CK(cudaGetLastError());
     CK(cudaEventSynchronize(c.ev[3]));
@@ -257,7 +262,10 @@ cudaError_t launch_scatter(Ctx& c, const int64_t* cells, const float* lcp, int64
   int64_t ncell = (int64_t)c.g.cells[0] * c.g.cells[1] * c.g.cells[2];
   cudaError_t e = cudaMemsetAsync(field, 0, sizeof(float) * ncell, c.stream);
   if (e != cudaSuccess) return e;
-  if (n > 0) k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cells, lcp, n, field);
+  if (n > 0) {
+    k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cells, lcp, n, field);
+    ++c.n_launch;
+  }
   return cudaGetLastError();
 }
 

@@ -101,8 +101,11 @@ cudaError_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t 
   if (e != cudaSuccess) return e;
   int64_t* bs = c.scan_tmp.as<int64_t>();
   k_scan_reduce<<<(unsigned)nb, SCAN_THREADS, 0, c.stream>>>(in, n, bs);
+  ++c.n_launch;
   k_scan_blocksums<<<1, SCAN_THREADS, 0, c.stream>>>(bs, nb, total_dev);
+  ++c.n_launch;
   k_scan_final<<<(unsigned)nb, SCAN_THREADS, 0, c.stream>>>(in, n, bs, out);
+  ++c.n_launch;
   return cudaGetLastError();
 }
 
@@ -146,9 +149,11 @@ cudaError_t group_by_bucket(Ctx& c, const int32_t* bucket_of_item, int64_t n, in
   cudaMemsetAsync(cnt, 0, sizeof(int64_t) * nbk, c.stream);
   unsigned grid = (unsigned)((n + 255) / 256);
   k_bucket_count<<<grid, 256, 0, c.stream>>>(bucket_of_item, n, cnt);
+  ++c.n_launch;
   e = exclusive_scan_i64(c, cnt, off, nbk, nullptr);
   if (e != cudaSuccess) return e;
   k_bucket_scatter<<<grid, 256, 0, c.stream>>>(bucket_of_item, n, off, perm_out);
+  ++c.n_launch;
   return cudaGetLastError();
 }
 
