@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
         if (var < a.var_err) atomicOr(derr, DERR_NUMERIC);
         double vf = var > a.var_floor ? var : a.var_floor;
         if (mode == Q_VERTEX) {
-          vcache[it] = make_double2(mu, sqrt(vf));
+          vcache[it] = make_double2(mu, 1.0 / (sqrt(vf) * SQRT2));   // (mu, 1 / (sigma sqrt 2))
         } else {
           out_mu[it] = mu;
           out_sd[it] = write_var ? var : sqrt(vf);

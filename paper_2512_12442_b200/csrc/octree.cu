@@ -72,36 +72,53 @@ __global__ void k_obs_probs(const int32_t* __restrict__ sidx, const double* __re
   phi[r] = 0.5 * erfc((theta - mu[o]) / s2);
 }
 
+// G lanes per node (G | 32): 1 at the finest level, up to a warp at coarse ones.
+template <int G>
+__device__ __forceinline__ double group_max(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int G>
+__device__ __forceinline__ double group_min(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int G>
 __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF,
                               const uint64_t* __restrict__ skey, const double* __restrict__ plo,
                               const double* __restrict__ phi, int64_t m, double alpha,
                               int8_t* __restrict__ ncase, int8_t* __restrict__ nref, double* __restrict__ np1,
                               double* __restrict__ np2, double* __restrict__ nU, uint32_t* __restrict__ vmask,
                               int64_t* __restrict__ req, unsigned long long* __restrict__ nreq) {
-  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (n >= nF) return;
-  int i, j, k;
-  node_unkey(front[n], i, j, k);
-  int h = g.lfull - level;
-  uint64_t mk = morton3(i, j, k);
+  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x % G;
+  const bool live = n < nF;
+  int i = 0, j = 0, k = 0;
+  if (live) node_unkey(front[n], i, j, k);
+  const int h = g.lfull - level;
   int64_t a = 0, b = 0;
-  if (lane == 0) {
+  if (live && sub == 0) {
+    uint64_t mk = morton3(i, j, k);
     a = lower_bound_u64(skey, m, mk << (3 * h));
     b = lower_bound_u64(skey, m, (mk + 1) << (3 * h));
   }
-  a = __shfl_sync(0xffffffffu, a, 0);
-  b = __shfl_sync(0xffffffffu, b, 0);
+  if (G > 1) {
+    a = __shfl_sync(0xffffffffu, a, 0, G);
+    b = __shfl_sync(0xffffffffu, b, 0, G);
+  }
   double p1 = -1.0, p2 = -1.0;
-  for (int64_t r = a + lane; r < b; r += 32) {
+  for (int64_t r = a + sub; r < b; r += G) {
     p1 = fmax(p1, plo[r]);
     p2 = fmax(p2, phi[r]);
   }
-  p1 = warp_max(p1);
-  p2 = warp_max(p2);
-  bool any = b > a;
-  int cs = !any ? 0 : ((p1 > alpha && p2 > alpha) ? 1 : (p2 <= alpha ? 2 : 3));
-  if (lane == 0) {
+  p1 = group_max<G>(p1);
+  p2 = group_max<G>(p2);
+  const bool any = b > a;
+  const int cs = !any ? 0 : ((p1 > alpha && p2 > alpha) ? 1 : (p2 <= alpha ? 2 : 3));
+  if (live && sub == 0) {
     ncase[n] = (int8_t)cs;
     np1[n] = p1;
     np2[n] = p2;
@@ -110,10 +127,10 @@ __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ fr
       nU[n] = 1.0;
     }
   }
-  if (cs == 1) return;
+  if (!live || cs == 1) return;
   Lattice L = node_lattice(g, h, i, j, k);
   int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
-  for (int64_t q = lane; q < nc; q += 32) {
+  for (int64_t q = sub; q < nc; q += G) {
     int64_t v = lattice_vertex(g, L, q);
     uint32_t bit = 1u << (v & 31);
     if (vmask[v >> 5] & bit) continue;
@@ -137,29 +154,30 @@ __global__ void k_gather_req(const int64_t* __restrict__ req, const int32_t* __r
   bkt_s[q] = bkt[p];
 }
 
+// vcache[v] = (mu_v, 1 / (sigma_v sqrt 2))
+template <int G>
 __global__ void k_node_bound(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF, double theta,
                              double alpha, const int8_t* __restrict__ ncase, const double2* __restrict__ vcache,
                              int8_t* __restrict__ nref, double* __restrict__ nU) {
-  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (n >= nF) return;
-  int cs = ncase[n];
-  if (cs == 1) return;
-  int i, j, k;
-  node_unkey(front[n], i, j, k);
-  int h = g.lfull - level;
+  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x % G;
+  const bool live = n < nF && ncase[n] != 1;
+  const int cs = live ? ncase[n] : 1;
+  int i = 0, j = 0, k = 0;
+  if (live) node_unkey(front[n], i, j, k);
+  const int h = g.lfull - level;
   Lattice L = node_lattice(g, h, i, j, k);
-  int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
+  int64_t nc = live ? (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2] : 0;
   double zmax = -INFINITY, zmin = INFINITY;
-  for (int64_t q = lane; q < nc; q += 32) {
+  for (int64_t q = sub; q < nc; q += G) {
     double2 ms = vcache[lattice_vertex(g, L, q)];
-    double z = (ms.x - theta) / (ms.y * SQRT2);
+    double z = (ms.x - theta) * ms.y;
     zmax = fmax(zmax, z);
     zmin = fmin(zmin, z);
   }
-  zmax = warp_max(zmax);
-  zmin = warp_min(zmin);
-  if (lane != 0) return;
+  zmax = group_max<G>(zmax);
+  zmin = group_min<G>(zmin);
+  if (!live || sub != 0) return;
   // Q_lo = max P(Y > th) = erfc(-zmax)/2, Q_hi = max P(Y < th) = erfc(zmin)/2
   double q_lo = 0.5 * erfc(-zmax), q_hi = 0.5 * erfc(zmin);
   double d = (double)(L.vmax[0] - L.base[0] + 1) * (double)(L.vmax[1] - L.base[1] + 1) *
@@ -182,21 +200,36 @@ __global__ void k_node_records(int level, const uint64_t* __restrict__ front, in
                                const double* __restrict__ np1, const double* __restrict__ np2,
                                const double* __restrict__ nU, lcp_node_rec_t* __restrict__ out,
                                unsigned long long* __restrict__ stats) {
+  __shared__ unsigned int s_cnt[5];
+  if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= nF) return;
-  if (out) {
+  bool live = n < nF;
+  int cs = live ? ncase[n] : -1;
+  bool rf = live && nref[n];
+  if (live && out) {
     lcp_node_rec_t r;
     node_unkey(front[n], r.i, r.j, r.k);
     r.level = level;
-    r.ncase = ncase[n];
-    r.refine = nref[n];
+    r.ncase = cs;
+    r.refine = rf;
     r.p1 = np1[n];
     r.p2 = np2[n];
     r.U = nU[n];
     out[n] = r;
   }
-  atomicAdd(&stats[ncase[n]], 1ull);
-  if (nref[n]) atomicAdd(&stats[4], 1ull);
+  // per-level statistics: warp ballots, one shared atomic per warp, one global per block
+  unsigned bq[5];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) bq[q] = __ballot_sync(0xffffffffu, cs == q);
+  bq[4] = __ballot_sync(0xffffffffu, rf);
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+      if (bq[q]) atomicAdd(&s_cnt[q], __popc(bq[q]));
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&stats[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
 
 // children / leaf counts of refined nodes
@@ -327,11 +360,18 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     CK(c.perm.ensure(sizeof(int64_t) * cap));
     CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * 16, c.stream));
     const uint64_t* F = c.front[cur].as<uint64_t>();
-    unsigned gw = (unsigned)((nF * 32 + 255) / 256);
-    k_node_prelim<<<gw, 256, 0, c.stream>>>(g, level, F, nF, c.obs_sorted_key.as<uint64_t>(), c.plo.as<double>(),
-                                            c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
-                                            c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(),
-                                            c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt);
+    const int G = h == 0 ? 1 : (h == 1 ? 4 : (h == 2 ? 8 : 32));
+    unsigned gw = (unsigned)((nF * G + 255) / 256);
+#define PRELIM(GG)                                                                                              \
+  k_node_prelim<GG><<<gw, 256, 0, c.stream>>>(g, level, F, nF, c.obs_sorted_key.as<uint64_t>(), c.plo.as<double>(), \
+                                               c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(),                \
+                                               c.nref.as<int8_t>(), c.np1.as<double>(), c.np2.as<double>(),       \
+                                               c.nU.as<double>(), c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt)
+    if (G == 1) PRELIM(1);
+    else if (G == 4) PRELIM(4);
+    else if (G == 8) PRELIM(8);
+    else PRELIM(32);
+#undef PRELIM
     ++c.n_launch;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
@@ -351,8 +391,14 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       CK(launch_marginals(c, Q_VERTEX, c.req_sorted.as<int64_t>(), bkt_s, nreq, nullptr, nullptr, nullptr, 0,
                           nullptr));
     }
-    k_node_bound<<<gw, 256, 0, c.stream>>>(g, level, F, nF, theta, alpha, c.ncase.as<int8_t>(),
-                                           c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>());
+#define BOUND(GG)                                                                                            \
+  k_node_bound<GG><<<gw, 256, 0, c.stream>>>(g, level, F, nF, theta, alpha, c.ncase.as<int8_t>(),             \
+                                              c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>())
+    if (G == 1) BOUND(1);
+    else if (G == 4) BOUND(4);
+    else if (G == 8) BOUND(8);
+    else BOUND(32);
+#undef BOUND
     ++c.n_launch;
     lcp_node_rec_t* rec_out = nullptr;
     const bool keep = level < c.opts.keep_records;

@@ -108,15 +108,23 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// u >= 2^-24 is a normal number: no denormal fix-up needed (MUFU.LG2 alone)
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
-// Box-Muller: (R cos 2 pi ub, R sin 2 pi ub), R = sqrt(-2 ln ua); the angle is
-// reduced to (-pi, pi) via ub - 1/2 (exact), which flips both signs.
+// Box-Muller: (R cos 2 pi ub, R sin 2 pi ub), R = sqrt(-2 ln ua).  The angle
+// is taken in (-pi, pi) as 2 pi (ub - 1/2), which flips both signs; with
+// F = 1 + (r mod 2^23) 2^-23 it is one FFMA: 2 pi F - 2 pi (3/2 - 2^-24).
 __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, float& z1) {
-  float ua = u23(ra), ub = u23(rb);
-  float r2 = fmaxf(-1.3862943611198906f * __log2f(ua), 0.0f);
+  float ua = u23(ra);
+  float fb = __uint_as_float(0x3f800000u | (rb & 0x7fffffu));
+  float r2 = fmaxf(-1.3862943611198906f * lg2_approx(ua), 0.0f);
   float nR = -sqrt_approx(r2);
   float s, co;
-  __sincosf(6.283185307179586f * (ub - 0.5f), &s, &co);
+  __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
   z0 = nR * co;
   z1 = nR * s;
 }
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(256) k_pmc(const int64_t* __restrict__ cells, 
   int64_t cell = cells[q];
   uint32_t c1 = (uint32_t)(uint64_t)cell, c2 = (uint32_t)((uint64_t)cell >> 32);
   uint32_t cnt = 0;
-  for (uint32_t s = lane; s < N; s += 32) {
+  auto sample = [&](uint32_t s) {
     uint32_t r[8];
     philox4x32_10(2u * s, c1, c2, iso, k0, k1, r[0], r[1], r[2], r[3]);
     philox4x32_10(2u * s + 1u, c1, c2, iso, k0, k1, r[4], r[5], r[6], r[7]);
@@ -158,7 +166,14 @@ __global__ void __launch_bounds__(256) k_pmc(const int64_t* __restrict__ cells, 
       mn = fminf(mn, y);
     }
     cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
+  };
+  // two independent samples per iteration for instruction-level parallelism
+  uint32_t s = lane;
+  for (; s + 32u < N; s += 64u) {
+    sample(s);
+    sample(s + 32u);
   }
+  if (s < N) sample(s);
   cnt = warp_sum(cnt);
   if (lane == 0) out[q] = (float)((double)cnt / (double)N);
 }
