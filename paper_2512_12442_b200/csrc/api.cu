@@ -311,11 +311,11 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
                 "\"fit_ms\": %.6f, \"refine_ms\": %.6f, \"posterior_ms\": %.6f, \"chol_ms\": %.6f, \"mc_ms\": %.6f, "
                 "\"scatter_ms\": %.6f, \"leaves\": %lld, \"pmc_cells\": %lld, \"pmc_samples\": %lld, "
                 "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld, "
-                "\"launches\": %lld",
+                "\"launches\": %lld, \"brick_runs\": %lld",
                 c.t.fit_ms, c.t.refine_ms, c.t.posterior_ms, c.t.chol_ms, c.t.mc_ms, c.t.scatter_ms,
                 (long long)c.n_leaves, (long long)c.last_pmc_cells, (long long)c.last_pmc_samples,
                 (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m,
-                (long long)c.n_launch);
+                (long long)c.n_launch, (long long)c.last_brick_runs);
   s += tmp;
   auto arr = [&](const char* name, const std::vector<int64_t>& v) {
     s += ", \"";

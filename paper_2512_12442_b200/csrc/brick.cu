@@ -1,0 +1,247 @@
+// brick.cu -- leaf posterior on 4x4x4-cell bricks with FP64 tensor cores.
+//
+// Eq. 1 on the bucket's local GP, evaluated once per VERTEX of
+// an aligned 4^3-cell brick instead of once per cell corner (the 8 corners of
+// the 64 cells of a brick are only 125 distinct vertices):
+//   phase 1  K[j][v] = k(x_j, v)            (k x 125, FP64, shared memory)
+//            mu_v    = m0 + sum_j K[j][v] alpha_j
+//   phase 2  V = L^-1 K                     (DMMA.8x8x4 FP64 tensor cores; L^-1 packed
+//                                            lower triangle staged in shared memory)
+//   phase 3  per leaf cell C of the brick:  Sigma_C = K_CC - V_C^T V_C  (DMMA, 8x8)
+// The leaf list of lcp_octree_refine is in Morton order, so the leaves of one
+// brick are contiguous; a CTA takes runs of one brick and keeps the bucket block
+// staged while consecutive runs stay in the same bucket.  Identical arithmetic
+// to k_cell_posterior up to FP64 rounding order.
+#include <algorithm>
+
+#include "ctx.h"
+
+namespace lcp {
+
+constexpr int BK = 4;                      // cells per brick side
+constexpr int NVB = (BK + 1) * (BK + 1) * (BK + 1);   // 125 vertices
+constexpr int NVP = 128;                    // padded vertex columns
+constexpr int VSTR = 136;                   // K/V row stride in doubles (64 mod 128 bytes: conflict-free B fragments)
+constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
+constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
+
+struct BrickArgs {
+  KernParams kp;
+  Geom g;
+  int k, kp8;                 // k and k rounded up to a multiple of 8
+  int64_t bstride;
+  const double* bdata;
+  double kcc[64];             // full 8x8 prior corner covariance
+  double var_err;
+};
+
+__device__ __forceinline__ void dmma(double a, double b, double& d0, double& d1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ int64_t brick_key(const Geom& g, int64_t cell) {
+  int i, j, k;
+  cell_ijk(g, cell, i, j, k);
+  return morton3(i / BK, j / BK, k / BK);
+}
+
+__global__ void k_brick_flags(Geom g, const int64_t* __restrict__ cells, int64_t n, int64_t* __restrict__ flag) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  flag[q] = (q == 0 || brick_key(g, cells[q]) != brick_key(g, cells[q - 1])) ? 1 : 0;
+}
+
+__global__ void k_brick_starts(const int64_t* __restrict__ flag, const int64_t* __restrict__ runidx, int64_t n,
+                               int64_t* __restrict__ start) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n && flag[q]) start[runidx[q]] = q;
+}
+
+__global__ void __launch_bounds__(BRICK_THREADS, 1)
+    k_brick_posterior(BrickArgs a, const int64_t* __restrict__ cells, const int64_t* __restrict__ run_start,
+                      int64_t nruns, unsigned long long* __restrict__ work, double* __restrict__ post,
+                      int* __restrict__ derr) {
+  extern __shared__ double smem[];
+  const int k = a.k, KP = a.kp8;
+  const int64_t tri = tri_size(k);
+  const int64_t head = (tri + 4 * (int64_t)k + 1) & ~1ll;
+  double* sLinv = smem;
+  double* sAlpha = smem + tri;
+  double* sX = sAlpha + k;
+  double* KV = smem + head;                     // KP x VSTR
+  double* sMu = KV + (int64_t)KP * VSTR;        // NVP
+  __shared__ int64_t s_r0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const Geom& g = a.g;
+  int staged = -1;
+  for (;;) {
+    if (tid == 0) s_r0 = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
+    __syncthreads();
+    const int64_t r0 = s_r0;
+    if (r0 >= nruns) break;
+    const int64_t r1 = min(nruns, r0 + BRICK_CHUNK);
+    for (int64_t r = r0; r < r1; ++r) {
+      const int64_t q0 = run_start[r], q1 = run_start[r + 1];
+      int ci, cj, ck;
+      cell_ijk(g, cells[q0], ci, cj, ck);
+      const int i0 = ci & ~(BK - 1), j0 = cj & ~(BK - 1), k0 = ck & ~(BK - 1);
+      const int b = bucket_id(g, vbucket_axis(g, 0, ci), vbucket_axis(g, 1, cj), vbucket_axis(g, 2, ck));
+      if (b != staged) {
+        const double2* src = reinterpret_cast<const double2*>(a.bdata + (int64_t)b * a.bstride);
+        double2* dst = reinterpret_cast<double2*>(smem);
+        for (int64_t t = tid; t < (a.bstride >> 1); t += BRICK_THREADS) dst[t] = __ldg(src + t);
+        staged = b;
+      }
+      __syncthreads();
+      // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding
+      for (int idx = tid; idx < KP * NVP; idx += BRICK_THREADS) {
+        int j = idx >> 7, v = idx & (NVP - 1);
+        double val = 0.0;
+        if (j < k && v < NVB) {
+          int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
+          int vi = min(i0 + va, g.cells[0]), vj = min(j0 + vb, g.cells[1]), vk = min(k0 + vc, g.cells[2]);
+          double r2 = kern_r2(a.kp, sX[j] - vpos(g, 0, vi), sX[k + j] - vpos(g, 1, vj),
+                              sX[2 * k + j] - vpos(g, 2, vk));
+          val = kern_from_r2(a.kp, r2);
+        }
+        KV[(int64_t)j * VSTR + v] = val;
+      }
+      __syncthreads();
+      if (tid < NVP) {
+        double s = 0.0;
+        for (int j = 0; j < k; ++j) s = fma(KV[(int64_t)j * VSTR + tid], sAlpha[j], s);
+        sMu[tid] = a.kp.m0 + s;
+      }
+      // phase 2: V = L^-1 K with DMMA; warp = (row set rs, column block cb)
+      const int rs = wid >> 2, cb = wid & 3;
+      const int nrt = KP >> 3;
+      double acc[4][4][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+      const int lr = lane >> 2, lc = lane & 3;
+      int last_rt = -1;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (rs + 4 * t < nrt) last_rt = rs + 4 * t;
+      const int jend = last_rt < 0 ? 0 : min(KP, 8 * last_rt + 8);
+      for (int j = 0; j < jend; j += 4) {
+        const int jj = j + lc;
+        double bf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bf[u] = KV[(int64_t)jj * VSTR + 32 * cb + 8 * u + lr];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int rt = rs + 4 * t;
+          if (rt >= nrt || 8 * rt + 7 < j) continue;   // warp-uniform: zero block of L^-1
+          const int i = 8 * rt + lr;
+          double af = (i < k && jj <= i) ? sLinv[tri_col(jj, k) + i - jj] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
+        }
+      }
+      __syncthreads();   // every warp has read K
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int rt = rs + 4 * t;
+        if (rt >= nrt) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          double2* d = reinterpret_cast<double2*>(KV + (int64_t)(8 * rt + lr) * VSTR + 32 * cb + 8 * u + 2 * lc);
+          *d = make_double2(acc[t][u][0], acc[t][u][1]);
+        }
+      }
+      __syncthreads();
+      // phase 3: Sigma_C = K_CC - V_C^T V_C per leaf cell (warp per cell)
+      for (int64_t q = q0 + wid; q < q1; q += BRICK_THREADS / 32) {
+        int64_t cell = cells[q];
+        int xi, xj, xk;
+        cell_ijk(g, cell, xi, xj, xk);
+        const int cr = lr;   // corner of this lane's A row / B column
+        const int lv = (xi - i0 + (cr & 1)) + (BK + 1) * ((xj - j0 + ((cr >> 1) & 1)) + (BK + 1) * (xk - k0 + (cr >> 2)));
+        double d0 = 0.0, d1 = 0.0;
+        for (int s = 0; s < KP; s += 4) {
+          double v = KV[(int64_t)(s + lc) * VSTR + lv];
+          dmma(v, v, d0, d1);
+        }
+        double* rec = post + 44 * q;
+        // lane holds D[cr][2 lc], D[cr][2 lc + 1]
+        const int c0 = 2 * lc, c1 = 2 * lc + 1;
+        if (c0 <= cr) {
+          double s0 = a.kcc[cr * 8 + c0] - d0;
+          rec[8 + cr * (cr + 1) / 2 + c0] = s0;
+          if (c0 == cr && s0 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+        }
+        if (c1 <= cr) {
+          double s1 = a.kcc[cr * 8 + c1] - d1;
+          rec[8 + cr * (cr + 1) / 2 + c1] = s1;
+          if (c1 == cr && s1 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+        }
+        if (lc == 0) rec[cr] = sMu[lv];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Returns true when the brick path handled the list (Morton-like order with
+// enough leaves per brick and k small enough for shared memory).
+bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err) {
+  err = cudaSuccess;
+  if (c.k > 128 || c.g.bs < BK) return false;
+  const int k = c.k;
+  const int kp8 = (k + 7) & ~7;
+  const int64_t tri = tri_size(k);
+  const int64_t head = (tri + 4 * (int64_t)k + 1) & ~1ll;
+  size_t smem = sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP);
+  if (smem > 227 * 1024) return false;
+  if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
+  if ((err = c.brick_idx.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
+  if ((err = c.counters.ensure(sizeof(unsigned long long) * 16)) != cudaSuccess) return false;
+  unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  unsigned gr = (unsigned)((n + 255) / 256);
+  k_brick_flags<<<gr, 256, 0, c.stream>>>(c.g, cells, n, c.brick_flag.as<int64_t>());
+  ++c.n_launch;
+  if ((err = exclusive_scan_i64(c, c.brick_flag.as<int64_t>(), c.brick_idx.as<int64_t>(), n,
+                                (int64_t*)(dcnt + 14))) != cudaSuccess)
+    return false;
+  if ((err = cudaMemcpyAsync(c.h_counters + 14, dcnt + 14, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream)) !=
+      cudaSuccess)
+    return false;
+  if ((err = cudaStreamSynchronize(c.stream)) != cudaSuccess) return false;
+  const int64_t nruns = c.h_counters[14];
+  if (n / std::max<int64_t>(nruns, 1) < 8) return false;   // too few leaves per brick: per-cell kernel
+  if ((err = c.brick_start.ensure(sizeof(int64_t) * (nruns + 1))) != cudaSuccess) return false;
+  int64_t* start = c.brick_start.as<int64_t>();
+  k_brick_starts<<<gr, 256, 0, c.stream>>>(c.brick_flag.as<int64_t>(), c.brick_idx.as<int64_t>(), n, start);
+  ++c.n_launch;
+  if ((err = cudaMemcpyAsync(start + nruns, &n, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream)) != cudaSuccess)
+    return false;
+  if ((err = cudaMemsetAsync(dcnt + 13, 0, sizeof(unsigned long long), c.stream)) != cudaSuccess) return false;
+  BrickArgs a;
+  a.kp = c.kp;
+  a.g = c.g;
+  a.k = k;
+  a.kp8 = kp8;
+  a.bstride = c.bstride;
+  a.bdata = c.bdata.as<double>();
+  for (int p = 0; p < 8; ++p)
+    for (int q = 0; q < 8; ++q) a.kcc[p * 8 + q] = c.kcc[p >= q ? p * (p + 1) / 2 + q : q * (q + 1) / 2 + p];
+  a.var_err = -1e-8 * c.kp.var;
+  if ((err = cudaFuncSetAttribute(k_brick_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return false;
+  int blocks_per_sm = smem <= 110 * 1024 ? 2 : 1;
+  unsigned grid = (unsigned)std::min<int64_t>((nruns + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count * blocks_per_sm);
+  k_brick_posterior<<<grid, BRICK_THREADS, smem, c.stream>>>(a, cells, start, nruns, dcnt + 13, post,
+                                                             c.derr.as<int>());
+  ++c.n_launch;
+  err = cudaGetLastError();
+  c.last_brick_runs = nruns;
+  return err == cudaSuccess;
+}
+
+}  // namespace lcp

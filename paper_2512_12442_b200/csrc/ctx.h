@@ -110,6 +110,8 @@ struct Ctx {
 
   // leaf pass scratch
   DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
+  DevBuf brick_flag, brick_idx, brick_start;
+  int64_t last_brick_runs = 0;   // brick runs of the last posterior (0: per-cell path)
 
   // host pinned staging for counters
   int64_t* h_counters = nullptr;
@@ -143,6 +145,7 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
                              int write_var, const int64_t* n_dev);
 cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* perm,
                                   const int32_t* bkt_sorted, int64_t n, double* post);
+bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err);
 
 lcp_status_t set_err(Ctx& c, lcp_status_t st, const std::string& msg);
 lcp_status_t cuda_err(Ctx& c, cudaError_t e, const char* where);

@@ -9,6 +9,8 @@
 //                (R5, R24).  LCP = count / N.
 //  a9  k_scatter : dense field, zero off the leaves.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "ctx.h"
 
@@ -201,6 +203,16 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
   unsigned gr = (unsigned)((n + 255) / 256);
   k_cell_bucket<<<gr, 256, 0, c.stream>>>(c.g, cells, n, bkt, c.derr.as<int>());
   ++c.n_launch;
+  c.last_brick_runs = 0;
+  static const bool force_cell = [] {
+    const char* v = std::getenv("LCP_POSTERIOR");
+    return v && std::strcmp(v, "cell") == 0;
+  }();
+  if (!force_cell) {
+    cudaError_t be;
+    if (brick_posterior(c, cells, n, post, be)) return LCP_OK;
+    if (be != cudaSuccess) return cuda_err(c, be, "brick posterior");
+  }
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
   CK(cudaMemsetAsync(dcnt + 15, 0, sizeof(unsigned long long), c.stream));
   k_count_runs<<<gr, 256, 0, c.stream>>>(bkt, n, dcnt + 15);

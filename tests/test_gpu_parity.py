@@ -82,6 +82,27 @@ def test_cell_posterior(name, dev):
     assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
 
 
+@pytest.mark.parametrize("name", ["c1", "t1", "t2", "c2", "c3", "c4"])
+def test_leaf_posterior_brick_path(name, dev):
+    # Morton-ordered leaf lists take the 4^3-brick DMMA path (brick.cu); check
+    # mu / Sigma of a sample of leaves against the oracle (R18, tau = 1e-5).
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    leaves = ctx.octree_refine(w.thetas[0], cfg.alpha, cfg.max_depth).clone()
+    mu_g, cov_g = ctx.cell_posterior(leaves)
+    st = ctx.stats()
+    lv = leaves.cpu().numpy()
+    sel = np.random.default_rng(7).choice(len(lv), min(300, len(lv)), replace=False)
+    mu_g, cov_g = mu_g.cpu().numpy()[sel], cov_g.cpu().numpy()[sel]
+    worst = (0.0, 0.0)
+    for q, c in enumerate(lv[sel]):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, cfg.variance, 1e-5)
+        worst = (max(worst[0], em), max(worst[1], ec))
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
+    assert st["brick_runs"] > 0 or cfg.k > 128 or name == "t1", st
+
+
 @pytest.mark.parametrize("name", ["c1", "t1", "t2", "c2", "c3"])
 def test_octree_node_sets(name, dev):
     w, ctx, M = _ctx(name, dev)
