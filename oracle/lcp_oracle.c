@@ -479,20 +479,31 @@ int64_t orc_mc_count(const double* mu, const double* L, double theta, int64_t n_
     return count;
 }
 
+/* R13: the 8x8 factor is taken in the corner order PI8 = (0,3,5,6,1,2,4,7) --
+ * the even-parity corners (a tetrahedron) first, then the odd ones -- and normal
+ * z_i drives corner PI8[i]: y_PI8[i] = mu_PI8[i] + sum_{d<=i} L'_{id} z_d with
+ * L' = chol(Sigma[PI8][PI8]).  Any square root of Sigma samples the same
+ * 8-variate Gaussian; the crossing test is order-free. */
+static const int PI8[8] = {0, 3, 5, 6, 1, 2, 4, 7};
+
 int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double theta,
                   int64_t n_samples, uint64_t seed, uint32_t iso_index, double* lcp_out) {
     if (n_samples < 1) return ORC_EINVAL;
     int status = ORC_OK;
 #pragma omp parallel for schedule(dynamic, 16)
     for (int64_t q = 0; q < n; ++q) {
-        double mu[8], cov[64], L[64];
+        double mu[8], cov[64], L[64], mup[8], covp[64];
         int st = orc_cell_posterior(M, cells[q], mu, cov);
         if (st != ORC_OK) {
 #pragma omp critical
             status = st;
         }
-        orc_chol8(cov, L);
-        lcp_out[q] = (double)orc_mc_count(mu, L, theta, n_samples, seed, cells[q], iso_index) /
+        for (int i = 0; i < 8; ++i) {
+            mup[i] = mu[PI8[i]];
+            for (int j = 0; j < 8; ++j) covp[i * 8 + j] = cov[PI8[i] * 8 + PI8[j]];
+        }
+        orc_chol8(covp, L);
+        lcp_out[q] = (double)orc_mc_count(mup, L, theta, n_samples, seed, cells[q], iso_index) /
                      (double)n_samples;
     }
     return status;

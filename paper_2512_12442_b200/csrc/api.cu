@@ -145,7 +145,8 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.obs_sd, &c.plo, &c.phi, &c.derr, &c.knn_fail, &c.vcache, &c.vstate, &c.front[0],
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
-                    &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp};
+                    &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)
@@ -311,11 +312,12 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
                 "\"fit_ms\": %.6f, \"refine_ms\": %.6f, \"posterior_ms\": %.6f, \"chol_ms\": %.6f, \"mc_ms\": %.6f, "
                 "\"scatter_ms\": %.6f, \"leaves\": %lld, \"pmc_cells\": %lld, \"pmc_samples\": %lld, "
                 "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld, "
-                "\"launches\": %lld, \"brick_runs\": %lld",
+                "\"launches\": %lld, \"brick_runs\": %lld, \"pmc_phase2_samples\": %lld",
                 c.t.fit_ms, c.t.refine_ms, c.t.posterior_ms, c.t.chol_ms, c.t.mc_ms, c.t.scatter_ms,
                 (long long)c.n_leaves, (long long)c.last_pmc_cells, (long long)c.last_pmc_samples,
                 (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m,
-                (long long)c.n_launch, (long long)c.last_brick_runs);
+                (long long)c.n_launch, (long long)c.last_brick_runs,
+                (long long)c.last_pmc_phase2);
   s += tmp;
   auto arr = [&](const char* name, const std::vector<int64_t>& v) {
     s += ", \"";

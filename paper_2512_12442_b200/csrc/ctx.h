@@ -111,6 +111,8 @@ struct Ctx {
   // leaf pass scratch
   DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
   DevBuf brick_flag, brick_idx, brick_start;
+  DevBuf pmc_counters;           // [0]: samples finished in phase 2 of k_pmc
+  int64_t last_pmc_phase2 = 0;
   int64_t last_brick_runs = 0;   // brick runs of the last posterior (0: per-cell path)
 
   // host pinned staging for counters

@@ -46,14 +46,27 @@ __global__ void k_gather_bkt(const int32_t* __restrict__ bkt, const int64_t* __r
 }
 
 // a8: in-place: rec = [mu (8 double) | Sigma packed (36 double)] ->
-//                     [mu (8 double) | L packed row-major lower (36 float) | unused]
+//                     [mu_pi (8 double) | L' packed row-major lower (36 float) | unused]
+// with L' = chol(Sigma[pi][pi]) in the corner order pi = (0,3,5,6,1,2,4,7) (R13b):
+// even-parity corners first, so the last four corners have small conditional
+// spread given the first four (used by the exact early decision of k_pmc).
 __global__ void k_chol8(double* __restrict__ post, int64_t n) {
+  constexpr int kPi8[8] = {0, 3, 5, 6, 1, 2, 4, 7};
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   double* rec = post + 44 * q;
-  double S[36];
+  double S[36], mu[8];
 #pragma unroll
-  for (int p = 0; p < 36; ++p) S[p] = rec[8 + p];
+  for (int i = 0; i < 8; ++i) {
+    const int pi = kPi8[i];
+    mu[i] = rec[pi];
+#pragma unroll
+    for (int j = 0; j <= i; ++j) {
+      const int pj = kPi8[j];
+      const int r = pi > pj ? pi : pj, c = pi > pj ? pj : pi;
+      S[i * (i + 1) / 2 + j] = rec[8 + r * (r + 1) / 2 + c];
+    }
+  }
   double md = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c) md = fmax(md, S[c * (c + 3) / 2]);
@@ -76,6 +89,8 @@ __global__ void k_chol8(double* __restrict__ post, int64_t n) {
       L[i * (i + 1) / 2 + j] = live ? t * inv : 0.0;
     }
   }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rec[i] = mu[i];
   float* Lf = reinterpret_cast<float*>(rec + 8);
 #pragma unroll
   for (int p = 0; p < 36; ++p) Lf[p] = (float)L[p];
@@ -131,53 +146,158 @@ __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, 
   z1 = nR * s;
 }
 
-__global__ void __launch_bounds__(256) k_pmc(const int64_t* __restrict__ cells, const double* __restrict__ post,
-                                             int64_t n, double theta, uint32_t N, uint32_t k0, uint32_t k1,
-                                             uint32_t iso, float* __restrict__ out) {
-  int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (q >= n) return;
-  const double* rec = post + 44 * q;
-  float m[8];
+// Largest |z| Box-Muller can produce: u_a >= 2^-24 gives R <= sqrt(48 ln 2) = 5.7668;
+// 5.7684 adds the lg2/sqrt approximation error.
+constexpr float ZMAX = 5.7684f;
+constexpr int PMC_WARPS = 8;
+constexpr int QCAP = 64;            // pending samples per warp
+
+// k_pmc: exact two-phase evaluation of the PMC count.
+// Phase 1 draws the first Philox block (normals z0..z3) of sample s and forms
+// y_c exactly for the first four corners and y_c - R_c for the other four,
+// where |R_c| = |sum_{d>=4} L_cd z_d| <= B_c = ZMAX sum_{d>=4} |L_cd| (+ rounding
+// slack).  If the bounds already fix the outcome (all below / all above / one
+// surely >= 0 and one surely <= 0) the sample is counted; otherwise it is queued
+// in shared memory and, 32 at a time, phase 2 draws the second Philox block
+// (z4..z7) and finishes the sample.  Every sample is decided exactly as the
+// one-pass FP32 evaluation decides it; the count is the same estimator.
+__global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restrict__ cells,
+                                                        const double* __restrict__ post, int64_t n, double theta,
+                                                        uint32_t N, uint32_t k0, uint32_t k1, uint32_t iso,
+                                                        float* __restrict__ out,
+                                                        unsigned long long* __restrict__ n_phase2) {
+  __shared__ float sq_y[PMC_WARPS][6][QCAP];   // yp4..yp7, max(y0..y3), min(y0..y3)
+  __shared__ uint32_t sq_s[PMC_WARPS][QCAP];
+  __shared__ unsigned int s_p2;
+  if (threadIdx.x == 0) s_p2 = 0;
+  __syncthreads();
+  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool live = q < n;
+  float m[8], L[36], B[4];
+  uint32_t c1 = 0, c2 = 0;
+  if (live) {
+    const double* rec = post + 44 * q;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) m[c] = (float)(rec[c] - theta);
-  const float4* L4 = reinterpret_cast<const float4*>(rec + 8);
-  float L[36];
+    for (int c = 0; c < 8; ++c) m[c] = (float)(rec[c] - theta);
+    const float4* L4 = reinterpret_cast<const float4*>(rec + 8);
 #pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    float4 v = L4[t];
-    L[4 * t] = v.x; L[4 * t + 1] = v.y; L[4 * t + 2] = v.z; L[4 * t + 3] = v.w;
-  }
-  int64_t cell = cells[q];
-  uint32_t c1 = (uint32_t)(uint64_t)cell, c2 = (uint32_t)((uint64_t)cell >> 32);
-  uint32_t cnt = 0;
-  auto sample = [&](uint32_t s) {
-    uint32_t r[8];
-    philox4x32_10(2u * s, c1, c2, iso, k0, k1, r[0], r[1], r[2], r[3]);
-    philox4x32_10(2u * s + 1u, c1, c2, iso, k0, k1, r[4], r[5], r[6], r[7]);
-    float z[8];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) box_muller(r[2 * p], r[2 * p + 1], z[2 * p], z[2 * p + 1]);
-    float mx = -INFINITY, mn = INFINITY;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float y = m[c];
-#pragma unroll
-      for (int d = 0; d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
-      mx = fmaxf(mx, y);
-      mn = fminf(mn, y);
+    for (int t = 0; t < 9; ++t) {
+      float4 v = L4[t];
+      L[4 * t] = v.x; L[4 * t + 1] = v.y; L[4 * t + 2] = v.z; L[4 * t + 3] = v.w;
     }
-    cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
-  };
-  // two independent samples per iteration for instruction-level parallelism
-  uint32_t s = lane;
-  for (; s + 32u < N; s += 64u) {
-    sample(s);
-    sample(s + 32u);
+    int64_t cell = cells[q];
+    c1 = (uint32_t)(uint64_t)cell;
+    c2 = (uint32_t)((uint64_t)cell >> 32);
+#pragma unroll
+    for (int c = 4; c < 8; ++c) {
+      float tail = 0.0f, all = fabsf(m[c]);
+#pragma unroll
+      for (int d = 0; d <= c; ++d) {
+        all += ZMAX * fabsf(L[c * (c + 1) / 2 + d]);
+        if (d >= 4) tail += fabsf(L[c * (c + 1) / 2 + d]);
+      }
+      B[c - 4] = ZMAX * tail * (1.0f + 1e-5f) + 1e-6f * all;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) m[c] = 0.0f;
+#pragma unroll
+    for (int p = 0; p < 36; ++p) L[p] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) B[c] = 0.0f;
   }
-  if (s < N) sample(s);
+  const uint32_t Nl = live ? N : 0u;
+  uint32_t cnt = 0;
+  int qn = 0;   // warp-uniform queue length
+  unsigned p2 = 0;
+  float* qy = &sq_y[wid][0][0];
+  uint32_t* qs = sq_s[wid];
+  auto phase2 = [&](int slot, bool act) {
+    if (act) {
+      uint32_t s = qs[slot];
+      uint32_t r4, r5, r6, r7;
+      philox4x32_10(2u * s + 1u, c1, c2, iso, k0, k1, r4, r5, r6, r7);
+      float z[8];
+      box_muller(r4, r5, z[4], z[5]);
+      box_muller(r6, r7, z[6], z[7]);
+      float mx = qy[4 * QCAP + slot], mn = qy[5 * QCAP + slot];
+#pragma unroll
+      for (int c = 4; c < 8; ++c) {
+        float y = qy[(c - 4) * QCAP + slot];
+#pragma unroll
+        for (int d = 4; d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
+        mx = fmaxf(mx, y);
+        mn = fminf(mn, y);
+      }
+      cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
+    }
+  };
+  for (uint32_t base = 0; base < Nl; base += 32u) {
+    const uint32_t s = base + lane;
+    bool pend = false;
+    float yp[8], mx03 = 0.f, mn03 = 0.f;
+    if (s < Nl) {
+      uint32_t r0, r1, r2, r3;
+      philox4x32_10(2u * s, c1, c2, iso, k0, k1, r0, r1, r2, r3);
+      float z[4];
+      box_muller(r0, r1, z[0], z[1]);
+      box_muller(r2, r3, z[2], z[3]);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float y = m[c];
+#pragma unroll
+        for (int d = 0; d < 4 && d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
+        yp[c] = y;
+      }
+      mx03 = fmaxf(fmaxf(yp[0], yp[1]), fmaxf(yp[2], yp[3]));
+      mn03 = fminf(fminf(yp[0], yp[1]), fminf(yp[2], yp[3]));
+      float hi_max = mx03, lo_min = mn03, lo_max = mx03, hi_min = mn03;
+#pragma unroll
+      for (int c = 4; c < 8; ++c) {
+        float lo = yp[c] - B[c - 4], hi = yp[c] + B[c - 4];
+        hi_max = fmaxf(hi_max, hi);
+        lo_min = fminf(lo_min, lo);
+        lo_max = fmaxf(lo_max, lo);
+        hi_min = fminf(hi_min, hi);
+      }
+      const bool below = hi_max < 0.0f, above = lo_min > 0.0f;
+      const bool cross = lo_max >= 0.0f && hi_min <= 0.0f;
+      if (below || above || cross) cnt += cross ? 1u : 0u;
+      else pend = true;
+    }
+    const unsigned pm = __ballot_sync(0xffffffffu, pend);
+    if (pend) {
+      const int slot = qn + __popc(pm & ((1u << lane) - 1u));
+      qs[slot] = s;
+      qy[0 * QCAP + slot] = yp[4];
+      qy[1 * QCAP + slot] = yp[5];
+      qy[2 * QCAP + slot] = yp[6];
+      qy[3 * QCAP + slot] = yp[7];
+      qy[4 * QCAP + slot] = mx03;
+      qy[5 * QCAP + slot] = mn03;
+    }
+    qn += __popc(pm);
+    if (qn >= 32) {
+      __syncwarp();
+      qn -= 32;
+      phase2(qn + lane, true);
+      p2 += 32;
+      __syncwarp();
+    }
+  }
+  if (qn > 0) {
+    __syncwarp();
+    phase2(lane, lane < qn);
+    p2 += qn;
+  }
   cnt = warp_sum(cnt);
-  if (lane == 0) out[q] = (float)((double)cnt / (double)N);
+  if (live && lane == 0) {
+    out[q] = (float)((double)cnt / (double)N);
+    atomicAdd(&s_p2, p2);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_p2) atomicAdd(n_phase2, (unsigned long long)s_p2);
 }
 
 __global__ void k_scatter(const int64_t* __restrict__ cells, const float* __restrict__ lcp, int64_t n,
@@ -252,6 +372,8 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
   }
   int64_t chunk = std::min(n, PMC_CHUNK);
   CK(c.post.ensure(sizeof(double) * 44 * chunk));
+  CK(c.pmc_counters.ensure(sizeof(unsigned long long) * 2));
+  CK(cudaMemsetAsync(c.pmc_counters.p, 0, sizeof(unsigned long long) * 2, c.stream));
   double* post = c.post.as<double>();
   float tp = 0, tc = 0, tm = 0;
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
@@ -263,9 +385,9 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
     k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(post, nn);
     ++c.n_launch;
     cudaEventRecord(c.ev[2], c.stream);
-    k_pmc<<<(unsigned)((nn * 32 + 255) / 256), 256, 0, c.stream>>>(cells + s0, post, nn, theta, (uint32_t)N,
-                                                                  (uint32_t)seed, (uint32_t)(seed >> 32), iso,
-                                                                  out + s0);
+    k_pmc<<<(unsigned)((nn + PMC_WARPS - 1) / PMC_WARPS), PMC_WARPS * 32, 0, c.stream>>>(
+        cells + s0, post, nn, theta, (uint32_t)N, (uint32_t)seed, (uint32_t)(seed >> 32), iso, out + s0,
+        c.pmc_counters.as<unsigned long long>());
     ++c.n_launch;
     cudaEventRecord(c.ev[3], c.stream);
     CK(cudaGetLastError());
@@ -281,6 +403,7 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
   c.t.mc_ms = tm;
   c.last_pmc_cells = n;
   c.last_pmc_samples = n * N;
+  CK(cudaMemcpy(&c.last_pmc_phase2, c.pmc_counters.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
 #undef CK
   return check_device_errors(c);
 }
