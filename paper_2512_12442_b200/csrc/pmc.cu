@@ -96,21 +96,25 @@ __global__ void k_chol8(double* __restrict__ post, int64_t n) {
   for (int p = 0; p < 36; ++p) Lf[p] = (float)L[p];
 }
 
-__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                              uint32_t k1, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+// Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9, passed as a kernel
+// parameter so that every XOR takes its key straight from the constant bank.
+struct PhiloxKeys {
+  uint32_t k[20];
+};
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                              const PhiloxKeys& K, uint32_t& r0, uint32_t& r1, uint32_t& r2,
                                               uint32_t& r3) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
     uint64_t p0 = (uint64_t)0xD2511F53u * c0;
     uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ K.k[2 * i];
+    uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ K.k[2 * i + 1];
     c0 = n0;
     c1 = (uint32_t)p1;
     c2 = n2;
     c3 = (uint32_t)p0;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
   }
   r0 = c0; r1 = c1; r2 = c2; r3 = c3;
 }
@@ -163,7 +167,7 @@ constexpr int QCAP = 64;            // pending samples per warp
 // one-pass FP32 evaluation decides it; the count is the same estimator.
 __global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restrict__ cells,
                                                         const double* __restrict__ post, int64_t n, double theta,
-                                                        uint32_t N, uint32_t k0, uint32_t k1, uint32_t iso,
+                                                        uint32_t N, const PhiloxKeys K, uint32_t iso,
                                                         float* __restrict__ out,
                                                         unsigned long long* __restrict__ n_phase2) {
   __shared__ float sq_y[PMC_WARPS][6][QCAP];   // yp4..yp7, max(y0..y3), min(y0..y3)
@@ -213,11 +217,53 @@ __global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restric
   unsigned p2 = 0;
   float* qy = &sq_y[wid][0][0];
   uint32_t* qs = sq_s[wid];
+  // phase 1 of sample s: returns true (and the stash) if the sample is undecided
+  auto phase1 = [&](uint32_t s, float (&yq)[6]) -> bool {
+    uint32_t r0, r1, r2, r3;
+    philox4x32_10(2u * s, c1, c2, iso, K, r0, r1, r2, r3);
+    float z[4];
+    box_muller(r0, r1, z[0], z[1]);
+    box_muller(r2, r3, z[2], z[3]);
+    float yp[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float y = m[c];
+#pragma unroll
+      for (int d = 0; d < 4 && d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
+      yp[c] = y;
+    }
+    const float mx03 = fmaxf(fmaxf(yp[0], yp[1]), fmaxf(yp[2], yp[3]));
+    const float mn03 = fminf(fminf(yp[0], yp[1]), fminf(yp[2], yp[3]));
+    float hi_max = mx03, lo_min = mn03, lo_max = mx03, hi_min = mn03;
+#pragma unroll
+    for (int c = 4; c < 8; ++c) {
+      const float lo = yp[c] - B[c - 4], hi = yp[c] + B[c - 4];
+      hi_max = fmaxf(hi_max, hi);
+      lo_min = fminf(lo_min, lo);
+      lo_max = fmaxf(lo_max, lo);
+      hi_min = fminf(hi_min, hi);
+    }
+    const bool cross = lo_max >= 0.0f && hi_min <= 0.0f;
+    const bool decided = hi_max < 0.0f || lo_min > 0.0f || cross;
+    cnt += cross ? 1u : 0u;
+    yq[0] = yp[4]; yq[1] = yp[5]; yq[2] = yp[6]; yq[3] = yp[7]; yq[4] = mx03; yq[5] = mn03;
+    return !decided;
+  };
+  auto push = [&](bool pend, uint32_t s, const float (&yq)[6]) {
+    const unsigned pm = __ballot_sync(0xffffffffu, pend);
+    if (pend) {
+      const int slot = qn + __popc(pm & ((1u << lane) - 1u));
+      qs[slot] = s;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) qy[t * QCAP + slot] = yq[t];
+    }
+    qn += __popc(pm);
+  };
   auto phase2 = [&](int slot, bool act) {
     if (act) {
       uint32_t s = qs[slot];
       uint32_t r4, r5, r6, r7;
-      philox4x32_10(2u * s + 1u, c1, c2, iso, k0, k1, r4, r5, r6, r7);
+      philox4x32_10(2u * s + 1u, c1, c2, iso, K, r4, r5, r6, r7);
       float z[8];
       box_muller(r4, r5, z[4], z[5]);
       box_muller(r6, r7, z[6], z[7]);
@@ -233,51 +279,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restric
       cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
     }
   };
-  for (uint32_t base = 0; base < Nl; base += 32u) {
-    const uint32_t s = base + lane;
-    bool pend = false;
-    float yp[8], mx03 = 0.f, mn03 = 0.f;
-    if (s < Nl) {
-      uint32_t r0, r1, r2, r3;
-      philox4x32_10(2u * s, c1, c2, iso, k0, k1, r0, r1, r2, r3);
-      float z[4];
-      box_muller(r0, r1, z[0], z[1]);
-      box_muller(r2, r3, z[2], z[3]);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        float y = m[c];
-#pragma unroll
-        for (int d = 0; d < 4 && d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
-        yp[c] = y;
-      }
-      mx03 = fmaxf(fmaxf(yp[0], yp[1]), fmaxf(yp[2], yp[3]));
-      mn03 = fminf(fminf(yp[0], yp[1]), fminf(yp[2], yp[3]));
-      float hi_max = mx03, lo_min = mn03, lo_max = mx03, hi_min = mn03;
-#pragma unroll
-      for (int c = 4; c < 8; ++c) {
-        float lo = yp[c] - B[c - 4], hi = yp[c] + B[c - 4];
-        hi_max = fmaxf(hi_max, hi);
-        lo_min = fminf(lo_min, lo);
-        lo_max = fmaxf(lo_max, lo);
-        hi_min = fminf(hi_min, hi);
-      }
-      const bool below = hi_max < 0.0f, above = lo_min > 0.0f;
-      const bool cross = lo_max >= 0.0f && hi_min <= 0.0f;
-      if (below || above || cross) cnt += cross ? 1u : 0u;
-      else pend = true;
-    }
-    const unsigned pm = __ballot_sync(0xffffffffu, pend);
-    if (pend) {
-      const int slot = qn + __popc(pm & ((1u << lane) - 1u));
-      qs[slot] = s;
-      qy[0 * QCAP + slot] = yp[4];
-      qy[1 * QCAP + slot] = yp[5];
-      qy[2 * QCAP + slot] = yp[6];
-      qy[3 * QCAP + slot] = yp[7];
-      qy[4 * QCAP + slot] = mx03;
-      qy[5 * QCAP + slot] = mn03;
-    }
-    qn += __popc(pm);
+  auto drain = [&]() {
     if (qn >= 32) {
       __syncwarp();
       qn -= 32;
@@ -285,6 +287,25 @@ __global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restric
       p2 += 32;
       __syncwarp();
     }
+  };
+  uint32_t base = 0;
+  // two samples per lane per iteration (instruction-level parallelism)
+  for (; base + 64u <= Nl; base += 64u) {
+    float ya[6], yb[6];
+    const bool pa = phase1(base + lane, ya);
+    const bool pb = phase1(base + 32u + lane, yb);
+    push(pa, base + lane, ya);
+    drain();
+    push(pb, base + 32u + lane, yb);
+    drain();
+  }
+  for (; base < Nl; base += 32u) {
+    float ya[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const uint32_t s = base + lane;
+    bool pa = false;
+    if (s < Nl) pa = phase1(s, ya);
+    push(pa, s, ya);
+    drain();
   }
   if (qn > 0) {
     __syncwarp();
@@ -376,6 +397,11 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
   CK(cudaMemsetAsync(c.pmc_counters.p, 0, sizeof(unsigned long long) * 2, c.stream));
   double* post = c.post.as<double>();
   float tp = 0, tc = 0, tm = 0;
+  PhiloxKeys keys;
+  for (int r = 0; r < 10; ++r) {
+    keys.k[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
+    keys.k[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+  }
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     int64_t nn = std::min(chunk, n - s0);
     cudaEventRecord(c.ev[0], c.stream);
@@ -386,8 +412,7 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
     ++c.n_launch;
     cudaEventRecord(c.ev[2], c.stream);
     k_pmc<<<(unsigned)((nn + PMC_WARPS - 1) / PMC_WARPS), PMC_WARPS * 32, 0, c.stream>>>(
-        cells + s0, post, nn, theta, (uint32_t)N, (uint32_t)seed, (uint32_t)(seed >> 32), iso, out + s0,
-        c.pmc_counters.as<unsigned long long>());
+        cells + s0, post, nn, theta, (uint32_t)N, keys, iso, out + s0, c.pmc_counters.as<unsigned long long>());
     ++c.n_launch;
     cudaEventRecord(c.ev[3], c.stream);
     CK(cudaGetLastError());
