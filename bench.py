@@ -28,9 +28,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PMC LCP cells/sec"
 UNIT = "cells/s"
-# minimal per-sample op mix of k_pmc: Philox4x32-10 x2 = 80,
-# uniforms 16, Box-Muller 4 x 11 = 44 (16 MUFU), L z + mu 36, crossing test 16
-ALG_OPS_PER_SAMPLE = 192
+# minimal op mix of the two-phase k_pmc, in issue slots (lane-ops):
+#   phase 1, every sample : Philox4x32-10 40, 2 Box-Muller pairs 26 (8 MUFU),
+#                           partial L z 26 FFMA, bounds 8, min/max 12, decision 5, queue 3  = 120
+#   phase 2, queued sample: Philox 40, 2 Box-Muller pairs 26, 10 FFMA, min/max 6,
+#                           decision 3, queue store + load 14                              =  99
+OPS_PHASE1 = 120
+OPS_PHASE2 = 99
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128
 
@@ -208,22 +212,26 @@ def run_ours(args):
             dist.barrier()
 
     def step(host=None):
+        """fit + run_field for every isovalue; returns (leaves, mc_ms, phase-2 samples)."""
         if host is None:
             ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
         else:
             ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
         leaves = 0
         mc_ms = 0.0
+        p2 = 0
         for it, th in enumerate(w.thetas):
             _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it, field=field)
             leaves += n
-            mc_ms += ctx.stats()["mc_ms"]
+            st = ctx.stats()
+            mc_ms += st["mc_ms"]
+            p2 += st["pmc_phase2_samples"]
             if world > 1:
                 dist.reduce(field, 0, op=dist.ReduceOp.SUM)
             if host is not None and rank == 0:
                 host[2].copy_(field, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
-        return leaves, mc_ms
+        return leaves, mc_ms, p2
 
     for _ in range(args.warmup):
         step()
@@ -236,6 +244,7 @@ def run_ours(args):
     total_ms = 0.0
     leaves_tot = 0
     mc_ms_tot = 0.0
+    p2_tot = 0
     st_phase = {"fit_ms": 0.0, "refine_ms": 0.0, "posterior_ms": 0.0, "chol_ms": 0.0, "mc_ms": 0.0}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -243,12 +252,13 @@ def run_ours(args):
         flush.fill_(1)                      # L2 flush between timed steps (256 MB > 126 MB L2)
         torch.cuda.synchronize()
         e0.record()
-        leaves, mc_ms = step()
+        leaves, mc_ms, p2 = step()
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
         leaves_tot += leaves
         mc_ms_tot += mc_ms
+        p2_tot += p2
         s = ctx.stats()
         for key in st_phase:
             st_phase[key] += s[key] if key != "mc_ms" else 0.0
@@ -258,7 +268,7 @@ def run_ours(args):
     clk = clocks.stop()
     launches = ctx.stats()["launches"] - launches0
     t = torch.tensor([total_ms, mc_ms_tot], dtype=torch.float64, device=dev)
-    lv = torch.tensor([leaves_tot, launches], dtype=torch.float64, device=dev)
+    lv = torch.tensor([leaves_tot, launches, p2_tot], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(lv, op=dist.ReduceOp.SUM)
@@ -297,11 +307,14 @@ def run_ours(args):
     # roofline of the dominant kernel (k_pmc): algorithmic lane-ops / measured time
     mc_s = float(t[1]) / args.steps / 1000.0
     peak = SM_COUNT * LANES_PER_SM_CLK * 1965e6 / 1e12          # T lane-op/s at the max SM clock
-    achieved = (samples_step / max(world, 1)) * ALG_OPS_PER_SAMPLE / mc_s / 1e12 if mc_s > 0 else None
+    p2_step = float(lv[2]) / args.steps
+    ops_step = samples_step * OPS_PHASE1 + p2_step * OPS_PHASE2
+    achieved = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
     traffic = load_traffic()
     roofline = {"bound": "alu", "kernel": "k_pmc", "achieved": achieved, "peak": peak,
                 "unit": "Tlane-op/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "ops_per_sample": ALG_OPS_PER_SAMPLE,
+                "ops_per_sample": ops_step / samples_step if samples_step else None,
+                "phase2_fraction": p2_step / samples_step if samples_step else None,
                 "samples_per_s": samples_step / max(world, 1) / mc_s if mc_s > 0 else None,
                 "mc_share_of_step": mc_s / (ms_step / 1000.0),
                 "peak_note": "148 SMs x 128 lanes x 1.965 GHz issue slots (guide unit counts, max clock)"}

@@ -38,44 +38,51 @@ __device__ __forceinline__ void stage_copy(double* dst, const double* __restrict
   if ((n & 1) && threadIdx.x == 0) dst[n - 1] = __ldg(src + n - 1);
 }
 
-// V rows of group g:  v[rb][c] = sum_{j <= i} Linv[i][j] K[j][c],  i = row0 + 32 rb + lane.
-__device__ __forceinline__ void trmv8_group(const double* __restrict__ Linv, int k, int row0,
-                                            const double* __restrict__ sK, double (&v)[4][8], int lane) {
+__device__ __forceinline__ void dmma884(double a, double b, double& d0, double& d1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// V rows [row0, row0 + 128) of V = L^-1 K (8 columns) on the FP64 tensor cores
+// (DMMA.8x8x4).  Fragment layout (probe tools/probes/dmma_layout.cu): A[lane>>2][lane&3],
+// B[lane&3][lane>>2], C[lane>>2][2 (lane&3) + {0,1}].  acc[t] holds
+// V[row0 + 8 t + (lane>>2)][2 (lane&3) + {0,1}].
+__device__ __forceinline__ void v_group_dmma(const double* __restrict__ Linv, int k, int row0,
+                                             const double* __restrict__ sK, double (&acc)[16][2], int lane) {
 #pragma unroll
-  for (int rb = 0; rb < 4; ++rb)
+  for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int nrows = min(ROWS_PER_GROUP, k - row0);
+  const int nrt = (nrows + 7) >> 3;
+  const int jend = min(k, row0 + 8 * nrt);
+  for (int j = 0; j < jend; j += 4) {
+    const int jj = j + lc;
+    const double b = jj < k ? sK[8 * jj + lr] : 0.0;
+    const double* col = Linv + tri_col(jj, k) - jj;   // col[i] = Linv[i][jj]
+    const int rt_lo = j < row0 ? 0 : ((j - row0) >> 3);
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[rb][c] = 0.0;
-  int nrows = min(ROWS_PER_GROUP, k - row0);
-  int nrb = (nrows + 31) >> 5;
-  int jend = row0 + nrows;
-  const double2* sK2 = reinterpret_cast<const double2*>(sK);
-  for (int j = 0; j < jend; ++j) {
-    double2 a0 = sK2[4 * j + 0], a1 = sK2[4 * j + 1], a2 = sK2[4 * j + 2], a3 = sK2[4 * j + 3];
-    double kj[8] = {a0.x, a0.y, a1.x, a1.y, a2.x, a2.y, a3.x, a3.y};
-    const double* col = Linv + tri_col(j, k) - j;   // col[i] = Linv[i][j]
-    int rb_lo = j < row0 ? 0 : ((j - row0) >> 5);
-#pragma unroll
-    for (int rb = 0; rb < 4; ++rb) {
-      if (rb < rb_lo || rb >= nrb) continue;   // warp-uniform
-      int i = row0 + 32 * rb + lane;
-      double l = (i >= j && i < k) ? col[i] : 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) v[rb][c] = fma(l, kj[c], v[rb][c]);
+    for (int t = 0; t < 16; ++t) {
+      if (t < rt_lo || t >= nrt) continue;   // warp-uniform: zero block of L^-1
+      const int i = row0 + 8 * t + lr;
+      const double av = (i < k && jj <= i) ? col[i] : 0.0;
+      dmma884(av, b, acc[t][0], acc[t][1]);
     }
   }
 }
 
 // Warp computes, for its 8 queries (positions in sQ[8][3]):
-//   mu  -> returned in lane c (c < 8) as mu_out
-//   pair sums sum_i V[i][c] V[i][d] for pair p = lane (and lane + 32 < 36) in pair_out[0..1]
-// pairs: all 36 (cov) or the 8 diagonals (diag_only; pair p < 8 is (p,p)).
+//   mu_out  : lane c (< 8) holds mu of query c
+//   diag_only: out[e] = sum_i V[i][2 (lane&3) + e]^2   (every lane)
+//   full     : out[e] = D[lane>>2][2 (lane&3) + e],  D = V^T V (8x8)
 __device__ __forceinline__ void warp_local_posterior(const TileArgs& a, const double* __restrict__ Linv,
                                                      const double* __restrict__ alpha,
                                                      const double* __restrict__ Xs,
                                                      const double* __restrict__ sQ, double* sK, double* sV,
-                                                     bool diag_only, double& mu_out, double (&pair_out)[2]) {
+                                                     bool diag_only, double& mu_out, double (&out)[2]) {
   const int k = a.k;
   const int lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lc = lane & 3;
   // 1. K[j][c] = k(x_j, q_c)
   for (int j = lane; j < k; j += 32) {
     double xj = Xs[j], yj = Xs[k + j], zj = Xs[2 * k + j];
@@ -95,50 +102,46 @@ __device__ __forceinline__ void warp_local_posterior(const TileArgs& a, const do
     s += __shfl_xor_sync(0xffffffffu, s, 16);
     mu_out = a.kp.m0 + s;
   }
-  // 3. V = L^-1 K, 4. pair sums of V^T V
-  int p0 = lane, p1 = lane + 32;
-  int c0, d0, c1 = 0, d1 = 0;
-  if (diag_only) {
-    c0 = d0 = lane & 7;
-  } else {
-    // p = c (c + 1) / 2 + d, d <= c
-    c0 = (int)((sqrt(8.0 * p0 + 1.0) - 1.0) * 0.5);
-    d0 = p0 - c0 * (c0 + 1) / 2;
-    if (p1 < 36) {
-      c1 = (int)((sqrt(8.0 * p1 + 1.0) - 1.0) * 0.5);
-      d1 = p1 - c1 * (c1 + 1) / 2;
-    }
-  }
-  double acc0 = 0.0, acc1 = 0.0;
+  // 3. V = L^-1 K by row groups of 128 (DMMA); 4. diag or V^T V (DMMA)
+  double o0 = 0.0, o1 = 0.0;
   const bool single = k <= ROWS_PER_GROUP;
   for (int row0 = 0; row0 < k; row0 += ROWS_PER_GROUP) {
-    double v[4][8];
-    trmv8_group(Linv, k, row0, sK, v, lane);
-    double* dst = single ? sK : sV;   // single group: K is dead, reuse its buffer
-    __syncwarp();
-    int nrows = min(ROWS_PER_GROUP, k - row0);
+    double acc[16][2];
+    v_group_dmma(Linv, k, row0, sK, acc, lane);
+    const int nrows = min(ROWS_PER_GROUP, k - row0);
+    if (diag_only) {
 #pragma unroll
-    for (int rb = 0; rb < 4; ++rb) {
-      int r = 32 * rb + lane;
-      if (r < nrows) {
-        double2* d2 = reinterpret_cast<double2*>(dst + 8 * r);
-        d2[0] = make_double2(v[rb][0], v[rb][1]);
-        d2[1] = make_double2(v[rb][2], v[rb][3]);
-        d2[2] = make_double2(v[rb][4], v[rb][5]);
-        d2[3] = make_double2(v[rb][6], v[rb][7]);
+      for (int t = 0; t < 16; ++t) {
+        o0 = fma(acc[t][0], acc[t][0], o0);
+        o1 = fma(acc[t][1], acc[t][1], o1);
       }
+    } else {
+      double* dst = single ? sK : sV;   // single group: K is dead, reuse its buffer
+      __syncwarp();
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int r = 8 * t + lr;
+        if (r < nrows) *reinterpret_cast<double2*>(dst + 8 * r + 2 * lc) = make_double2(acc[t][0], acc[t][1]);
+      }
+      __syncwarp();
+      for (int s = 0; s < nrows; s += 4) {
+        const int r = s + lc;
+        const double v = r < nrows ? dst[8 * r + lr] : 0.0;
+        dmma884(v, v, o0, o1);
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    if (diag_only ? lane < 8 : true) {
-      for (int r = 0; r < nrows; ++r) acc0 = fma(dst[8 * r + c0], dst[8 * r + d0], acc0);
-    }
-    if (!diag_only && p1 < 36) {
-      for (int r = 0; r < nrows; ++r) acc1 = fma(dst[8 * r + c1], dst[8 * r + d1], acc1);
-    }
-    __syncwarp();
   }
-  pair_out[0] = acc0;
-  pair_out[1] = acc1;
+  if (diag_only) {
+    // rows were spread over lr: reduce across lanes with the same (lane & 3)
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      o0 += __shfl_xor_sync(0xffffffffu, o0, o);
+      o1 += __shfl_xor_sync(0xffffffffu, o1, o);
+    }
+  }
+  out[0] = o0;
+  out[1] = o1;
 }
 
 __device__ __forceinline__ int item_bucket(const TileArgs& a, int mode, int64_t item, const double* pts,
@@ -230,9 +233,12 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
       __syncwarp();
       double mu, pr[2];
       warp_local_posterior(a, Linv, alpha, Xs, sQ, sK, sV, true, mu, pr);
+      // query c's sum of squares sits in lane c >> 1, element c & 1
+      const double sq0 = __shfl_sync(0xffffffffu, pr[0], lane >> 1);
+      const double sq1 = __shfl_sync(0xffffffffu, pr[1], lane >> 1);
       if (lane < nq) {
         int64_t it = items[base + lane];
-        double var = a.kp.var - pr[0];   // k(q,q) = sigma_f^2 for both kernels
+        double var = a.kp.var - ((lane & 1) ? sq1 : sq0);   // k(q,q) = sigma_f^2 for both kernels
         if (var < a.var_err) atomicOr(derr, DERR_NUMERIC);
         double vf = var > a.var_floor ? var : a.var_floor;
         if (mode == Q_VERTEX) {
@@ -285,15 +291,17 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
       warp_local_posterior(a, Linv, alpha, Xs, sQ, sK, sV, false, mu, pr);
       double* rec = post + 44 * slot;
       if (lane < 8) rec[lane] = mu;
-      double s0 = a.kcc[lane] - pr[0];
-      rec[8 + lane] = s0;
-      // diagonal pairs are p = c (c + 3) / 2: 0 2 5 9 14 20 27 | 35
-      bool diag0 = lane == 0 || lane == 2 || lane == 5 || lane == 9 || lane == 14 || lane == 20 || lane == 27;
-      if (diag0 && s0 < a.var_err) atomicOr(derr, DERR_NUMERIC);
-      if (lane < 4) {
-        double s1 = a.kcc[32 + lane] - pr[1];
-        rec[8 + 32 + lane] = s1;
-        if (lane == 3 && s1 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      // lane holds D[r][c] for r = lane >> 2, c = 2 (lane & 3) + e; keep c <= r
+      const int r = lane >> 2;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = 2 * (lane & 3) + e;
+        if (cc <= r) {
+          const int p = r * (r + 1) / 2 + cc;
+          const double sv = a.kcc[p] - pr[e];
+          rec[8 + p] = sv;
+          if (cc == r && sv < a.var_err) atomicOr(derr, DERR_NUMERIC);
+        }
       }
       __syncwarp();
     }

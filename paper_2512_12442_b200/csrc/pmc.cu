@@ -165,7 +165,13 @@ constexpr int QCAP = 64;            // pending samples per warp
 // in shared memory and, 32 at a time, phase 2 draws the second Philox block
 // (z4..z7) and finishes the sample.  Every sample is decided exactly as the
 // one-pass FP32 evaluation decides it; the count is the same estimator.
-__global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restrict__ cells,
+#ifndef PMC_MINBLOCKS
+#define PMC_MINBLOCKS 2
+#endif
+#ifndef PMC_ILP
+#define PMC_ILP 2
+#endif
+__global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int64_t* __restrict__ cells,
                                                         const double* __restrict__ post, int64_t n, double theta,
                                                         uint32_t N, const PhiloxKeys K, uint32_t iso,
                                                         float* __restrict__ out,
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32) k_pmc(const int64_t* __restric
   };
   uint32_t base = 0;
   // two samples per lane per iteration (instruction-level parallelism)
-  for (; base + 64u <= Nl; base += 64u) {
+  for (; PMC_ILP == 2 && base + 64u <= Nl; base += 64u) {
     float ya[6], yb[6];
     const bool pa = phase1(base + lane, ya);
     const bool pb = phase1(base + 32u + lane, yb);

@@ -15,7 +15,7 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblcp.so")
+LIB_PATH = os.environ.get("LCP_LIB", os.path.join(_HERE, "liblcp.so"))
 
 LCP_OK, LCP_EINVAL, LCP_ESTATE, LCP_EFACTOR, LCP_ENUMERIC, LCP_ECUDA, LCP_ENOMEM = range(7)
 STATUS_NAMES = {0: "LCP_OK", 1: "LCP_EINVAL", 2: "LCP_ESTATE", 3: "LCP_EFACTOR", 4: "LCP_ENUMERIC",
