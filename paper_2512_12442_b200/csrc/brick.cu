@@ -65,10 +65,10 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
                       int* __restrict__ derr) {
   extern __shared__ double smem[];
   const int k = a.k, KP = a.kp8;
-  const int64_t tri = tri_size(k);
-  const int64_t head = (tri + 4 * (int64_t)k + 1) & ~1ll;
-  double* sLinv = smem;
-  double* sAlpha = smem + tri;
+  const int64_t LA = la_size(k);
+  const int64_t head = (LA + 4 * (int64_t)k + 1) & ~1ll;
+  double* sLA = smem;
+  double* sAlpha = smem + LA;
   double* sX = sAlpha + k;
   double* KV = smem + head;                     // KP x VSTR
   double* sMu = KV + (int64_t)KP * VSTR;        // NVP
@@ -137,8 +137,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         for (int t = 0; t < 4; ++t) {
           const int rt = rs + 4 * t;
           if (rt >= nrt || 8 * rt + 7 < j) continue;   // warp-uniform: zero block of L^-1
-          const int i = 8 * rt + lr;
-          double af = (i < k && jj <= i) ? sLinv[tri_col(jj, k) + i - jj] : 0.0;
+          const double af = sLA[la_block(rt, j >> 2) + lane];
 #pragma unroll
           for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
         }
@@ -194,8 +193,7 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
   if (c.k > 128 || c.g.bs < BK) return false;
   const int k = c.k;
   const int kp8 = (k + 7) & ~7;
-  const int64_t tri = tri_size(k);
-  const int64_t head = (tri + 4 * (int64_t)k + 1) & ~1ll;
+  const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
   size_t smem = sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP);
   if (smem > 227 * 1024) return false;
   if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;

@@ -144,6 +144,18 @@ __host__ __device__ __forceinline__ int64_t tri_col(int64_t j, int64_t k) {
 }
 __host__ __device__ __forceinline__ int64_t tri_size(int64_t k) { return k * (k + 1) / 2; }
 
+// L^-1 stored as DMMA A-fragments (the "LA" layout of a bucket block): row
+// tile rt (rows 8rt..8rt+7) and k-step js (columns 4js..4js+3), js <= 2rt+1,
+// are 32 doubles in lane order lane = 4 (row - 8rt) + (col - 4js), zero above
+// the diagonal and beyond k.  A lane of a DMMA.8x8x4 loads element `lane` of
+// block (rt, js): conflict-free and without index arithmetic.
+__host__ __device__ __forceinline__ int la_nrt(int k) { return (k + 7) >> 3; }
+__host__ __device__ __forceinline__ int64_t la_size(int k) {
+  int64_t n = la_nrt(k);
+  return n * (n + 1) * 32;
+}
+__host__ __device__ __forceinline__ int64_t la_block(int rt, int js) { return ((int64_t)rt * (rt + 1) + js) * 32; }
+
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll

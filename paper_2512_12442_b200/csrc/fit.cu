@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g
   }
 }
 
-// a3: per-bucket factor.  Block layout in bdata: [L^-1 packed col-major (tri)]
-// [alpha (k)] [x (k)] [y (k)] [z (k)].
+// a3: per-bucket factor.  Block layout in bdata: [L^-1 in the DMMA A-fragment
+// layout (la_size(k), common.cuh)] [alpha (k)] [x (k)] [y (k)] [z (k)].
 __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, int k, const double* __restrict__ X,
                                                                 const double* __restrict__ yobs,
                                                                 const int32_t* __restrict__ S,
@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
   const int tid = threadIdx.x, bd = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = bd >> 5;
   const int64_t tri = tri_size(k);
+  const int64_t LA = la_size(k);
   double* sx = sm;
   double* sy = sx + k;
   double* sz = sy + k;
@@ -270,9 +271,9 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     sy[a] = X[3 * o + 1];
     sz[a] = X[3 * o + 2];
     rr[a] = yobs[o] - kp.m0;
-    out[tri + k + a] = sx[a];
-    out[tri + 2 * k + a] = sy[a];
-    out[tri + 3 * k + a] = sz[a];
+    out[LA + k + a] = sx[a];
+    out[LA + 2 * k + a] = sy[a];
+    out[LA + 3 * k + a] = sz[a];
   }
   bool ok = false;
   for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
@@ -345,9 +346,18 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     const double* Lc = Li + tri_col(j, k) - j;
     double s = 0.0;
     for (int i = j; i < k; ++i) s = fma(Lc[i], vv[i], s);
-    out[tri + j] = s;
+    out[LA + j] = s;
   }
-  for (int64_t e = tid; e < tri; e += bd) out[e] = Li[e];
+  for (int64_t e = tid; e < LA; e += bd) {
+    const int64_t blk = e >> 5;
+    const int ln = (int)(e & 31);
+    int rt = (int)((sqrt(4.0 * (double)blk + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(rt + 1) * (rt + 2) <= blk) ++rt;
+    while ((int64_t)rt * (rt + 1) > blk) --rt;
+    const int js = (int)(blk - (int64_t)rt * (rt + 1));
+    const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
+    out[e] = (i < k && j <= i) ? Li[tri_col(j, k) + i - j] : 0.0;
+  }
 }
 
 // ------------------------------------------------------------------- host
@@ -435,7 +445,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       c.kcc[cc * (cc + 1) / 2 + dd] = host_kern(kp, a, b);
     }
   int64_t tri = tri_size(k);
-  c.bstride = (tri + 4 * (int64_t)k + 1) & ~1ll;
+  c.bstride = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
   const int nbk = g.nbuckets;
 
   cudaError_t e;

@@ -10,6 +10,8 @@
 // independent points (vertex / observation marginals, a4-a5).  A CTA stages the
 // bucket block [L^-1 | alpha | X_S] into shared memory once and all its warps
 // reuse it; work lists are grouped by bucket (scan.cu) so restaging is rare.
+#include <algorithm>
+
 #include "ctx.h"
 
 namespace lcp {
@@ -23,8 +25,10 @@ struct TileArgs {
   int k;
   int staged;            // L^-1 staged in shared memory
   int64_t bstride;       // doubles per bucket block
-  const double* bdata;   // [L^-1 packed col-major | alpha | x | y | z] per bucket
+  const double* bdata;   // [L^-1 A-fragments (la_size(k)) | alpha | x | y | z] per bucket
   double kcc[36];        // prior covariance of the 8 cell corners (packed lower, row-major pairs)
+  int64_t la;            // doubles of the L^-1 A-fragment block (la_size(k))
+  int ks;                // row stride of the per-warp K buffer sK[c][j] (ks = 4 mod 16: conflict-free)
   double var_floor;      // 1e-12 sigma_f^2
   double var_err;        // -1e-8 sigma_f^2
 };
@@ -48,25 +52,23 @@ __device__ __forceinline__ void dmma884(double a, double b, double& d0, double& 
 // (DMMA.8x8x4).  Fragment layout (probe tools/probes/dmma_layout.cu): A[lane>>2][lane&3],
 // B[lane&3][lane>>2], C[lane>>2][2 (lane&3) + {0,1}].  acc[t] holds
 // V[row0 + 8 t + (lane>>2)][2 (lane&3) + {0,1}].
-__device__ __forceinline__ void v_group_dmma(const double* __restrict__ Linv, int k, int row0,
+__device__ __forceinline__ void v_group_dmma(const double* __restrict__ LA, int k, int ks, int row0,
                                              const double* __restrict__ sK, double (&acc)[16][2], int lane) {
 #pragma unroll
   for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = 0.0;
   const int lr = lane >> 2, lc = lane & 3;
   const int nrows = min(ROWS_PER_GROUP, k - row0);
   const int nrt = (nrows + 7) >> 3;
-  const int jend = min(k, row0 + 8 * nrt);
+  const int rt0 = row0 >> 3;
+  const int jend = row0 + 8 * nrt;
   for (int j = 0; j < jend; j += 4) {
-    const int jj = j + lc;
-    const double b = jj < k ? sK[8 * jj + lr] : 0.0;
-    const double* col = Linv + tri_col(jj, k) - jj;   // col[i] = Linv[i][jj]
+    const int jj = j + lc, js = j >> 2;
+    const double b = jj < k ? sK[lr * ks + jj] : 0.0;
     const int rt_lo = j < row0 ? 0 : ((j - row0) >> 3);
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       if (t < rt_lo || t >= nrt) continue;   // warp-uniform: zero block of L^-1
-      const int i = row0 + 8 * t + lr;
-      const double av = (i < k && jj <= i) ? col[i] : 0.0;
-      dmma884(av, b, acc[t][0], acc[t][1]);
+      dmma884(LA[la_block(rt0 + t, js) + lane], b, acc[t][0], acc[t][1]);
     }
   }
 }
@@ -83,21 +85,22 @@ __device__ __forceinline__ void warp_local_posterior(const TileArgs& a, const do
   const int k = a.k;
   const int lane = threadIdx.x & 31;
   const int lr = lane >> 2, lc = lane & 3;
-  // 1. K[j][c] = k(x_j, q_c)
+  const int ks = a.ks;
+  // 1. K[c][j] = k(x_j, q_c)  (query-major: lanes over j store conflict-free)
   for (int j = lane; j < k; j += 32) {
     double xj = Xs[j], yj = Xs[k + j], zj = Xs[2 * k + j];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       double r2 = kern_r2(a.kp, xj - sQ[3 * c], yj - sQ[3 * c + 1], zj - sQ[3 * c + 2]);
-      sK[8 * j + c] = kern_from_r2(a.kp, r2);
+      sK[c * ks + j] = kern_from_r2(a.kp, r2);
     }
   }
   __syncwarp();
-  // 2. mu_c = m0 + sum_j K[j][c] alpha_j   (lane: c = lane & 7, part = lane >> 3)
+  // 2. mu_c = m0 + sum_j K[c][j] alpha_j   (lane: c = lane & 7, part = lane >> 3)
   {
     int c = lane & 7, part = lane >> 3;
     double s = 0.0;
-    for (int j = part; j < k; j += 4) s = fma(sK[8 * j + c], alpha[j], s);
+    for (int j = part; j < k; j += 4) s = fma(sK[c * ks + j], alpha[j], s);
     s += __shfl_xor_sync(0xffffffffu, s, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 16);
     mu_out = a.kp.m0 + s;
@@ -107,7 +110,7 @@ __device__ __forceinline__ void warp_local_posterior(const TileArgs& a, const do
   const bool single = k <= ROWS_PER_GROUP;
   for (int row0 = 0; row0 < k; row0 += ROWS_PER_GROUP) {
     double acc[16][2];
-    v_group_dmma(Linv, k, row0, sK, acc, lane);
+    v_group_dmma(Linv, k, ks, row0, sK, acc, lane);
     const int nrows = min(ROWS_PER_GROUP, k - row0);
     if (diag_only) {
 #pragma unroll
@@ -151,40 +154,62 @@ __device__ __forceinline__ int item_bucket(const TileArgs& a, int mode, int64_t 
   return cell_bucket(a.g, item);
 }
 
-// Generic tile loop: CTA handles sorted positions [t0, t1); runs of equal bucket
-// share one staging of the bucket block.
+// Generic tile loop: CTA handles sorted positions [t0, t1) (t1 - t0 <= TILE_MAX);
+// runs of equal bucket are found in parallel (ballot + warp-prefix compaction)
+// and share one staging of the bucket block.
+constexpr int TILE_MAX = 2048;
+
 template <typename Body>
 __device__ __forceinline__ void tile_loop(const TileArgs& a, int64_t t0, int64_t t1, double* smem,
                                           const int32_t* __restrict__ runb, Body body) {
-  __shared__ int s_run_end;
-  __shared__ int s_bucket;
-  const int64_t blk = a.bstride;
-  int staged_bucket = -1;
-  int64_t q = t0;
-  while (q < t1) {
-    if (threadIdx.x == 0) {
-      int b = runb[q];
-      int64_t e = q + 1;
-      while (e < t1 && runb[e] == b) ++e;
-      s_run_end = (int)(e - t0);
-      s_bucket = b;
+  __shared__ int s_starts[TILE_MAX + 1];
+  __shared__ int s_wcnt[33];
+  __shared__ int s_nruns;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int n = (int)(t1 - t0);
+  if (tid == 0) s_nruns = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + tid;
+    const bool f = i < n && (i == 0 || runb[t0 + i] != runb[t0 + i - 1]);
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) s_wcnt[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? s_wcnt[lane] : 0, x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane < nw) s_wcnt[lane] = x - v;
+      if (lane == 31) s_wcnt[32] = x;
     }
     __syncthreads();
-    int b = s_bucket;
-    int64_t qe = t0 + s_run_end;
+    if (f) s_starts[s_nruns + s_wcnt[wid] + __popc(bal & ((1u << lane) - 1u))] = i;
+    __syncthreads();
+    if (tid == 0) s_nruns += s_wcnt[32];
+    __syncthreads();
+  }
+  const int nruns = s_nruns;
+  if (tid == 0) s_starts[nruns] = n;
+  __syncthreads();
+  const int64_t blk = a.bstride;
+  int staged_bucket = -1;
+  for (int r = 0; r < nruns; ++r) {
+    const int64_t q = t0 + s_starts[r], qe = t0 + s_starts[r + 1];
+    const int b = runb[q];
     if (b != staged_bucket) {
       const double* src = a.bdata + (int64_t)b * blk;
-      int64_t tri = tri_size(a.k);
       if (a.staged) stage_copy(smem, src, blk);
-      else stage_copy(smem, src + tri, 4 * (int64_t)a.k);
+      else stage_copy(smem, src + a.la, 4 * (int64_t)a.k);
       staged_bucket = b;
     }
     __syncthreads();
     const double* Linv = a.staged ? smem : a.bdata + (int64_t)b * blk;
-    const double* tail = a.staged ? smem + tri_size(a.k) : smem;
+    const double* tail = a.staged ? smem + a.la : smem;
     body(b, q, qe, Linv, tail, tail + a.k);
     __syncthreads();
-    q = qe;
   }
 }
 
@@ -208,10 +233,10 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
   const int k = a.k;
   int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
   head = (head + 1) & ~1ll;
-  const int64_t per_warp = 8 * (int64_t)k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
+  const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
   double* wbuf = smem + head + wid * per_warp;
   double* sK = wbuf;
-  double* sV = wbuf + 8 * k;
+  double* sV = wbuf + 8 * a.ks;
   double* sQ = wbuf + per_warp - 24;
   const Geom& g = a.g;
   tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
@@ -268,10 +293,10 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
   const int k = a.k;
   int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
   head = (head + 1) & ~1ll;
-  const int64_t per_warp = 8 * (int64_t)k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
+  const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
   double* wbuf = smem + head + wid * per_warp;
   double* sK = wbuf;
-  double* sV = wbuf + 8 * k;
+  double* sV = wbuf + 8 * a.ks;
   double* sQ = wbuf + per_warp - 24;
   const Geom& g = a.g;
   tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
@@ -317,6 +342,8 @@ static TileArgs make_tile_args(Ctx& c) {
   a.bdata = c.bdata.as<double>();
   for (int p = 0; p < 36; ++p) a.kcc[p] = c.kcc[p];
   a.var_floor = 1e-12 * c.kp.var;
+  a.la = la_size(c.k);
+  a.ks = c.k + ((4 - c.k % 16) + 16) % 16;
   a.var_err = -1e-8 * c.kp.var;
   a.staged = 0;
   return a;
@@ -326,7 +353,8 @@ static TileArgs make_tile_args(Ctx& c) {
 static void plan_tile(const Ctx& c, int& staged, int& warps, size_t& smem) {
   const size_t cap = 220 * 1024;
   int64_t k = c.k;
-  size_t per_warp = sizeof(double) * (8 * k + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24);
+  const int64_t ks = k + ((4 - k % 16) + 16) % 16;
+  size_t per_warp = sizeof(double) * (8 * ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24);
   size_t head_staged = sizeof(double) * ((c.bstride + 1) & ~1ll);
   size_t head_tail = sizeof(double) * (4 * k + 1);
   staged = 0;
@@ -354,7 +382,7 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
   if (warps == 0) return cudaErrorInvalidConfiguration;
   a.staged = staged;
   cudaFuncSetAttribute(k_marginals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int tile = 8 * warps * 4;
+  int tile = std::min(8 * warps * 8, TILE_MAX);
   unsigned grid = (unsigned)((n + tile - 1) / tile);
   k_marginals<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
                                                     out_mu, out_sd, write_var, c.vcache.as<double2>(),
