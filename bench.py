@@ -187,6 +187,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2512_12442_b200 import Context, config_args
+    from paper_2512_12442_b200.dist import gather_field
     from workloads import generate
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -227,7 +228,7 @@ def run_ours(args):
             mc_ms += st["mc_ms"]
             p2 += st["pmc_phase2_samples"]
             if world > 1:
-                dist.reduce(field, 0, op=dist.ReduceOp.SUM)
+                gather_field(field, cfg.cells, 3)   # NCCL all-gather of the slab slices
             if host is not None and rank == 0:
                 host[2].copy_(field, non_blocking=True)
                 torch.cuda.current_stream().synchronize()

@@ -21,7 +21,9 @@ namespace lcp {
 constexpr int BK = 4;                      // cells per brick side
 constexpr int NVB = (BK + 1) * (BK + 1) * (BK + 1);   // 125 vertices
 constexpr int NVP = 128;                    // padded vertex columns
-constexpr int VSTR = 136;                   // K/V row stride in doubles (64 mod 128 bytes: conflict-free B fragments)
+// K/V row stride in doubles: 132 = 4 mod 16, so the four rows of a B fragment
+// fall on disjoint bank octets within each half-warp phase (conflict-free).
+constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
 constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
 
