@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--dense", action="store_true",
+                    help="pruning-free baseline: exact GP (k = m, one bucket), PMC of every cell")
     return ap.parse_args()
 
 
@@ -206,6 +208,13 @@ def run_ours(args):
     field = torch.empty(ncell, dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     slab = dict(slab_rank=rank, slab_count=world, slab_level=3) if world > 1 else {}
+    if args.dense:
+        # pruning-free baseline (BASELINE c3): exact GP (k = m, one bucket), every cell of the slab
+        from paper_2512_12442_b200.dist import slab_cells
+        k, b = cfg.m, 0
+        c0, c1 = slab_cells(cfg.cells, 3, rank, world) if world > 1 else (0, ncell)
+        dense_cells = torch.arange(c0, c1, dtype=torch.int64, device=dev)
+        dense_lcp = torch.empty(c1 - c0, dtype=torch.float32, device=dev)
     ctx = Context(local)
 
     def barrier():
@@ -222,7 +231,12 @@ def run_ours(args):
         mc_ms = 0.0
         p2 = 0
         for it, th in enumerate(w.thetas):
-            _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it, field=field)
+            if args.dense:
+                ctx.pmc_cells(dense_cells, th, cfg.n_samples, cfg.mc_seed, it, out=dense_lcp)
+                ctx.scatter_field(dense_cells, dense_lcp, field)
+                n = len(dense_cells)
+            else:
+                _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it, field=field)
             leaves += n
             st = ctx.stats()
             mc_ms += st["mc_ms"]
@@ -331,7 +345,9 @@ def run_ours(args):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
-           "config": {"workload": workload_desc(cfg, w.thetas), "cells": ncell, "m": cfg.m, "k": cfg.k,
+           "config": {"workload": workload_desc(cfg, w.thetas) + (
+                          " | DENSE baseline: exact GP k=m, every cell" if args.dense else ""),
+                      "mode": "dense" if args.dense else "octree-pruned", "cells": ncell, "m": cfg.m, "k": k,
                       "n_samples": cfg.n_samples, "alpha": cfg.alpha, "max_depth": cfg.max_depth,
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                       "l2": "flushed between timed steps (256 MB write, outside the step events)"},
