@@ -72,7 +72,8 @@ typedef struct {
     int32_t slab_count;    /* ... of slab_count (1 = whole domain) */
     int32_t slab_level;    /* octree level whose z-layers are split across ranks (default 3) */
     int32_t keep_records;  /* parity tap: keep per-node records of levels < keep_records (0 = none) */
-    int32_t pad_;
+    int32_t extreme_iters; /* NEXT-1 (R26): iterations of the continuous extreme search at nodes
+                              coarser than h_full; 0 = lattice only */
 } lcp_opts_t;
 
 /* per evaluated octree node (Alg. 1) */

@@ -99,6 +99,12 @@ def lib():
         L.orc_tail_probs.argtypes = [C.c_double, C.c_double, C.c_double,
                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.orc_tail_probs.restype = None
+        L.orc_model_set_extreme.argtypes = [P, C.c_int32]
+        L.orc_model_set_extreme.restype = None
+        L.orc_local_f_grad.restype = C.c_double
+        L.orc_local_f_grad.argtypes = [P, C.c_int32, dp, C.c_double, dp]
+        L.orc_node_extremes.argtypes = [P, C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int32, dp]
+        L.orc_node_extremes.restype = None
         L.orc_free.argtypes = [P]
         L.orc_free.restype = None
         L.orc_num_threads.restype = C.c_int
@@ -233,6 +239,20 @@ class Model:
         _check(lib().orc_local_marginal(self._h, b, np.ascontiguousarray(x, np.float64),
                                         C.byref(mu), C.byref(var)), "local_marginal")
         return mu.value, var.value
+
+    def set_extreme(self, iters):
+        """NEXT-1 (R26): continuous extreme search iterations at nodes with h > h_full."""
+        lib().orc_model_set_extreme(self._h, int(iters))
+
+    def f_grad(self, b, x, theta):
+        g = np.zeros(3)
+        f = lib().orc_local_f_grad(self._h, b, np.ascontiguousarray(x, np.float64), theta, g)
+        return f, g
+
+    def node_extremes(self, theta, level, i, j, k):
+        out = np.zeros(6)
+        lib().orc_node_extremes(self._h, theta, level, i, j, k, out)
+        return out
 
     def cell_posterior(self, cell):
         mu = np.zeros(8)

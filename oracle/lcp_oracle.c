@@ -156,6 +156,7 @@ struct orc_model {
     double h[3];          /* cell size */
     double w[3];          /* k-NN metric weights 1 / l_d */
     int32_t lfull, b, bs, h_full;
+    int32_t extreme_iters;  /* NEXT-1: projected-gradient iterations at nodes with h > h_full (0 = off) */
     int32_t nb[3], nbuckets;
     int32_t m, k;
     double* X;            /* m x 3 */
@@ -518,6 +519,165 @@ void orc_tail_probs(double mu, double var, double theta, double* p_lo, double* p
     *p_hi = 0.5 * erfc((theta - mu) / sd2);
 }
 
+/* ---------------------------------------------------------------- NEXT-1 --- */
+/* Gradient of the kernel w.r.t. its first argument a:
+ * SE: dk/da_d = -k (a_d - b_d) / l_d^2;  Matern-5/2: -(5/3) s2 (1 + sqrt5 r) e^{-sqrt5 r} (a_d - b_d) / l_d^2. */
+static void kernel_grad(const orc_kernel_t* kern, const double* a, const double* b, double* g) {
+    double r2 = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        double t = (a[d] - b[d]) / kern->lengthscale[d];
+        r2 += t * t;
+    }
+    double c;
+    if (kern->kind == 0) {
+        c = -kern->variance * exp(-0.5 * r2);
+    } else {
+        double r = sqrt(r2), s5 = sqrt(5.0);
+        c = -(5.0 / 3.0) * kern->variance * (1.0 + s5 * r) * exp(-s5 * r);
+    }
+    for (int d = 0; d < 3; ++d)
+        g[d] = c * (a[d] - b[d]) / (kern->lengthscale[d] * kern->lengthscale[d]);
+}
+
+/* f(x) = (mu(x) - theta) / (sigma(x) sqrt 2) of bucket b's local GP and its gradient:
+ * grad mu = sum_j grad k_j alpha_j; var = k(x,x) - v.v, v = L^-1 k_x;
+ * grad var = -2 v . (L^-1 grad k); sigma = sqrt(max(var, floor)) (flat when floored). */
+static double local_f_grad(const orc_model_t* M, int32_t b, const double* x, double theta, double* gf) {
+    int k = M->k;
+    const int32_t* S = M->S + (size_t)b * k;
+    const double* L = M->L + (size_t)b * k * k;
+    const double* al = M->alpha + (size_t)b * k;
+    double* kv = malloc(sizeof(double) * k * 4);
+    double* v = malloc(sizeof(double) * k * 4);
+    double mu = M->kern.prior_mean, gmu[3] = {0, 0, 0};
+    for (int a = 0; a < k; ++a) {
+        const double* xa = M->X + 3 * (size_t)S[a];
+        double g[3];
+        kv[a] = orc_kernel(&M->kern, x, xa);
+        kernel_grad(&M->kern, x, xa, g);
+        for (int d = 0; d < 3; ++d) kv[(d + 1) * k + a] = g[d];
+        mu += kv[a] * al[a];
+        for (int d = 0; d < 3; ++d) gmu[d] += g[d] * al[a];
+    }
+    for (int c = 0; c < 4; ++c) forward_sub(L, k, kv + (size_t)c * k, v + (size_t)c * k);
+    double var = orc_kernel(&M->kern, x, x), gvar[3] = {0, 0, 0};
+    for (int a = 0; a < k; ++a) {
+        var -= v[a] * v[a];
+        for (int d = 0; d < 3; ++d) gvar[d] -= 2.0 * v[a] * v[(d + 1) * k + a];
+    }
+    double fl = 1e-12 * M->kern.variance;
+    double vf = var > fl ? var : fl, s = sqrt(vf);
+    double f = (mu - theta) / (s * ORC_SQRT2);
+    for (int d = 0; d < 3; ++d) {
+        double gs = var > fl ? gvar[d] / (2.0 * s) : 0.0;
+        gf[d] = (gmu[d] * s - (mu - theta) * gs) / (vf * ORC_SQRT2);
+    }
+    free(kv); free(v);
+    return f;
+}
+
+/* R26: deterministic bounded search for the extreme of f over the node box,
+ * maximising sgn * f from the lattice extreme `av`.  Local model: the node's
+ * bucket when the node lies inside one bucket (level >= bucket_log2, the paper's
+ * per-node local model), else the start vertex's bucket with the
+ * box clipped to that bucket.  Iteration (extreme_iters times): normalised
+ * projected-gradient step of length `step` (start: a quarter of the shortest box
+ * side); accept if sgn*f increases (step doubles, capped at the longest side),
+ * else halve the step; stop when the projected gradient vanishes. */
+static double extreme_search(const orc_model_t* M, double theta, int32_t level, const int64_t* base,
+                             const int64_t* vmax, const int32_t* av, int sgn, double* f_start) {
+    int64_t lo_v[3], hi_v[3];
+    int32_t b;
+    if (level >= M->b) {
+        b = orc_vertex_bucket(M, (int32_t)base[0], (int32_t)base[1], (int32_t)base[2]);
+        for (int d = 0; d < 3; ++d) { lo_v[d] = base[d]; hi_v[d] = vmax[d]; }
+    } else {
+        b = orc_vertex_bucket(M, av[0], av[1], av[2]);
+        int32_t bi[3] = {b % M->nb[0], (b / M->nb[0]) % M->nb[1], b / (M->nb[0] * M->nb[1])};
+        for (int d = 0; d < 3; ++d) {
+            int64_t b0 = (int64_t)bi[d] * M->bs, b1 = b0 + M->bs;
+            lo_v[d] = base[d] > b0 ? base[d] : b0;
+            hi_v[d] = vmax[d] < b1 ? vmax[d] : b1;
+        }
+    }
+    double blo[3], bhi[3], x[3], g[3];
+    vertex_pos(M, (int32_t)lo_v[0], (int32_t)lo_v[1], (int32_t)lo_v[2], blo);
+    vertex_pos(M, (int32_t)hi_v[0], (int32_t)hi_v[1], (int32_t)hi_v[2], bhi);
+    vertex_pos(M, av[0], av[1], av[2], x);
+    double mn = INFINITY, mx = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        double w = bhi[d] - blo[d];
+        if (w < mn) mn = w;
+        if (w > mx) mx = w;
+    }
+    double step = 0.25 * mn;
+    double F = sgn * local_f_grad(M, b, x, theta, g);
+    if (f_start) *f_start = sgn * F;
+    for (int d = 0; d < 3; ++d) g[d] *= sgn;
+    for (int it = 0; it < M->extreme_iters; ++it) {
+        for (int d = 0; d < 3; ++d)
+            if ((x[d] <= blo[d] && g[d] < 0.0) || (x[d] >= bhi[d] && g[d] > 0.0)) g[d] = 0.0;
+        double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+        if (!(gn > 0.0)) break;
+        double xn[3], gt[3];
+        for (int d = 0; d < 3; ++d) {
+            double t = x[d] + step * (g[d] / gn);
+            xn[d] = t < blo[d] ? blo[d] : (t > bhi[d] ? bhi[d] : t);
+        }
+        double Fn = sgn * local_f_grad(M, b, xn, theta, gt);
+        if (Fn > F) {
+            F = Fn;
+            for (int d = 0; d < 3; ++d) { x[d] = xn[d]; g[d] = sgn * gt[d]; }
+            step = step * 2.0 < mx ? step * 2.0 : mx;
+        } else {
+            step *= 0.5;
+        }
+    }
+    return sgn * F;
+}
+
+void orc_model_set_extreme(orc_model_t* M, int32_t iters) { M->extreme_iters = iters > 0 ? iters : 0; }
+
+/* test tap: out = {lattice zmax, lattice zmin, searched zmax, searched zmin, f at the two starts} */
+void orc_node_extremes(const orc_model_t* M, double theta, int32_t level, int32_t i, int32_t j, int32_t k,
+                       double* out) {
+    int32_t h = M->lfull - level;
+    int64_t side = (int64_t)1 << h, base[3], vmax[3];
+    int32_t a[3] = {i, j, k};
+    for (int d = 0; d < 3; ++d) {
+        base[d] = (int64_t)a[d] * side;
+        vmax[d] = base[d] + side < M->grid.cells[d] ? base[d] + side : M->grid.cells[d];
+    }
+    int32_t st = h - M->h_full > 0 ? h - M->h_full : 0;
+    int64_t stride = (int64_t)1 << st;
+    double zmax = -INFINITY, zmin = INFINITY;
+    int32_t amax[3] = {0, 0, 0}, amin[3] = {0, 0, 0};
+    for (int64_t vk = base[2];; vk = vk + stride < vmax[2] ? vk + stride : vmax[2]) {
+        for (int64_t vj = base[1];; vj = vj + stride < vmax[1] ? vj + stride : vmax[1]) {
+            for (int64_t vi = base[0];; vi = vi + stride < vmax[0] ? vi + stride : vmax[0]) {
+                double xv[3], mu, var, vf = 0.0;
+                vertex_pos(M, (int32_t)vi, (int32_t)vj, (int32_t)vk, xv);
+                orc_local_marginal(M, orc_vertex_bucket(M, (int32_t)vi, (int32_t)vj, (int32_t)vk), xv, &mu, &var);
+                floor_var(M, var, &vf);
+                double zz = (mu - theta) / (sqrt(vf) * ORC_SQRT2);
+                if (zz > zmax) { zmax = zz; amax[0] = (int32_t)vi; amax[1] = (int32_t)vj; amax[2] = (int32_t)vk; }
+                if (zz < zmin) { zmin = zz; amin[0] = (int32_t)vi; amin[1] = (int32_t)vj; amin[2] = (int32_t)vk; }
+                if (vi == vmax[0]) break;
+            }
+            if (vj == vmax[1]) break;
+        }
+        if (vk == vmax[2]) break;
+    }
+    out[0] = zmax;
+    out[1] = zmin;
+    out[2] = extreme_search(M, theta, level, base, vmax, amax, +1, &out[4]);
+    out[3] = extreme_search(M, theta, level, base, vmax, amin, -1, &out[5]);
+}
+
+double orc_local_f_grad(const orc_model_t* M, int32_t b, const double* x, double theta, double* grad) {
+    return local_f_grad(M, b, x, theta, grad);
+}
+
 int orc_eval_node(const orc_model_t* M, double theta, double alpha, int32_t level,
                   int32_t i, int32_t j, int32_t k, orc_node_rec_t* rec) {
     int32_t h = M->lfull - level;
@@ -561,20 +721,33 @@ int orc_eval_node(const orc_model_t* M, double theta, double alpha, int32_t leve
         for (int64_t v = base[d]; v < vmax[d]; v += stride) lst[d][nl[d]++] = v;
         lst[d][nl[d]++] = vmax[d];
     }
-    double q_lo = 0.0, q_hi = 0.0;
+    /* z = (mu - theta) / (sigma sqrt 2): P(Y > theta) = erfc(-z)/2 and P(Y < theta) =
+     * erfc(z)/2 are monotone in z, so Q_lo = max P(Y>theta) sits at max z and
+     * Q_hi = max P(Y<theta) at min z (first occurrence wins ties). */
+    double zmax = -INFINITY, zmin = INFINITY;
+    int32_t amax[3] = {0, 0, 0}, amin[3] = {0, 0, 0};
     int status = ORC_OK;
     for (int z = 0; z < nl[2]; ++z)
         for (int y = 0; y < nl[1]; ++y)
             for (int x = 0; x < nl[0]; ++x) {
                 int32_t vi = (int32_t)lst[0][x], vj = (int32_t)lst[1][y], vk = (int32_t)lst[2][z];
-                double xv[3], mu, var, vf = 0.0, pl, ph;
+                double xv[3], mu, var, vf = 0.0;
                 vertex_pos(M, vi, vj, vk, xv);
                 orc_local_marginal(M, orc_vertex_bucket(M, vi, vj, vk), xv, &mu, &var);
                 if (floor_var(M, var, &vf) != ORC_OK) status = ORC_ENUMERIC;
-                orc_tail_probs(mu, vf, theta, &pl, &ph);
-                if (ph > q_lo) q_lo = ph;
-                if (pl > q_hi) q_hi = pl;
+                double zz = (mu - theta) / (sqrt(vf) * ORC_SQRT2);
+                if (zz > zmax) { zmax = zz; amax[0] = vi; amax[1] = vj; amax[2] = vk; }
+                if (zz < zmin) { zmin = zz; amin[0] = vi; amin[1] = vj; amin[2] = vk; }
             }
+    /* NEXT-1: refine the lattice extremes of coarse nodes by a
+     * continuous bounded search of z over the node box (R26). */
+    if (M->extreme_iters > 0 && h > M->h_full) {
+        double zs = extreme_search(M, theta, level, base, vmax, amax, +1, NULL);
+        if (zs > zmax) zmax = zs;
+        zs = extreme_search(M, theta, level, base, vmax, amin, -1, NULL);
+        if (zs < zmin) zmin = zs;
+    }
+    double q_lo = 0.5 * erfc(-zmax), q_hi = 0.5 * erfc(zmin);
     /* d = inclusive vertex count of the (clipped) node (Alg. 1 line 10, R7) */
     double dcount = (double)(vmax[0] - base[0] + 1) * (double)(vmax[1] - base[1] + 1) *
                     (double)(vmax[2] - base[2] + 1);

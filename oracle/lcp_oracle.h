@@ -91,6 +91,15 @@ int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double 
 /* C5: P(Y < theta), P(Y > theta) for Y ~ N(mu, var). */
 void orc_tail_probs(double mu, double var, double theta, double* p_lo, double* p_hi);
 
+/* NEXT-1 (R26): continuous extreme search at nodes with h > h_full; iters = 0 disables. */
+void orc_model_set_extreme(orc_model_t* M, int32_t iters);
+/* f = (mu - theta) / (sigma sqrt 2) of bucket b's local GP at x, and grad f (3) */
+double orc_local_f_grad(const orc_model_t* M, int32_t b, const double* x, double theta, double* grad);
+
+/* test tap: {lattice zmax, lattice zmin, searched zmax, searched zmin} of a node (R26) */
+void orc_node_extremes(const orc_model_t* M, double theta, int32_t level, int32_t i, int32_t j, int32_t k,
+                       double* out);
+
 /* C6: evaluate one octree node (Alg. 1 lines 2-13, Eq. 3-4). */
 int orc_eval_node(const orc_model_t* M, double theta, double alpha, int32_t level,
                   int32_t i, int32_t j, int32_t k, orc_node_rec_t* rec);

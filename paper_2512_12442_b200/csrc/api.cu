@@ -146,7 +146,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
-                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters};
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.ext_z, &c.ext_v};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)

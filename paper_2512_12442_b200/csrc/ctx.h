@@ -106,6 +106,7 @@ struct Ctx {
   DevBuf leaves;             // int64 leaf cell ids
   int64_t n_leaves = 0;
   DevBuf recs;               // lcp_node_rec_t
+  DevBuf ext_z, ext_v;       // NEXT-1: lattice extremes (z, vertex) per node
   int64_t n_recs = 0;
 
   // leaf pass scratch

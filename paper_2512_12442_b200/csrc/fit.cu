@@ -396,7 +396,9 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   o.slab_count = 1;
   o.slab_level = 3;
   o.keep_records = 0;
+  o.extreme_iters = 0;
   if (opts) o = *opts;
+  if (o.extreme_iters < 0 || o.extreme_iters > 1000) return set_err(c, LCP_EINVAL, "fit: extreme_iters not in [0, 1000]");
   if (o.slab_count < 1) o.slab_count = 1;
   int cmax = std::max(grid->cells[0], std::max(grid->cells[1], grid->cells[2]));
   int lfull = ilog2_ceil(cmax);

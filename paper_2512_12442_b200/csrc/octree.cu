@@ -154,11 +154,35 @@ __global__ void k_gather_req(const int64_t* __restrict__ req, const int32_t* __r
   bkt_s[q] = bkt[p];
 }
 
-// vcache[v] = (mu_v, 1 / (sigma_v sqrt 2))
+// U of Eq. 4 in log space from the extreme z values (R9):
+// Q_lo = max P(Y > th) = erfc(-zmax)/2, Q_hi = max P(Y < th) = erfc(zmin)/2
+__device__ __forceinline__ double bound_U(int cs, double d, double zmax, double zmin) {
+  double q_lo = 0.5 * erfc(-zmax), q_hi = 0.5 * erfc(zmin);
+  double U;
+  if (cs == 2) {
+    U = -expm1(d * log1p(-q_lo));
+  } else if (cs == 3) {
+    U = -expm1(d * log1p(-q_hi));
+  } else {
+    U = -expm1(d * log1p(-q_lo)) - exp(d * log1p(-q_hi));
+    U = U < 0.0 ? 0.0 : (U > 1.0 ? 1.0 : U);
+  }
+  return U;
+}
+
+__device__ __forceinline__ double node_dcount(const Lattice& L) {
+  return (double)(L.vmax[0] - L.base[0] + 1) * (double)(L.vmax[1] - L.base[1] + 1) *
+         (double)(L.vmax[2] - L.base[2] + 1);
+}
+
+// vcache[v] = (mu_v, 1 / (sigma_v sqrt 2)).  If ext != nullptr the lattice
+// extremes and their vertices (first lattice index on ties, like the oracle's
+// x-fastest scan) are kept for the continuous search (NEXT-1).
 template <int G>
 __global__ void k_node_bound(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF, double theta,
                              double alpha, const int8_t* __restrict__ ncase, const double2* __restrict__ vcache,
-                             int8_t* __restrict__ nref, double* __restrict__ nU) {
+                             int8_t* __restrict__ nref, double* __restrict__ nU, double* __restrict__ ext_z,
+                             int64_t* __restrict__ ext_v) {
   int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int sub = threadIdx.x % G;
   const bool live = n < nF && ncase[n] != 1;
@@ -169,31 +193,36 @@ __global__ void k_node_bound(Geom g, int level, const uint64_t* __restrict__ fro
   Lattice L = node_lattice(g, h, i, j, k);
   int64_t nc = live ? (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2] : 0;
   double zmax = -INFINITY, zmin = INFINITY;
+  int64_t qmax = INT64_MAX, qmin = INT64_MAX;
   for (int64_t q = sub; q < nc; q += G) {
     double2 ms = vcache[lattice_vertex(g, L, q)];
     double z = (ms.x - theta) * ms.y;
-    zmax = fmax(zmax, z);
-    zmin = fmin(zmin, z);
+    if (z > zmax) { zmax = z; qmax = q; }
+    if (z < zmin) { zmin = z; qmin = q; }
   }
-  zmax = group_max<G>(zmax);
-  zmin = group_min<G>(zmin);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    double zx = __shfl_xor_sync(0xffffffffu, zmax, o), zn = __shfl_xor_sync(0xffffffffu, zmin, o);
+    int64_t qx = __shfl_xor_sync(0xffffffffu, qmax, o), qn = __shfl_xor_sync(0xffffffffu, qmin, o);
+    if (zx > zmax || (zx == zmax && qx < qmax)) { zmax = zx; qmax = qx; }
+    if (zn < zmin || (zn == zmin && qn < qmin)) { zmin = zn; qmin = qn; }
+  }
   if (!live || sub != 0) return;
-  // Q_lo = max P(Y > th) = erfc(-zmax)/2, Q_hi = max P(Y < th) = erfc(zmin)/2
-  double q_lo = 0.5 * erfc(-zmax), q_hi = 0.5 * erfc(zmin);
-  double d = (double)(L.vmax[0] - L.base[0] + 1) * (double)(L.vmax[1] - L.base[1] + 1) *
-             (double)(L.vmax[2] - L.base[2] + 1);
-  double U;
-  if (cs == 2) {
-    U = -expm1(d * log1p(-q_lo));
-  } else if (cs == 3) {
-    U = -expm1(d * log1p(-q_hi));
-  } else {
-    U = -expm1(d * log1p(-q_lo)) - exp(d * log1p(-q_hi));
-    U = U < 0.0 ? 0.0 : (U > 1.0 ? 1.0 : U);
-  }
+  double U = bound_U(cs, node_dcount(L), zmax, zmin);
   nU[n] = U;
   nref[n] = U > alpha ? 1 : 0;
+  if (ext_z) {
+    ext_z[2 * n] = zmax;
+    ext_z[2 * n + 1] = zmin;
+    ext_v[2 * n] = lattice_vertex(g, L, qmax);
+    ext_v[2 * n + 1] = lattice_vertex(g, L, qmin);
+  }
 }
+
+// NEXT-1 (R26): continuous refinement of the lattice extremes (extreme.cu)
+cudaError_t launch_node_extreme(Ctx& c, int level, const uint64_t* front, int64_t nF, double theta,
+                                double alpha, const int8_t* ncase, int8_t* nref, double* nU, const double* ext_z,
+                                const int64_t* ext_v);
 
 __global__ void k_node_records(int level, const uint64_t* __restrict__ front, int64_t nF,
                                const int8_t* __restrict__ ncase, const int8_t* __restrict__ nref,
@@ -391,15 +420,25 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       CK(launch_marginals(c, Q_VERTEX, c.req_sorted.as<int64_t>(), bkt_s, nreq, nullptr, nullptr, nullptr, 0,
                           nullptr));
     }
+    const bool ext = c.opts.extreme_iters > 0 && h > g.h_full;   // NEXT-1
+    if (ext) {
+      CK(c.ext_z.ensure(sizeof(double) * 2 * nF));
+      CK(c.ext_v.ensure(sizeof(int64_t) * 2 * nF));
+    }
+    double* ez = ext ? c.ext_z.as<double>() : nullptr;
+    int64_t* ev = ext ? c.ext_v.as<int64_t>() : nullptr;
 #define BOUND(GG)                                                                                            \
   k_node_bound<GG><<<gw, 256, 0, c.stream>>>(g, level, F, nF, theta, alpha, c.ncase.as<int8_t>(),             \
-                                              c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>())
+                                              c.vcache.as<double2>(), c.nref.as<int8_t>(), c.nU.as<double>(),  \
+                                              ez, ev)
     if (G == 1) BOUND(1);
     else if (G == 4) BOUND(4);
     else if (G == 8) BOUND(8);
     else BOUND(32);
 #undef BOUND
     ++c.n_launch;
+    if (ext) CK(launch_node_extreme(c, level, F, nF, theta, alpha, c.ncase.as<int8_t>(), c.nref.as<int8_t>(),
+                                    c.nU.as<double>(), ez, ev));
     lcp_node_rec_t* rec_out = nullptr;
     const bool keep = level < c.opts.keep_records;
     if (keep) {

@@ -118,6 +118,28 @@ def test_octree_node_sets(name, dev):
             assert np.array_equal(np.sort(leaves_g), leaves_o)
 
 
+@pytest.mark.parametrize("name", ["t1", "t2", "c2", "c3"])
+def test_octree_node_sets_continuous_extremes(name, dev):
+    # NEXT-1 (R26): the deterministic continuous extreme search at coarse nodes,
+    # same iteration on both sides.
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate(name)
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    ctx = Context(0)
+    ctx.fit_local(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(np.array(w.y)).to(dev), kernel, k,
+                  grid, bucket_log2=b, h_full=hf, keep_records=True, extreme_iters=48)
+    M = O.Model.from_config(cfg, w.X, w.y)
+    M.set_extreme(48)
+    th = w.thetas[0]
+    ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    rec_g = ctx.node_records()
+    rec_o, _ = M.octree(th, cfg.alpha, cfg.max_depth)
+    res = compare_node_sets(rec_g, rec_o, cfg.alpha)
+    assert not res["unexcused"], (res["unexcused"][:10], res)
+    assert res["max_dU"] < 1e-6, res
+
+
 @pytest.mark.parametrize("name", ["c1", "t1", "t2"])
 def test_pmc_leaves_parity(name, dev):
     w, ctx, M = _ctx(name, dev, keep_records=False)
