@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--extreme", type=int, default=0,
+                    help="NEXT-1: continuous extreme-search iterations at coarse octree nodes (0 = lattice)")
     ap.add_argument("--dense", action="store_true",
                     help="pruning-free baseline: exact GP (k = m, one bucket), PMC of every cell")
     return ap.parse_args()
@@ -224,9 +226,10 @@ def run_ours(args):
     def step(host=None):
         """fit + run_field for every isovalue; returns (leaves, mc_ms, phase-2 samples)."""
         if host is None:
-            ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
+            ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, extreme_iters=args.extreme, **slab)
         else:
-            ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf, **slab)
+            ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf,
+                          extreme_iters=args.extreme, **slab)
         leaves = 0
         mc_ms = 0.0
         p2 = 0
@@ -347,7 +350,7 @@ def run_ours(args):
            "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
            "config": {"workload": workload_desc(cfg, w.thetas) + (
                           " | DENSE baseline: exact GP k=m, every cell" if args.dense else ""),
-                      "mode": "dense" if args.dense else "octree-pruned", "cells": ncell, "m": cfg.m, "k": k,
+                      "mode": "dense" if args.dense else "octree-pruned", "extreme_iters": args.extreme, "cells": ncell, "m": cfg.m, "k": k,
                       "n_samples": cfg.n_samples, "alpha": cfg.alpha, "max_depth": cfg.max_depth,
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                       "l2": "flushed between timed steps (256 MB write, outside the step events)"},
