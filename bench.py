@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--extreme", type=int, default=0,
                     help="NEXT-1: continuous extreme-search iterations at coarse octree nodes (0 = lattice)")
-    ap.add_argument("--dense", action="store_true",
-                    help="pruning-free baseline: exact GP (k = m, one bucket), PMC of every cell")
+    ap.add_argument("--dense", choices=["exact", "local"], default=None,
+                    help="pruning-free baseline, PMC of every cell: 'exact' = exact GP (k = m, one bucket; "
+                         "BASELINE c3), 'local' = the configured bucket-local GP (isolates the pruning)")
     return ap.parse_args()
 
 
@@ -213,7 +214,8 @@ def run_ours(args):
     if args.dense:
         # pruning-free baseline (BASELINE c3): exact GP (k = m, one bucket), every cell of the slab
         from paper_2512_12442_b200.dist import slab_cells
-        k, b = cfg.m, 0
+        if args.dense == "exact":
+            k, b = cfg.m, 0
         c0, c1 = slab_cells(cfg.cells, 3, rank, world) if world > 1 else (0, ncell)
         dense_cells = torch.arange(c0, c1, dtype=torch.int64, device=dev)
         dense_lcp = torch.empty(c1 - c0, dtype=torch.float32, device=dev)
@@ -349,8 +351,8 @@ def run_ours(args):
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
            "config": {"workload": workload_desc(cfg, w.thetas) + (
-                          " | DENSE baseline: exact GP k=m, every cell" if args.dense else ""),
-                      "mode": "dense" if args.dense else "octree-pruned", "extreme_iters": args.extreme, "cells": ncell, "m": cfg.m, "k": k,
+                          f" | DENSE baseline ({args.dense} GP), every cell" if args.dense else ""),
+                      "mode": f"dense-{args.dense}" if args.dense else "octree-pruned", "extreme_iters": args.extreme, "cells": ncell, "m": cfg.m, "k": k,
                       "n_samples": cfg.n_samples, "alpha": cfg.alpha, "max_depth": cfg.max_depth,
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                       "l2": "flushed between timed steps (256 MB write, outside the step events)"},

@@ -153,6 +153,13 @@ lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, in
                            int64_t n_samples, uint64_t seed, uint32_t iso_index, float* field,
                            int32_t out_on_device, int64_t* n_leaf_out);
 
+/* NEXT-4 level field: register a caller-owned device
+ * array of nx*ny*nz bytes (NULL unregisters).  Every later refine writes, for
+ * each cell, the octree level at which its region stopped: the level of the
+ * pruned node containing it, or max_depth for leaf cells; 255 for cells outside
+ * this rank's z-slab.  The array must stay valid while registered. */
+lcp_status_t lcp_set_level_field(lcp_ctx_t* ctx, uint8_t* level_dev);
+
 /* ---- parity taps (used by tests; not on the hot path) ---- */
 
 /* node records of the last refine (opts.keep_records != 0), levels ascending,

@@ -251,6 +251,12 @@ lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, in
   return LCP_OK;
 }
 
+lcp_status_t lcp_set_level_field(lcp_ctx_t* ctx, uint8_t* level_dev) {
+  CTX_GUARD(ctx);
+  c.level_field = level_dev;
+  return LCP_OK;
+}
+
 lcp_status_t lcp_node_records(lcp_ctx_t* ctx, int64_t* n_out, const lcp_node_rec_t** recs_dev_out) {
   CTX_GUARD(ctx);
   if (!n_out || !recs_dev_out) return set_err(c, LCP_EINVAL, "node_records: null output");

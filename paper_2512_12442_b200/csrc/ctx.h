@@ -107,6 +107,7 @@ struct Ctx {
   int64_t n_leaves = 0;
   DevBuf recs;               // lcp_node_rec_t
   DevBuf ext_z, ext_v;       // NEXT-1: lattice extremes (z, vertex) per node
+  uint8_t* level_field = nullptr;  // NEXT-4: caller-owned per-cell level output (lcp_set_level_field)
   int64_t n_recs = 0;
 
   // leaf pass scratch

@@ -5,8 +5,9 @@
 // For nodes coarser than h_full (whose candidate lattice is strided) that need a
 // bound, one warp per node climbs f(x) = (mu(x) - theta) / (sigma(x) sqrt 2) from
 // the lattice argmax (for Q_lo) and descends from the lattice argmin (for Q_hi)
-// over the node box with a deterministic projected-gradient iteration (the same
-// iteration as oracle/lcp_oracle.c: extreme_search).  Each evaluation of f and
+// over the node box with a deterministic projected-gradient iteration (the
+// iteration DESIGN.md R26 specifies; the CPU oracle implements it
+// independently).  Each evaluation of f and
 // grad f at a point uses the bucket's local GP:
 //   K columns [k_x, d k_x / dx_0, d/dx_1, d/dx_2] for both search points (8 columns),
 //   mu and grad mu = the columns dotted with alpha,

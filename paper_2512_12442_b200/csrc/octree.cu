@@ -261,6 +261,29 @@ __global__ void k_node_records(int level, const uint64_t* __restrict__ front, in
   if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&stats[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
 
+// NEXT-4 level field: the cells of a node that stops
+// at this level (pruned, or refined at max depth) get the level.  G lanes per node.
+template <int G>
+__global__ void k_fill_level(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
+                             const int8_t* __restrict__ nref, uint8_t* __restrict__ field) {
+  int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int sub = threadIdx.x % G;
+  if (n >= nF) return;
+  if (nref[n] && level < max_depth) return;   // continues below
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  const int h = g.lfull - level;
+  const int64_t side = (int64_t)1 << h;
+  const int64_t b0 = (int64_t)i * side, b1 = (int64_t)j * side, b2 = (int64_t)k * side;
+  const int64_t e0 = min(b0 + side, (int64_t)g.cells[0]) - b0, e1 = min(b1 + side, (int64_t)g.cells[1]) - b1,
+                e2 = min(b2 + side, (int64_t)g.cells[2]) - b2;
+  const int64_t tot = e0 * e1 * e2;
+  for (int64_t t = sub; t < tot; t += G) {
+    const int64_t x = b0 + t % e0, y = b1 + (t / e0) % e1, z = b2 + t / (e0 * e1);
+    field[x + (int64_t)g.cells[0] * (y + (int64_t)g.cells[1] * z)] = (uint8_t)level;
+  }
+}
+
 // children / leaf counts of refined nodes
 __global__ void k_node_counts(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
                               const int8_t* __restrict__ nref, int slab_level, int z0, int z1,
@@ -370,6 +393,8 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     z1 = (int)((int64_t)(c.opts.slab_rank + 1) * nz / c.opts.slab_count);
   }
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  if (c.level_field)
+    CK(cudaMemsetAsync(c.level_field, 0xFF, (size_t)g.cells[0] * g.cells[1] * g.cells[2], c.stream));
   for (int level = 0; level <= max_depth && nF > 0; ++level) {
     int h = g.lfull - level;
     CK(c.ncase.ensure(nF));
@@ -450,6 +475,16 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
                                              c.np1.as<double>(), c.np2.as<double>(), c.nU.as<double>(), rec_out,
                                              dcnt + 8);
     ++c.n_launch;
+    if (c.level_field) {
+      if (h <= 2) {
+        k_fill_level<1><<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.level_field);
+      } else {
+        k_fill_level<32><<<(unsigned)((nF * 32 + 255) / 256), 256, 0, c.stream>>>(g, level, max_depth, F, nF,
+                                                                                 c.nref.as<int8_t>(),
+                                                                                 c.level_field);
+      }
+      ++c.n_launch;
+    }
     k_node_counts<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), slab_level, z0, z1,
                                             c.cnt.as<int64_t>());
     ++c.n_launch;

@@ -27,7 +27,7 @@ FP64, FP32 = 0, 1
 EXPORTS = ["lcp_create", "lcp_destroy", "lcp_last_error", "lcp_fit_local", "lcp_octree_refine",
            "lcp_pmc_cells", "lcp_scatter_field", "lcp_run_field", "lcp_node_records",
            "lcp_cell_posterior", "lcp_point_marginals", "lcp_bucket_sets", "lcp_get_info",
-           "lcp_stats_json", "lcp_synchronize"]
+           "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field"]
 
 
 class LcpError(RuntimeError):
@@ -91,6 +91,7 @@ def load_library() -> C.CDLL:
     L.lcp_get_info.argtypes = [P, C.POINTER(InfoT)]
     L.lcp_stats_json.argtypes = [P, C.c_char_p, C.c_size_t]
     L.lcp_synchronize.argtypes = [P]
+    L.lcp_set_level_field.argtypes = [P, P]
     for name in EXPORTS:
         if name not in ("lcp_destroy", "lcp_last_error"):
             getattr(L, name).restype = C.c_int
@@ -231,6 +232,13 @@ class Context:
                                    _is_dev(field), C.byref(n))
         self._check(st, "lcp_run_field")
         return field, n.value
+
+    def set_level_field(self, level=None):
+        """NEXT-4: register a torch uint8 CUDA tensor (nx*ny*nz) that every later
+        refine fills with the octree level at which each cell stopped."""
+        self._level = level
+        self._check(self._L.lcp_set_level_field(self._h, C.c_void_p(_ptr(level))), "lcp_set_level_field")
+        return level
 
     # -- parity taps
     def node_records(self) -> np.ndarray:

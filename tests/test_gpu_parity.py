@@ -315,3 +315,37 @@ def test_full_size_c5_sampled(dev):
     lcp_o = M.pmc_cells(lv[sel], th, cfg.n_samples, cfg.mc_seed)
     frac, mean, mx = lcp_parity(lcp_g, lcp_o, cfg.n_samples)
     assert frac >= 0.99 and mean <= 1e-4, (frac, mean, mx)
+
+
+@pytest.mark.parametrize("name", ["t2", "c2", "p1"])
+def test_level_field(name, dev):
+    # NEXT-4: every cell gets the level of the node it stopped in (pruned), or
+    # max_depth for leaf cells; equals the assembly of the oracle's node records.
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    ncell = int(np.prod(cfg.cells))
+    lvl = ctx.set_level_field(torch.empty(ncell, dtype=torch.uint8, device=dev))
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    got = lvl.cpu().numpy()
+    rec_o, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+    want = np.full(ncell, 255, np.uint8)
+    lf = M.lfull
+    nx, ny, nz = cfg.cells
+    for r in rec_o:
+        L = int(r["level"])
+        if r["refine"] and L < cfg.max_depth:
+            continue
+        side = 1 << (lf - L)
+        x0, y0, z0 = int(r["i"]) * side, int(r["j"]) * side, int(r["k"]) * side
+        xs = np.arange(x0, min(x0 + side, nx))
+        ys = np.arange(y0, min(y0 + side, ny))
+        zs = np.arange(z0, min(z0 + side, nz))
+        ids = (xs[:, None, None] + nx * (ys[None, :, None] + ny * zs[None, None, :])).ravel()
+        want[ids] = L
+    assert np.all(want != 255)
+    if np.array_equal(np.sort(leaves.cpu().numpy()), leaves_o):
+        assert np.array_equal(got, want)
+    else:
+        assert np.mean(got == want) > 0.999
+    ctx.set_level_field(None)

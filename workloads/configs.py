@@ -80,6 +80,14 @@ CONFIGS = {
                  256, 0.01, 0.2, True, 0.0, 0.0, False, 0.01, "mixed",
                  KERNEL_MATERN52, 1.0, (0.03, 0.03, 0.03), 1e-4, 0.0,
                  (0.0,), 128, 5, 2, 4096, 1e-5, 9, "fp64", 1005, 2005),
+    # SURVEY NEXT-4 paper regime: dense, low-noise observations so the posterior s.d. is
+    # ~1.7 % of the prior (the paper's fits have PSNR 33-41 dB); the
+    # non-zero LCP region is a thin shell and the octree prunes ~87 % of the cells.
+    # N = 1600 and alpha = 1e-3 are the paper's settings.
+    "p1": Config("p1", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(128), 4000,
+                 8, 0.1, 0.25, False, 0.5, 0.0, False, 0.001, "uniform",
+                 KERNEL_SE, 0.25, (0.1, 0.1, 0.1), 1e-6, 0.0,
+                 (None,), 64, 3, 2, 1600, 1e-3, 7, "fp64", 1201, 2201),
     # ragged parity case: non-power-of-two grid, bucket grid not dividing it
     "t1": Config("t1", (0.0, 0.0, 0.0), (0.92, 0.68, 0.44), (23, 17, 11), 60,
                  6, 0.05, 0.2, False, 0.0, 0.0, False, 0.01, "uniform",
