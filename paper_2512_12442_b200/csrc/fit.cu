@@ -398,6 +398,8 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   o.keep_records = 0;
   o.extreme_iters = 0;
   if (opts) o = *opts;
+  if (o.precision != LCP_FP64 && o.precision != LCP_FP32) return set_err(c, LCP_EINVAL, "fit: bad precision");
+  if (o.precision == LCP_FP32 && k > 128) return set_err(c, LCP_EINVAL, "fit: the FP32 posterior needs k <= 128");
   if (o.extreme_iters < 0 || o.extreme_iters > 1000) return set_err(c, LCP_EINVAL, "fit: extreme_iters not in [0, 1000]");
   if (o.slab_count < 1) o.slab_count = 1;
   int cmax = std::max(grid->cells[0], std::max(grid->cells[1], grid->cells[2]));

@@ -333,6 +333,107 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
   });
 }
 
+// R17 (BASELINE c2 "FP32 posterior"): the same posterior with the cross-covariance,
+// the solve V = L^-1 K and Sigma = K_cc - V^T V in FP32 (CUDA-core FFMA) from the
+// FP64-built bucket factor (cast on load); mu and Sigma are stored widened to FP64
+// and the 8x8 Cholesky stays FP64 (k_chol8).  Warp per cell, k <= 128.
+__global__ void __launch_bounds__(512) k_cell_posterior_f32(TileArgs a, const int64_t* __restrict__ cells,
+                                                            const int64_t* __restrict__ perm,
+                                                            const int32_t* __restrict__ bkt_sorted, int64_t n,
+                                                            int tile, double* __restrict__ post,
+                                                            int* __restrict__ derr) {
+  extern __shared__ double smem[];
+  int64_t t0 = (int64_t)blockIdx.x * tile;
+  if (t0 >= n) return;
+  int64_t t1 = min(n, t0 + tile);
+  const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
+  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  head = (head + 1) & ~1ll;
+  const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
+  float* sKf = reinterpret_cast<float*>(smem + head + wid * per_warp);   // [j][8] floats
+  const Geom& g = a.g;
+  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* LA,
+                                              const double* alpha, const double* Xs) {
+    for (int64_t q = q0 + wid; q < q1; q += warps) {
+      int64_t slot = perm ? perm[q] : q;
+      int ci, cj, ck;
+      cell_ijk(g, cells[slot], ci, cj, ck);
+      float qx[8][3];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        qx[c][0] = (float)vpos(g, 0, ci + (c & 1));
+        qx[c][1] = (float)vpos(g, 1, cj + ((c >> 1) & 1));
+        qx[c][2] = (float)vpos(g, 2, ck + (c >> 2));
+      }
+      const float var_f = (float)a.kp.var;
+      const float il[3] = {(float)a.kp.inv_ls[0], (float)a.kp.inv_ls[1], (float)a.kp.inv_ls[2]};
+      float mu_p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int j = lane; j < k; j += 32) {
+        const float xj = (float)Xs[j], yj = (float)Xs[k + j], zj = (float)Xs[2 * k + j], al = (float)alpha[j];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float tx = (xj - qx[c][0]) * il[0], ty = (yj - qx[c][1]) * il[1], tz = (zj - qx[c][2]) * il[2];
+          float r2 = tx * tx + ty * ty + tz * tz, kv;
+          if (a.kp.kind == LCP_K_SE) {
+            kv = var_f * expf(-0.5f * r2);
+          } else {
+            float r = sqrtf(r2), s5 = 2.2360679775f * r;
+            kv = var_f * (1.0f + s5 + (5.0f / 3.0f) * r2) * expf(-s5);
+          }
+          sKf[8 * j + c] = kv;
+          mu_p[c] = fmaf(kv, al, mu_p[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mu_p[c] = warp_sum(mu_p[c]);
+      __syncwarp();
+      // V rows i = lane + 32 rb; pair partial sums of V^T V
+      float pp[36];
+#pragma unroll
+      for (int p = 0; p < 36; ++p) pp[p] = 0.0f;
+#pragma unroll
+      for (int rb = 0; rb < 4; ++rb) {
+        const int i = lane + 32 * rb;
+        if (32 * rb >= k) break;
+        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (i < k) {
+          const int rt = i >> 3, ri = i & 7;
+          for (int j = 0; j <= i; ++j) {
+            const float l = (float)LA[la_block(rt, j >> 2) + 4 * ri + (j & 3)];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = fmaf(l, sKf[8 * j + c], v[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int d = 0; d <= c; ++d) pp[c * (c + 1) / 2 + d] = fmaf(v[c], v[d], pp[c * (c + 1) / 2 + d]);
+      }
+#pragma unroll
+      for (int p = 0; p < 36; ++p) pp[p] = warp_sum(pp[p]);
+      double* rec = post + 44 * slot;
+      if (lane < 8) {
+        float muv = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) muv = lane == c ? mu_p[c] : muv;
+        rec[lane] = (double)((float)a.kp.m0 + muv);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < 36; ++p) {
+          const double sv = (double)((float)a.kcc[p] - pp[p]);
+          rec[8 + p] = sv;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (rec[8 + c * (c + 3) / 2] < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      }
+      __syncwarp();
+    }
+  });
+}
+
 static TileArgs make_tile_args(Ctx& c) {
   TileArgs a;
   a.kp = c.kp;
@@ -393,6 +494,22 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
 
 cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* perm,
                                   const int32_t* bkt_sorted, int64_t n, double* post) {
+  if (c.opts.precision == LCP_FP32 && c.k <= 128) {
+    if (n <= 0) return cudaSuccess;
+    TileArgs a = make_tile_args(c);
+    int staged, warps;
+    size_t smem;
+    plan_tile(c, staged, warps, smem);
+    if (warps == 0) return cudaErrorInvalidConfiguration;
+    a.staged = staged;
+    cudaFuncSetAttribute(k_cell_posterior_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int tile = warps * 16;
+    unsigned grid = (unsigned)((n + tile - 1) / tile);
+    k_cell_posterior_f32<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
+                                                               c.derr.as<int>());
+    ++c.n_launch;
+    return cudaGetLastError();
+  }
   if (n <= 0) return cudaSuccess;
   TileArgs a = make_tile_args(c);
   int staged, warps;

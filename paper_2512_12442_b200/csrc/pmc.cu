@@ -355,7 +355,7 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
     const char* v = std::getenv("LCP_POSTERIOR");
     return v && std::strcmp(v, "cell") == 0;
   }();
-  if (!force_cell) {
+  if (!force_cell && c.opts.precision != LCP_FP32) {
     cudaError_t be;
     if (brick_posterior(c, cells, n, post, be)) return LCP_OK;
     if (be != cudaSuccess) return cuda_err(c, be, "brick posterior");
