@@ -114,6 +114,17 @@ lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, i
                            int32_t on_device, const lcp_kernel_t* kernel, int32_t k,
                            const lcp_grid_t* grid, const lcp_opts_t* opts);
 
+/* NEXT-2: the same as lcp_fit_local for a sparse-GP (SGPR) model: inducing
+ * points xyz_M (m x 3), their posterior mean mu_M (m) and covariance A_M
+ * (m x m row-major, symmetric, A_M <= K_MM) as stored after SGPR fitting
+ * (PAPER.md:80-100).  Each bucket keeps its k nearest inducing points and
+ * evaluates Eq. 1 with the A_M term on them.  kernel->nugget
+ * is the jitter added to K_SS (use ~1e-8 sigma_f^2).  Host or device pointers
+ * as for lcp_fit_local.  Errors as lcp_fit_local, plus EINVAL for m > 60000. */
+lcp_status_t lcp_fit_sgpr(lcp_ctx_t* ctx, const double* xyz_M, const double* mu_M, const double* A_M,
+                          int64_t m, int32_t on_device, const lcp_kernel_t* kernel, int32_t k,
+                          const lcp_grid_t* grid, const lcp_opts_t* opts);
+
 /* a5-a6: Alg. 1 as a level-synchronous pass over levels
  * 0..max_depth with the three-case preliminary test and the
  * Slepian bound U = 1 - B_l^d - B_u^d (Eq. 3-4; R6-R9).

@@ -105,6 +105,9 @@ def lib():
         L.orc_local_f_grad.argtypes = [P, C.c_int32, dp, C.c_double, dp]
         L.orc_node_extremes.argtypes = [P, C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int32, dp]
         L.orc_node_extremes.restype = None
+        L.orc_sgpr_exact.argtypes = [C.POINTER(Kernel), dp, dp, dp, C.c_int64, dp, C.c_int64, dp, P]
+        L.orc_model_create_sgpr.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, dp, C.c_int64,
+                                            C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]
         L.orc_free.argtypes = [P]
         L.orc_free.restype = None
         L.orc_num_threads.restype = C.c_int
@@ -146,6 +149,19 @@ def gp_exact(kern: Kernel, X, y, Q, with_cov=True):
     cov = np.zeros((len(Q), len(Q))) if with_cov else None
     _check(lib().orc_gp_exact(C.byref(kern), X, y, len(X), Q, len(Q),
                               mu, cov.ctypes.data if with_cov else None), "gp_exact")
+    return mu, cov
+
+
+def sgpr_exact(kern: Kernel, XM, muM, AM, Q, with_cov=True):
+    """Eq. 1 of an SGPR model at query points Q."""
+    XM = np.ascontiguousarray(XM, np.float64)
+    muM = np.ascontiguousarray(muM, np.float64)
+    AM = np.ascontiguousarray(AM, np.float64)
+    Q = np.ascontiguousarray(Q, np.float64).reshape(-1, 3)
+    mu = np.zeros(len(Q))
+    cov = np.zeros((len(Q), len(Q))) if with_cov else None
+    _check(lib().orc_sgpr_exact(C.byref(kern), XM, muM, AM, len(XM), Q, len(Q), mu,
+                                cov.ctypes.data if with_cov else None), "sgpr_exact")
     return mu, cov
 
 
@@ -198,6 +214,22 @@ class Model:
                                       int(k), int(bucket_log2), int(h_full), C.byref(h)),
                "model_create")
         self._h = h
+
+    @classmethod
+    def sgpr(cls, kern: Kernel, grid: Grid, XM, muM, AM, k, bucket_log2, h_full):
+        """NEXT-2: bucket-local SGPR model (Eq. 1 with the A_M term)."""
+        self = cls.__new__(cls)
+        self.kern, self.grid = kern, grid
+        self.X = np.ascontiguousarray(XM, np.float64)
+        self.y = np.ascontiguousarray(muM, np.float64)
+        self.A = np.ascontiguousarray(AM, np.float64)
+        self.k = int(k)
+        self.cells = tuple(grid.cells)
+        h = C.c_void_p()
+        _check(lib().orc_model_create_sgpr(C.byref(kern), C.byref(grid), self.X, self.y, self.A, len(self.X),
+                                           int(k), int(bucket_log2), int(h_full), C.byref(h)), "model_create_sgpr")
+        self._h = h
+        return self
 
     @classmethod
     def from_config(cls, cfg, X, y, k=None, bucket_log2=None, h_full=None):

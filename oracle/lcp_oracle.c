@@ -164,6 +164,7 @@ struct orc_model {
     int32_t* S;           /* nbuckets x k, ascending observation index */
     double* L;            /* nbuckets x k x k, lower factor of K_y(S_B) */
     double* alpha;        /* nbuckets x k */
+    double* WAW;          /* NEXT-2 SGPR mode: nbuckets x k x k, W A_SS W with W = K_SS^-1 (NULL: GP regression) */
     double* mu_obs;       /* m: local marginal at x_i from bucket(x_i) (R10) */
     double* var_obs;      /* m (floored) */
     int32_t* obs_cell;    /* m x 3 finest cell of x_i (clamped) */
@@ -241,6 +242,11 @@ int orc_local_marginal(const orc_model_t* M, int32_t b, const double* x, double*
     forward_sub(L, k, kv, v);
     double q = orc_kernel(&M->kern, x, x);
     for (int a = 0; a < k; ++a) q -= v[a] * v[a];
+    if (M->WAW) {   /* + K_xS W A_SS W K_Sx (Eq. 1, third term) */
+        const double* C = M->WAW + (size_t)b * k * k;
+        for (int a = 0; a < k; ++a)
+            for (int c = 0; c < k; ++c) q += kv[a] * C[(size_t)a * k + c] * kv[c];
+    }
     *var = q;
     free(kv); free(v);
     return ORC_OK;
@@ -355,9 +361,113 @@ int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const dou
 
 void orc_model_destroy(orc_model_t* M) {
     if (!M) return;
-    free(M->X); free(M->y); free(M->S); free(M->L); free(M->alpha);
+    free(M->X); free(M->y); free(M->S); free(M->L); free(M->alpha); free(M->WAW);
     free(M->mu_obs); free(M->var_obs); free(M->obs_cell);
     free(M);
+}
+
+/* ---------------------------------------------------------------- NEXT-2 --- */
+/* W = K_MM^-1 from the Cholesky factor L of K_MM: column j solves L L^T w = e_j. */
+static void inverse_from_chol(const double* L, int n, double* W) {
+    double* e = calloc(n, sizeof(double));
+    double* t = malloc(sizeof(double) * n);
+    double* w = malloc(sizeof(double) * n);
+    for (int j = 0; j < n; ++j) {
+        e[j] = 1.0;
+        forward_sub(L, n, e, t);
+        backward_sub(L, n, t, w);
+        for (int i = 0; i < n; ++i) W[(size_t)i * n + j] = w[i];
+        e[j] = 0.0;
+    }
+    free(e); free(t); free(w);
+}
+
+/* Eq. 1 literally, for an SGPR model (inducing points X_M,
+ * their posterior mean mu_M and covariance A_M, m x m row-major):
+ *   mu_I    = m0 + K_IM K_MM^-1 (mu_M - m0)
+ *   Sigma_I = K_II - K_IM K_MM^-1 K_MI + K_IM K_MM^-1 A_M K_MM^-1 K_MI,
+ * with K_MM + jitter I (jitter = kern->nugget). */
+int orc_sgpr_exact(const orc_kernel_t* kern, const double* XM, const double* muM, const double* AM, int64_t m,
+                   const double* Q, int64_t nq, double* mu, double* cov) {
+    int n = (int)m;
+    double* K = malloc(sizeof(double) * n * n);
+    double* L = malloc(sizeof(double) * n * n);
+    double* W = malloc(sizeof(double) * n * n);
+    double* KQ = malloc(sizeof(double) * nq * n);
+    double* P = malloc(sizeof(double) * nq * n);   /* K_IM W */
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b)
+            K[a * n + b] = orc_kernel(kern, XM + 3 * a, XM + 3 * b) + (a == b ? kern->nugget : 0.0);
+    int st = chol_jitter(K, L, n, kern->variance);
+    if (st == ORC_OK) {
+        inverse_from_chol(L, n, W);
+        for (int64_t q = 0; q < nq; ++q)
+            for (int a = 0; a < n; ++a) KQ[q * n + a] = orc_kernel(kern, Q + 3 * q, XM + 3 * a);
+        for (int64_t q = 0; q < nq; ++q)
+            for (int b = 0; b < n; ++b) {
+                double s = 0.0;
+                for (int a = 0; a < n; ++a) s += KQ[q * n + a] * W[(size_t)a * n + b];
+                P[q * n + b] = s;
+            }
+        for (int64_t q = 0; q < nq; ++q) {
+            double s = 0.0;
+            for (int a = 0; a < n; ++a) s += P[q * n + a] * (muM[a] - kern->prior_mean);
+            mu[q] = kern->prior_mean + s;
+        }
+        if (cov)
+            for (int64_t p = 0; p < nq; ++p)
+                for (int64_t q = 0; q < nq; ++q) {
+                    double s = orc_kernel(kern, Q + 3 * p, Q + 3 * q);
+                    for (int a = 0; a < n; ++a) s -= P[p * n + a] * KQ[q * n + a];
+                    for (int a = 0; a < n; ++a)
+                        for (int b = 0; b < n; ++b) s += P[p * n + a] * AM[(size_t)a * n + b] * P[q * n + b];
+                    cov[p * nq + q] = s;
+                }
+    }
+    free(K); free(L); free(W); free(KQ); free(P);
+    return st;
+}
+
+/* Bucket-local SGPR: each bucket keeps its k nearest inducing points S (R2) and
+ * Eq. 1 restricted to S: L = chol(K_SS + jitter), alpha = W (mu_S - m0),
+ * WAW = W A_SS W.  Marginals / cell posteriors add the third term of Eq. 1. */
+int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM, const double* muM,
+                          const double* AM, int64_t m, int32_t k, int32_t bucket_log2, int32_t h_full,
+                          orc_model_t** out) {
+    /* the k-NN sets, K_SS factor and alpha are the GP-regression model with nugget = jitter */
+    int st = orc_model_create(kern, grid, XM, muM, m, k, bucket_log2, h_full, out);
+    if (st != ORC_OK) return st;
+    orc_model_t* M = *out;
+    M->WAW = malloc(sizeof(double) * (size_t)M->nbuckets * k * k);
+#pragma omp parallel for schedule(dynamic)
+    for (int32_t bkt = 0; bkt < M->nbuckets; ++bkt) {
+        const int32_t* S = M->S + (size_t)bkt * k;
+        const double* Lb = M->L + (size_t)bkt * k * k;
+        double* W = malloc(sizeof(double) * k * k);
+        double* T = malloc(sizeof(double) * k * k);
+        inverse_from_chol(Lb, k, W);
+        for (int a = 0; a < k; ++a)          /* T = W A_SS */
+            for (int c = 0; c < k; ++c) {
+                double s = 0.0;
+                for (int d = 0; d < k; ++d) s += W[(size_t)a * k + d] * AM[(size_t)S[d] * m + S[c]];
+                T[(size_t)a * k + c] = s;
+            }
+        double* C = M->WAW + (size_t)bkt * k * k;
+        for (int a = 0; a < k; ++a)          /* W A_SS W */
+            for (int c = 0; c < k; ++c) {
+                double s = 0.0;
+                for (int d = 0; d < k; ++d) s += T[(size_t)a * k + d] * W[(size_t)d * k + c];
+                C[(size_t)a * k + c] = s;
+            }
+        free(W); free(T);
+    }
+    /* observation marginals now include the A term */
+    for (int64_t i = 0; i < m; ++i) {
+        double var;
+        orc_local_marginal(M, orc_point_bucket(M, XM + 3 * i), XM + 3 * i, &M->mu_obs[i], &var);
+        if (floor_var(M, var, &M->var_obs[i]) != ORC_OK) { orc_model_destroy(M); *out = NULL; return ORC_ENUMERIC; }
+    }
+    return ORC_OK;
 }
 
 /* ------------------------------------------------------------------ C8 --- */
@@ -371,22 +481,27 @@ int orc_cell_posterior(const orc_model_t* M, int64_t cell, double* mu, double* c
     const double* al = M->alpha + (size_t)b * k;
     double xc[8][3];
     for (int c = 0; c < 8; ++c) vertex_pos(M, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2), xc[c]);
-    double* K = malloc(sizeof(double) * k);
+    double* K = malloc(sizeof(double) * 8 * k);
     double* V = malloc(sizeof(double) * 8 * k);
     for (int c = 0; c < 8; ++c) {
         double s = 0.0;
+        double* Kc = K + (size_t)c * k;
         for (int a = 0; a < k; ++a) {
-            K[a] = orc_kernel(&M->kern, M->X + 3 * (size_t)S[a], xc[c]);
-            s += K[a] * al[a];
+            Kc[a] = orc_kernel(&M->kern, M->X + 3 * (size_t)S[a], xc[c]);
+            s += Kc[a] * al[a];
         }
         mu[c] = M->kern.prior_mean + s;
-        forward_sub(L, k, K, V + (size_t)c * k);
+        forward_sub(L, k, Kc, V + (size_t)c * k);
     }
     int st = ORC_OK;
+    const double* Cw = M->WAW ? M->WAW + (size_t)b * k * k : NULL;
     for (int c = 0; c < 8; ++c)
         for (int e = 0; e < 8; ++e) {
             double s = orc_kernel(&M->kern, xc[c], xc[e]);
             for (int a = 0; a < k; ++a) s -= V[(size_t)c * k + a] * V[(size_t)e * k + a];
+            if (Cw)   /* + K_cS W A_SS W K_Se (Eq. 1, third term) */
+                for (int a = 0; a < k; ++a)
+                    for (int d = 0; d < k; ++d) s += K[(size_t)c * k + a] * Cw[(size_t)a * k + d] * K[(size_t)e * k + d];
             cov[c * 8 + e] = s;
         }
     for (int c = 0; c < 8; ++c)

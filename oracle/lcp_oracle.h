@@ -91,6 +91,15 @@ int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double 
 /* C5: P(Y < theta), P(Y > theta) for Y ~ N(mu, var). */
 void orc_tail_probs(double mu, double var, double theta, double* p_lo, double* p_hi);
 
+/* NEXT-2: SGPR model (inducing points X_M, posterior mean mu_M, covariance A_M m x m
+ * row-major): Eq. 1 globally, and restricted to each bucket's k
+ * nearest inducing points.  kern->nugget is the jitter added to K_MM. */
+int orc_sgpr_exact(const orc_kernel_t* kern, const double* XM, const double* muM, const double* AM, int64_t m,
+                   const double* Q, int64_t nq, double* mu, double* cov);
+int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM, const double* muM,
+                          const double* AM, int64_t m, int32_t k, int32_t bucket_log2, int32_t h_full,
+                          orc_model_t** out);
+
 /* NEXT-1 (R26): continuous extreme search at nodes with h > h_full; iters = 0 disables. */
 void orc_model_set_extreme(orc_model_t* M, int32_t iters);
 /* f = (mu - theta) / (sigma sqrt 2) of bucket b's local GP at x, and grad f (3) */

@@ -146,7 +146,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
-                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.ext_z, &c.ext_v};
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.ext_z, &c.ext_v, &c.sgpr_A};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)
@@ -161,6 +161,16 @@ lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, i
                            const lcp_kernel_t* kernel, int32_t k, const lcp_grid_t* grid, const lcp_opts_t* opts) {
   CTX_GUARD(ctx);
   return fit_impl(c, xyz, y, m, on_device, kernel, k, grid, opts);
+}
+
+lcp_status_t lcp_fit_sgpr(lcp_ctx_t* ctx, const double* xyz_M, const double* mu_M, const double* A_M, int64_t m,
+                          int32_t on_device, const lcp_kernel_t* kernel, int32_t k, const lcp_grid_t* grid,
+                          const lcp_opts_t* opts) {
+  CTX_GUARD(ctx);
+  if (!A_M) return set_err(c, LCP_EINVAL, "fit_sgpr: null A_M");
+  if (m > 60000) return set_err(c, LCP_EINVAL, "fit_sgpr: m > 60000 (A_M would exceed 28 GB)");
+  if (k > 1024) return set_err(c, LCP_EINVAL, "fit_sgpr: k > 1024");
+  return fit_impl(c, xyz_M, mu_M, m, on_device, kernel, k, grid, opts, A_M);
 }
 
 lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold, int32_t max_depth,

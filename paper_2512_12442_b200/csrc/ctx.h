@@ -82,6 +82,7 @@ struct Ctx {
   DevBuf S;                  // int32 nbuckets x k (ascending)
   DevBuf bdata;              // double nbuckets x bstride
   DevBuf fscratch;           // factor scratch for large k
+  DevBuf sgpr_A;             // NEXT-2: A_M (m x m) of an SGPR model
   DevBuf obs_key, obs_sorted_key, obs_sorted_idx;  // Morton keys of the finest cell
   DevBuf obs_mu, obs_sd;     // observation marginals (Morton order after fit)
   DevBuf plo, phi;           // per-theta observation tails (Morton order)
@@ -133,7 +134,8 @@ cudaError_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t 
 cudaError_t group_by_bucket(Ctx& c, const int32_t* bucket_of_item, int64_t n, int64_t* perm_out);
 
 lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* y, int64_t m, int on_device,
-                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts);
+                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts,
+                      const double* AM = nullptr);
 lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth);
 lcp_status_t pmc_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double theta, int64_t N,
                       uint64_t seed, uint32_t iso, float* out_dev);

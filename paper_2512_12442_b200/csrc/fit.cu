@@ -360,6 +360,165 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
   }
 }
 
+// NEXT-2: SGPR bucket factor.  Eq. 1 restricted to the bucket's k nearest
+// inducing points S:  mu(x) = m0 + k_x^T W (mu_S - m0),
+//   Sigma = K - k^T C k,  C = W - W A_SS W,  W = (K_SS + jitter)^-1.
+// C is factored as C = G^T G with G LOWER triangular (Cholesky of the
+// index-reversed matrix P C P = R R^T, G = P R^T P; PSD clamp as R14), so the
+// bucket block [G as DMMA A-fragments | beta = W (mu_S - m0) | x_S] has the
+// same form as the GP-regression block (G = L^-1 there) and every downstream
+// kernel is unchanged.  Persistent CTAs with dense k x k global scratch.
+__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams kp, int k, const double* __restrict__ X,
+                                                                     const double* __restrict__ muM,
+                                                                     const double* __restrict__ AM, int64_t m,
+                                                                     const int32_t* __restrict__ S,
+                                                                     double* __restrict__ bdata, int64_t bstride,
+                                                                     double* __restrict__ scratch, int nbuckets,
+                                                                     int* __restrict__ derr) {
+  extern __shared__ double sm[];
+  __shared__ int s_ok;
+  __shared__ double s_piv;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t kk = (int64_t)k * k;
+  double* M0 = scratch + (int64_t)blockIdx.x * 5 * kk;   // K -> L, later C
+  double* M1 = M0 + kk;                                  // L^-1, later T = W A
+  double* M2 = M1 + kk;                                  // W
+  double* M3 = M2 + kk;                                  // A_SS, later R
+  double* sx = sm;
+  double* sy = sx + k;
+  double* sz = sy + k;
+  double* rr = sz + k;
+  const int64_t LA = la_size(k);
+  for (int b = blockIdx.x; b < nbuckets; b += gridDim.x) {
+    const int32_t* Sb = S + (int64_t)b * k;
+    double* out = bdata + (int64_t)b * bstride;
+    __syncthreads();
+    for (int a = tid; a < k; a += bd) {
+      int64_t o = Sb[a];
+      sx[a] = X[3 * o]; sy[a] = X[3 * o + 1]; sz[a] = X[3 * o + 2];
+      rr[a] = muM[o] - kp.m0;
+      out[LA + k + a] = sx[a]; out[LA + 2 * k + a] = sy[a]; out[LA + 3 * k + a] = sz[a];
+    }
+    bool ok = false;
+    for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+      double jit = kp.nugget + (attempt == 0 ? 0.0 : 1e-10 * kp.var * (attempt == 1 ? 1.0 : attempt == 2 ? 10.0 : 100.0));
+      __syncthreads();
+      for (int64_t e = tid; e < kk; e += bd) {
+        int i = (int)(e / k), j = (int)(e % k);
+        double r2 = kern_r2(kp, sx[i] - sx[j], sy[i] - sy[j], sz[i] - sz[j]);
+        M0[e] = kern_from_r2(kp, r2) + (i == j ? jit : 0.0);
+      }
+      if (tid == 0) s_ok = 1;
+      for (int j = 0; j < k; ++j) {
+        __syncthreads();
+        if (tid == 0) {
+          double d = M0[(int64_t)j * k + j];
+          if (!(d > 0.0)) s_ok = 0;
+          else { d = sqrt(d); M0[(int64_t)j * k + j] = d; s_piv = d; }
+        }
+        __syncthreads();
+        if (!s_ok) break;
+        const double piv = s_piv;
+        for (int i = j + 1 + tid; i < k; i += bd) M0[(int64_t)i * k + j] /= piv;
+        __syncthreads();
+        for (int64_t e = tid; e < (int64_t)(k - j - 1) * (k - j - 1); e += bd) {
+          int i = j + 1 + (int)(e / (k - j - 1)), l = j + 1 + (int)(e % (k - j - 1));
+          if (l <= i) M0[(int64_t)i * k + l] -= M0[(int64_t)i * k + j] * M0[(int64_t)l * k + j];
+        }
+      }
+      __syncthreads();
+      ok = s_ok != 0;
+    }
+    if (!ok) {
+      if (tid == 0) atomicOr(derr, DERR_FACTOR);
+      continue;
+    }
+    // L^-1 (column forward substitutions)
+    for (int j = tid; j < k; j += bd) {
+      for (int i = 0; i < j; ++i) M1[(int64_t)i * k + j] = 0.0;
+      M1[(int64_t)j * k + j] = 1.0 / M0[(int64_t)j * k + j];
+      for (int i = j + 1; i < k; ++i) {
+        double s = 0.0;
+        for (int p = j; p < i; ++p) s = fma(M0[(int64_t)i * k + p], M1[(int64_t)p * k + j], s);
+        M1[(int64_t)i * k + j] = -s / M0[(int64_t)i * k + i];
+      }
+    }
+    // A_SS
+    for (int64_t e = tid; e < kk; e += bd) M3[e] = AM[(int64_t)Sb[e / k] * m + Sb[e % k]];
+    __syncthreads();
+    // W = L^-T L^-1
+    for (int64_t e = tid; e < kk; e += bd) {
+      int i = (int)(e / k), j = (int)(e % k);
+      double s = 0.0;
+      for (int l = max(i, j); l < k; ++l) s = fma(M1[(int64_t)l * k + i], M1[(int64_t)l * k + j], s);
+      M2[e] = s;
+    }
+    __syncthreads();
+    // beta = W r -> alpha slot;  T = W A_SS (into M1)
+    for (int i = tid; i < k; i += bd) {
+      double s = 0.0;
+      for (int l = 0; l < k; ++l) s = fma(M2[(int64_t)i * k + l], rr[l], s);
+      out[LA + i] = s;
+    }
+    for (int64_t e = tid; e < kk; e += bd) {
+      int i = (int)(e / k), j = (int)(e % k);
+      double s = 0.0;
+      for (int l = 0; l < k; ++l) s = fma(M2[(int64_t)i * k + l], M3[(int64_t)l * k + j], s);
+      M1[e] = s;
+    }
+    __syncthreads();
+    // C = W - T W, stored index-reversed and symmetrised: M0[i][j] = C[k-1-i][k-1-j]
+    for (int64_t e = tid; e < kk; e += bd) {
+      int i = (int)(e / k), j = (int)(e % k);
+      double s1 = 0.0, s2 = 0.0;
+      for (int l = 0; l < k; ++l) {
+        s1 = fma(M1[(int64_t)i * k + l], M2[(int64_t)l * k + j], s1);
+        s2 = fma(M1[(int64_t)j * k + l], M2[(int64_t)l * k + i], s2);
+      }
+      double c = M2[e] - 0.5 * (s1 + s2);
+      M0[(int64_t)(k - 1 - i) * k + (k - 1 - j)] = c;
+    }
+    __syncthreads();
+    // clamped Cholesky of P C P (in place, lower), tol = 1e-12 max diag
+    if (tid == 0) {
+      double md = 0.0;
+      for (int i = 0; i < k; ++i) md = fmax(md, M0[(int64_t)i * k + i]);
+      s_piv = 1e-12 * md;
+    }
+    __syncthreads();
+    const double tol = s_piv;
+    for (int j = 0; j < k; ++j) {
+      __syncthreads();
+      if (tid == 0) {
+        double d = M0[(int64_t)j * k + j];
+        s_ok = d > tol;
+        M0[(int64_t)j * k + j] = d > tol ? sqrt(d) : 0.0;
+      }
+      __syncthreads();
+      const bool live = s_ok;
+      const double piv = M0[(int64_t)j * k + j];
+      for (int i = j + 1 + tid; i < k; i += bd) M0[(int64_t)i * k + j] = live ? M0[(int64_t)i * k + j] / piv : 0.0;
+      __syncthreads();
+      for (int64_t e = tid; e < (int64_t)(k - j - 1) * (k - j - 1); e += bd) {
+        int i = j + 1 + (int)(e / (k - j - 1)), l = j + 1 + (int)(e % (k - j - 1));
+        if (l <= i) M0[(int64_t)i * k + l] -= M0[(int64_t)i * k + j] * M0[(int64_t)l * k + j];
+      }
+    }
+    __syncthreads();
+    // G = P R^T P (lower): G[i][j] = R[k-1-j][k-1-i], written as DMMA A-fragments
+    for (int64_t e = tid; e < LA; e += bd) {
+      const int64_t blk = e >> 5;
+      const int ln = (int)(e & 31);
+      int rt = (int)((sqrt(4.0 * (double)blk + 1.0) - 1.0) * 0.5);
+      while ((int64_t)(rt + 1) * (rt + 2) <= blk) ++rt;
+      while ((int64_t)rt * (rt + 1) > blk) --rt;
+      const int js = (int)(blk - (int64_t)rt * (rt + 1));
+      const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
+      out[e] = (i < k && j <= i) ? M0[(int64_t)(k - 1 - j) * k + (k - 1 - i)] : 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------------------------- host
 static int ilog2_ceil(int v) {
   int l = 0;
@@ -379,7 +538,8 @@ static double host_kern(const KernParams& p, const double* a, const double* b) {
 }
 
 lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, int on_device,
-                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts) {
+                      const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts,
+                      const double* AM) {
   if (!xyz || !yv || !kern || !grid) return set_err(c, LCP_EINVAL, "fit: null argument");
   if (m < 1 || k < 1 || (int64_t)k > m) return set_err(c, LCP_EINVAL, "fit: need 1 <= k <= m");
   if (k > 1024 && (int64_t)k != m) return set_err(c, LCP_EINVAL, "fit: k > 1024 requires k == m");
@@ -523,7 +683,21 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     }
   }
   // a3
-  {
+  if (AM) {
+    // NEXT-2 SGPR factors (A_M uploaded as m x m)
+    CK(c.sgpr_A.ensure(sizeof(double) * (size_t)m * m));
+    CK(cudaMemcpyAsync(c.sgpr_A.p, AM, sizeof(double) * (size_t)m * m,
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    int grid_f = std::min(nbk, c.sm_count * 2);
+    CK(c.fscratch.ensure(sizeof(double) * 5 * (size_t)k * k * grid_f));
+    size_t smem = sizeof(double) * 4 * (size_t)k;
+    k_bucket_factor_sgpr<<<grid_f, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.sgpr_A.as<double>(),
+                                                                   m, c.S.as<int32_t>(), c.bdata.as<double>(),
+                                                                   c.bstride, c.fscratch.as<double>(), nbk,
+                                                                   c.derr.as<int>());
+    ++c.n_launch;
+    CK(cudaGetLastError());
+  } else {
     size_t head = sizeof(double) * 5 * (size_t)k;
     size_t full = head + sizeof(double) * 2 * (size_t)tri;
     int use_smem = full <= 200 * 1024;

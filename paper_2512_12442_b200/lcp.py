@@ -27,7 +27,7 @@ FP64, FP32 = 0, 1
 EXPORTS = ["lcp_create", "lcp_destroy", "lcp_last_error", "lcp_fit_local", "lcp_octree_refine",
            "lcp_pmc_cells", "lcp_scatter_field", "lcp_run_field", "lcp_node_records",
            "lcp_cell_posterior", "lcp_point_marginals", "lcp_bucket_sets", "lcp_get_info",
-           "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field"]
+           "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field", "lcp_fit_sgpr"]
 
 
 class LcpError(RuntimeError):
@@ -92,6 +92,8 @@ def load_library() -> C.CDLL:
     L.lcp_stats_json.argtypes = [P, C.c_char_p, C.c_size_t]
     L.lcp_synchronize.argtypes = [P]
     L.lcp_set_level_field.argtypes = [P, P]
+    L.lcp_fit_sgpr.argtypes = [P, P, P, P, i64, i32, C.POINTER(KernelT), i32, C.POINTER(GridT),
+                               C.POINTER(OptsT)]
     for name in EXPORTS:
         if name not in ("lcp_destroy", "lcp_last_error"):
             getattr(L, name).restype = C.c_int
@@ -168,6 +170,29 @@ class Context:
         st = self._L.lcp_fit_local(self._h, C.c_void_p(_ptr(xyz)), C.c_void_p(_ptr(y)), len(y),
                                    _is_dev(xyz), C.byref(kt), int(k), C.byref(gt), C.byref(ot))
         self._check(st, "lcp_fit_local")
+        self.grid = (tuple(lo), tuple(hi), tuple(cells))
+        return self
+
+    def fit_sgpr(self, xyz_M, mu_M, A_M, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,
+                 h_full: int = 2, keep_records=False, extreme_iters: int = 0):
+        """NEXT-2: bucket-local Eq. 1 of an SGPR model (inducing points, mean, covariance A_M)."""
+        if keep_records is True:
+            keep_records = 64
+        kind, var, ls, nug, m0 = kernel
+        ls = list(np.broadcast_to(np.asarray(ls, dtype=np.float64), (3,)))
+        kt = KernelT(int(kind), 0, float(var), (C.c_double * 3)(*ls), float(nug), float(m0))
+        lo, hi, cells = grid
+        gt = GridT((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int32 * 3)(*cells), 0)
+        ot = OptsT(bucket_log2, h_full, FP64, 0, 1, 3, int(keep_records), int(extreme_iters))
+        if isinstance(xyz_M, np.ndarray):
+            xyz_M = np.ascontiguousarray(xyz_M, np.float64)
+            mu_M = np.ascontiguousarray(mu_M, np.float64)
+            A_M = np.ascontiguousarray(A_M, np.float64)
+        self._keep = (xyz_M, mu_M, A_M)
+        st = self._L.lcp_fit_sgpr(self._h, C.c_void_p(_ptr(xyz_M)), C.c_void_p(_ptr(mu_M)),
+                                  C.c_void_p(_ptr(A_M)), len(mu_M), _is_dev(xyz_M), C.byref(kt), int(k),
+                                  C.byref(gt), C.byref(ot))
+        self._check(st, "lcp_fit_sgpr")
         self.grid = (tuple(lo), tuple(hi), tuple(cells))
         return self
 

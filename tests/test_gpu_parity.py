@@ -377,3 +377,48 @@ def test_fp32_posterior_c2(dev):
     # FP32 mode misses BASELINE's 99.9 % bar by a hair; the FP64 posterior is the default
     # for every config (R17).  Guard the measured level here.
     assert frac >= 0.995 and mean <= 1e-4, (frac, mean, mx)
+
+
+def _sgpr_inputs(name, noise_scale):
+    w = generate(name)
+    cfg = w.cfg
+    sn2 = cfg.nugget * noise_scale
+    kern_gp = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, sn2, cfg.prior_mean)
+    K = np.array([[O.kernel_value(kern_gp, a, b) for b in w.X] for a in w.X])
+    Ky = K + sn2 * np.eye(len(w.X))
+    muM = cfg.prior_mean + K @ np.linalg.solve(Ky, w.y - cfg.prior_mean)
+    AM = sn2 * K @ np.linalg.inv(Ky)
+    return w, cfg, muM, 0.5 * (AM + AM.T)
+
+
+@pytest.mark.parametrize("name", ["t1", "t2", "c2"])
+def test_sgpr_parity(name, dev):
+    # NEXT-2: bucket-local Eq. 1 with the A_M term (lcp_fit_sgpr) vs the oracle's literal Eq. 1
+    from paper_2512_12442_b200 import Context
+    w, cfg, muM, AM = _sgpr_inputs(name, 20.0)
+    jitter = 1e-9 * cfg.variance
+    kernel = (cfg.kernel, cfg.variance, cfg.lengthscale, jitter, cfg.prior_mean)
+    grid = (cfg.lo, cfg.hi, cfg.cells)
+    ctx = Context(0).fit_sgpr(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(muM).to(dev),
+                              torch.from_numpy(AM).to(dev), kernel, cfg.k, grid, bucket_log2=cfg.bucket_log2,
+                              h_full=cfg.h_full, keep_records=True)
+    M = O.Model.sgpr(O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, jitter, cfg.prior_mean),
+                     O.make_grid(cfg.lo, cfg.hi, cfg.cells), w.X, muM, AM, cfg.k, cfg.bucket_log2, cfg.h_full)
+    cells = random_cells(name, 200, 5)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    worst = (0.0, 0.0)
+    for q, c in enumerate(cells):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
+        worst = (max(worst[0], em), max(worst[1], ec))
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    rec_o, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+    res = compare_node_sets(ctx.node_records(), rec_o, cfg.alpha)
+    assert not res["unexcused"], (res["unexcused"][:10], res)
+    sel = np.arange(0, len(leaves), max(1, len(leaves) // 300))
+    lcp_g = ctx.pmc_cells(leaves, th, 1000, cfg.mc_seed).cpu().numpy()[sel]
+    lcp_o = M.pmc_cells(leaves.cpu().numpy()[sel], th, 1000, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1000)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)

@@ -1,0 +1,91 @@
+"""Pins for NEXT-2: SGPR models (Eq. 1 with the A_M term).  CPU only."""
+import numpy as np
+
+import oracle as O
+from workloads import generate
+
+SE, MAT = 0, 1
+
+
+def _gp_to_sgpr(kern_noisy, X, y, sn2):
+    """The exact GP posterior of inducing values at M = X (R1):
+    mu_M = K (K + sn2 I)^-1 y, A_M = sn2 K (K + sn2 I)^-1 (test-side construction)."""
+    K = np.array([[O.kernel_value(kern_noisy, a, b) for b in X] for a in X])
+    Ky = K + sn2 * np.eye(len(X))
+    muM = K @ np.linalg.solve(Ky, y)
+    AM = sn2 * K @ np.linalg.inv(Ky)
+    return muM, 0.5 * (AM + AM.T)
+
+
+def test_sgpr_reduces_to_gp_regression():
+    # Eq. 1 with (mu_M, A_M) of R1 equals GP regression with nugget sn2
+    g = np.random.default_rng(1)
+    X = g.random((24, 3))
+    y = g.standard_normal(24)
+    sn2 = 2e-3
+    kern_gp = O.make_kernel(SE, 1.0, 0.3, sn2)
+    kern_sg = O.make_kernel(SE, 1.0, 0.3, 0.0)
+    muM, AM = _gp_to_sgpr(kern_gp, X, y, sn2)
+    Q = g.random((7, 3))
+    mu_s, cov_s = O.sgpr_exact(kern_sg, X, muM, AM, Q)
+    mu_g, cov_g = O.gp_exact(kern_gp, X, y, Q)
+    assert np.abs(mu_s - mu_g).max() < 1e-7
+    assert np.abs(cov_s - cov_g).max() < 1e-7
+
+
+def test_sgpr_special_cases():
+    g = np.random.default_rng(2)
+    X = g.random((20, 3))
+    muM = g.standard_normal(20)
+    kern = O.make_kernel(MAT, 0.8, 0.25, 0.0, prior_mean=0.1)
+    K = np.array([[O.kernel_value(kern, a, b) for b in X] for a in X])
+    # A_M = 0: the inducing values are known -> interpolation with zero variance
+    mu, cov = O.sgpr_exact(kern, X, muM, np.zeros((20, 20)), X)
+    assert np.abs(mu - muM).max() < 1e-8 and np.abs(np.diag(cov)).max() < 1e-8
+    # A_M = K_MM: the inducing values carry no information -> the prior covariance
+    Q = g.random((6, 3))
+    mu, cov = O.sgpr_exact(kern, X, muM, K, Q)
+    KQQ = np.array([[O.kernel_value(kern, a, b) for b in Q] for a in Q])
+    assert np.abs(cov - KQQ).max() < 1e-8
+    # far field: prior mean and variance
+    mu, cov = O.sgpr_exact(kern, X, muM, 0.3 * K, np.array([[40.0, 40.0, 40.0]]))
+    assert abs(mu[0] - 0.1) < 1e-14 and abs(cov[0, 0] - 0.8) < 1e-14
+
+
+def _sgpr_workload(name, noise_scale):
+    w = generate(name)
+    cfg = w.cfg
+    sn2 = cfg.nugget * noise_scale
+    kern_gp = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, sn2, cfg.prior_mean)
+    muM, AM = _gp_to_sgpr(kern_gp, w.X, w.y - cfg.prior_mean, sn2)
+    return w, cfg, muM + cfg.prior_mean, AM
+
+
+def test_local_sgpr_with_k_equal_m_is_global_eq1():
+    w, cfg, muM, AM = _sgpr_workload("t1", 30.0)
+    kern = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, 1e-10, cfg.prior_mean)
+    grid = O.make_grid(cfg.lo, cfg.hi, cfg.cells)
+    M = O.Model.sgpr(kern, grid, w.X, muM, AM, cfg.m, 0, cfg.h_full)
+    nx, ny = cfg.cells[0], cfg.cells[1]
+    h = [(cfg.hi[d] - cfg.lo[d]) / cfg.cells[d] for d in range(3)]
+    for cell in (0, 555, 2000, 4300):
+        i, j, k = cell % nx, (cell // nx) % ny, cell // (nx * ny)
+        Q = np.array([[cfg.lo[0] + (i + (c & 1)) * h[0], cfg.lo[1] + (j + ((c >> 1) & 1)) * h[1],
+                       cfg.lo[2] + (k + (c >> 2)) * h[2]] for c in range(8)])
+        mu_e, cov_e = O.sgpr_exact(kern, w.X, muM, AM, Q)
+        mu_l, cov_l = M.cell_posterior(cell)
+        assert np.abs(mu_l - mu_e).max() < 1e-9
+        assert np.abs(cov_l - cov_e).max() < 1e-9
+        m7, v7 = M.local_marginal(M.cell_bucket(cell), Q[7])
+        assert abs(m7 - mu_l[7]) < 1e-12 and abs(v7 - cov_l[7, 7]) < 1e-12
+
+
+def test_local_sgpr_octree_and_pmc_run():
+    w, cfg, muM, AM = _sgpr_workload("t2", 10.0)
+    kern = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, 1e-10, cfg.prior_mean)
+    grid = O.make_grid(cfg.lo, cfg.hi, cfg.cells)
+    M = O.Model.sgpr(kern, grid, w.X, muM, AM, cfg.k, cfg.bucket_log2, cfg.h_full)
+    recs, leaves = M.octree(w.thetas[0], cfg.alpha, cfg.max_depth)
+    assert len(leaves) > 0
+    lcp = M.pmc_cells(leaves[::50], w.thetas[0], 400, 3)
+    assert np.all((lcp >= 0) & (lcp <= 1))
