@@ -91,6 +91,11 @@ def lib():
                                    C.c_uint32]
         L.orc_pmc_cells.argtypes = [P, ip64, C.c_int64, C.c_double, C.c_int64, C.c_uint64,
                                     C.c_uint32, dp]
+        L.orc_mc_count_multi.restype = None
+        L.orc_mc_count_multi.argtypes = [dp, dp, dp, C.c_int32, C.c_int64, C.c_uint64, C.c_int64,
+                                         C.c_uint32, ip64]
+        L.orc_pmc_cells_multi.argtypes = [P, ip64, C.c_int64, dp, C.c_int32, P, C.c_int64,
+                                          C.c_uint64, C.c_uint32, dp]
         L.orc_eval_node.argtypes = [P, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, P]
         L.orc_octree.argtypes = [P, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_int32,
@@ -188,6 +193,15 @@ def mc_count(mu, L, theta, n_samples, seed, cell, iso_index=0):
     return lib().orc_mc_count(np.ascontiguousarray(mu, np.float64).reshape(8),
                               np.ascontiguousarray(L, np.float64).reshape(64), theta,
                               n_samples, seed, cell, iso_index)
+
+
+def mc_count_multi(mu, L, thetas, n_samples, seed, cell, stream=0):
+    th = np.ascontiguousarray(thetas, np.float64)
+    out = np.zeros(len(th), np.int64)
+    lib().orc_mc_count_multi(np.ascontiguousarray(mu, np.float64),
+                             np.ascontiguousarray(np.asarray(L, np.float64).reshape(64)), th, len(th),
+                             n_samples, seed, cell, stream, out)
+    return out
 
 
 def tail_probs(mu, var, theta):
@@ -298,6 +312,18 @@ class Model:
         _check(lib().orc_pmc_cells(self._h, cells, len(cells), theta, n_samples, seed,
                                    iso_index, out), "pmc_cells")
         return out
+
+    def pmc_cells_multi(self, cells, thetas, n_samples, seed, stream=0, mask=None):
+        """NEXT-3 (R27): T x n LCP, one sample stream for all isovalues; mask[q] bit t
+        marks cell q as a leaf of isovalue t (None = all)."""
+        cells = np.ascontiguousarray(cells, np.int64)
+        th = np.ascontiguousarray(thetas, np.float64)
+        out = np.zeros(len(th) * len(cells))
+        mk = None if mask is None else np.ascontiguousarray(mask, np.uint32)
+        _check(lib().orc_pmc_cells_multi(self._h, cells, len(cells), th, len(th),
+                                         None if mk is None else mk.ctypes.data, n_samples, seed,
+                                         stream, out), "pmc_cells_multi")
+        return out.reshape(len(th), len(cells))
 
     def eval_node(self, theta, alpha, level, i, j, k):
         rec = np.zeros(1, NODE_DTYPE)

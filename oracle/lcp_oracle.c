@@ -625,6 +625,68 @@ int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double 
     return status;
 }
 
+/* ---------------------------------------------------------------- NEXT-3 --- */
+/* Fused multi-isovalue MC (the paper's isovalue sweep,
+ * PAPER.md:346, :386): ONE sample stream per cell -- the counter word 3 is the
+ * caller's `stream` index instead of a per-isovalue index (R27) -- and, for every
+ * sample, the crossing test of C11 (ties cross, R24) applied
+ * to each of the T isovalues.  counts_out[t] is therefore exactly
+ * orc_mc_count(mu, L, thetas[t], N, seed, cell, stream). */
+void orc_mc_count_multi(const double* mu, const double* L, const double* thetas, int32_t T,
+                        int64_t n_samples, uint64_t seed, int64_t cell, uint32_t stream,
+                        int64_t* counts_out) {
+    for (int32_t t = 0; t < T; ++t) counts_out[t] = 0;
+    for (int64_t s = 0; s < n_samples; ++s) {
+        double z[8], y[8];
+        orc_normals8(seed, cell, stream, s, z);
+        for (int c = 0; c < 8; ++c) {
+            y[c] = mu[c];
+            for (int e = 0; e <= c; ++e) y[c] += L[c * 8 + e] * z[e];
+        }
+        for (int32_t t = 0; t < T; ++t) {
+            int below = 1, above = 1;
+            for (int c = 0; c < 8; ++c) {
+                below = below && (y[c] < thetas[t]);
+                above = above && (y[c] > thetas[t]);
+            }
+            if (!below && !above) ++counts_out[t];
+        }
+    }
+}
+
+/* Leaf pass for T isovalues on one cell list: posterior and chol8 once per cell
+ * (they do not depend on theta), one sample stream, T counts.  mask[q] bit t
+ * (NULL = all bits) says whether cell q is a leaf of isovalue t's octree; a
+ * cleared bit gives LCP 0 (the cell was pruned for that isovalue).
+ * lcp_out is T x n, isovalue-major. */
+int orc_pmc_cells_multi(const orc_model_t* M, const int64_t* cells, int64_t n, const double* thetas,
+                        int32_t T, const uint32_t* mask, int64_t n_samples, uint64_t seed,
+                        uint32_t stream, double* lcp_out) {
+    if (n_samples < 1 || T < 1 || T > 32) return ORC_EINVAL;
+    int status = ORC_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t q = 0; q < n; ++q) {
+        double mu[8], cov[64], L[64], mup[8], covp[64];
+        int64_t cnt[32];
+        int st = orc_cell_posterior(M, cells[q], mu, cov);
+        if (st != ORC_OK) {
+#pragma omp critical
+            status = st;
+        }
+        for (int i = 0; i < 8; ++i) {
+            mup[i] = mu[PI8[i]];
+            for (int j = 0; j < 8; ++j) covp[i * 8 + j] = cov[PI8[i] * 8 + PI8[j]];
+        }
+        orc_chol8(covp, L);
+        orc_mc_count_multi(mup, L, thetas, T, n_samples, seed, cells[q], stream, cnt);
+        for (int32_t t = 0; t < T; ++t) {
+            int on = mask ? (int)((mask[q] >> t) & 1u) : 1;
+            lcp_out[(int64_t)t * n + q] = on ? (double)cnt[t] / (double)n_samples : 0.0;
+        }
+    }
+    return status;
+}
+
 /* ------------------------------------------------------------------ C6 --- */
 /* P(Y < theta) = Phi((theta - mu) / sigma) (Sigma read as sigma, R4),
  * evaluated as erfc so that both tails keep full relative precision. */

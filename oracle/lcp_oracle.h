@@ -88,6 +88,18 @@ int64_t orc_mc_count(const double* mu, const double* L, double theta, int64_t n_
 int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double theta,
                   int64_t n_samples, uint64_t seed, uint32_t iso_index, double* lcp_out);
 
+/* NEXT-3 (R27): fused multi-isovalue MC -- one sample stream (counter word 3 =
+ * stream), the C11 crossing test for each of T thetas.  counts_out[T]. */
+void orc_mc_count_multi(const double* mu, const double* L, const double* thetas, int32_t T,
+                        int64_t n_samples, uint64_t seed, int64_t cell, uint32_t stream,
+                        int64_t* counts_out);
+
+/* NEXT-3: leaf pass for T <= 32 isovalues; mask[q] bit t (NULL = all) marks cell q
+ * as a leaf of isovalue t (else LCP 0).  lcp_out[t * n + q]. */
+int orc_pmc_cells_multi(const orc_model_t* M, const int64_t* cells, int64_t n, const double* thetas,
+                        int32_t T, const uint32_t* mask, int64_t n_samples, uint64_t seed,
+                        uint32_t stream, double* lcp_out);
+
 /* C5: P(Y < theta), P(Y > theta) for Y ~ N(mu, var). */
 void orc_tail_probs(double mu, double var, double theta, double* p_lo, double* p_hi);
 
