@@ -164,6 +164,41 @@ lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, in
                            int64_t n_samples, uint64_t seed, uint32_t iso_index, float* field,
                            int32_t out_on_device, int64_t* n_leaf_out);
 
+/* NEXT-3 fused multi-isovalue leaf pass (the paper's isovalue sweep,
+ * PAPER.md:346, :386; reading R27).  For n_iso <= 16 isovalues: the 8-corner
+ * posterior and its 8x8 Cholesky once per cell, and ONE Philox sample stream
+ * per cell -- counter word 3 = `stream` (R13) -- whose every sample is tested
+ * against each isovalue (ties cross).  Row t therefore equals
+ * lcp_pmc_cells(cells, isovalues[t], ..., iso_index = stream) up to the FP32
+ * rounding of y - isovalue (R25).
+ *   cells_dev: n_cells ids; mask_dev: n_cells uint32 (bit t = cell is a leaf of
+ *   isovalue t; a cleared bit writes 0), or NULL = all bits;
+ *   lcp_dev: n_iso x n_cells floats, isovalue-major (caller-owned, device).
+ * Asynchronous on the ctx stream.  Errors: ESTATE, EINVAL (n_iso not in
+ * [1, 16], non-finite isovalue, n_samples < 1), ENUMERIC, ECUDA. */
+lcp_status_t lcp_pmc_cells_multi(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_t n_cells,
+                                 const double* isovalues, int32_t n_iso, const uint32_t* mask_dev,
+                                 int64_t n_samples, uint64_t seed, uint32_t stream, float* lcp_dev);
+
+/* NEXT-3 whole step for n_iso <= 16 isovalues: Alg. 1 per isovalue (the vertex
+ * marginal cache is shared), the union of the leaf sets in Morton order with a
+ * per-cell isovalue mask, lcp_pmc_cells_multi on the union, and one dense field
+ * per isovalue (0 off that isovalue's leaves).
+ *   fields: n_iso x nx*ny*nz floats, isovalue-major (device pointer if
+ *   out_on_device, else host, copied before return); n_leaf_out: n_iso leaf
+ *   counts (may be NULL); n_union_out: union size (may be NULL).
+ * Grids up to 2048 cells per axis.  Blocks the host.  Errors as
+ * lcp_octree_refine and lcp_pmc_cells_multi. */
+lcp_status_t lcp_run_field_multi(lcp_ctx_t* ctx, const double* isovalues, int32_t n_iso,
+                                 double threshold, int32_t max_depth, int64_t n_samples,
+                                 uint64_t seed, uint32_t stream, float* fields, int32_t out_on_device,
+                                 int64_t* n_leaf_out, int64_t* n_union_out);
+
+/* parity tap: the union leaf list (Morton order) and per-cell isovalue masks of
+ * the last lcp_run_field_multi; ctx-owned device arrays. */
+lcp_status_t lcp_union_cells(lcp_ctx_t* ctx, int64_t* n_out, const int64_t** cells_dev_out,
+                             const uint32_t** mask_dev_out);
+
 /* NEXT-4 level field: register a caller-owned device
  * array of nx*ny*nz bytes (NULL unregisters).  Every later refine writes, for
  * each cell, the octree level at which its region stopped: the level of the

@@ -146,7 +146,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
-                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.ext_z, &c.ext_v, &c.sgpr_A};
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)
@@ -258,6 +258,54 @@ lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, in
   float ms = 0;
   cudaEventElapsedTime(&ms, c.ev[4], c.ev[5]);
   c.t.scatter_ms = ms;
+  return LCP_OK;
+}
+
+lcp_status_t lcp_pmc_cells_multi(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_t n_cells, const double* isovalues,
+                                 int32_t n_iso, const uint32_t* mask_dev, int64_t n_samples, uint64_t seed,
+                                 uint32_t stream, float* lcp_dev) {
+  CTX_GUARD(ctx);
+  if (n_cells < 0 || !isovalues || (n_cells > 0 && (!cells_dev || !lcp_dev)))
+    return set_err(c, LCP_EINVAL, "pmc_multi: bad arguments");
+  return pmc_multi_impl(c, cells_dev, n_cells, isovalues, n_iso, mask_dev, n_samples, seed, stream, lcp_dev,
+                        n_cells);
+}
+
+lcp_status_t lcp_run_field_multi(lcp_ctx_t* ctx, const double* isovalues, int32_t n_iso, double threshold,
+                                 int32_t max_depth, int64_t n_samples, uint64_t seed, uint32_t stream,
+                                 float* fields, int32_t out_on_device, int64_t* n_leaf_out, int64_t* n_union_out) {
+  CTX_GUARD(ctx);
+  if (!fields || !isovalues) return set_err(c, LCP_EINVAL, "run_field_multi: null pointer");
+  if (n_iso < 1 || n_iso > 16) return set_err(c, LCP_EINVAL, "run_field_multi: need 1 <= n_iso <= 16");
+  cudaError_t e;
+  const int64_t ncell = (int64_t)c.g.cells[0] * c.g.cells[1] * c.g.cells[2];
+  float* dfields = fields;
+  if (!out_on_device) {
+    if ((e = c.field_tmp.ensure(sizeof(float) * ncell * n_iso)) != cudaSuccess) return cuda_err(c, e, "alloc");
+    dfields = c.field_tmp.as<float>();
+  }
+  lcp_status_t st = run_field_multi_impl(c, isovalues, n_iso, threshold, max_depth, n_samples, seed, stream,
+                                         dfields, n_leaf_out, n_union_out);
+  if (st != LCP_OK) return st;
+  if (!out_on_device) {
+    if ((e = cudaMemcpyAsync(fields, dfields, sizeof(float) * ncell * n_iso, cudaMemcpyDeviceToHost, c.stream)) !=
+        cudaSuccess)
+      return cuda_err(c, e, "copy fields");
+  }
+  if ((e = cudaStreamSynchronize(c.stream)) != cudaSuccess) return cuda_err(c, e, "sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c.ev[4], c.ev[5]);
+  c.t.scatter_ms = ms;
+  return check_device_errors(c);
+}
+
+lcp_status_t lcp_union_cells(lcp_ctx_t* ctx, int64_t* n_out, const int64_t** cells_dev_out,
+                             const uint32_t** mask_dev_out) {
+  CTX_GUARD(ctx);
+  if (!n_out || !cells_dev_out || !mask_dev_out) return set_err(c, LCP_EINVAL, "union_cells: null output");
+  *n_out = c.n_union;
+  *cells_dev_out = c.union_cells.as<int64_t>();
+  *mask_dev_out = c.union_mask.as<uint32_t>();
   return LCP_OK;
 }
 

@@ -114,6 +114,9 @@ struct Ctx {
   // leaf pass scratch
   DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
   DevBuf brick_flag, brick_idx, brick_start;
+  DevBuf cellmask;               // NEXT-3: uint16 per cell, bit t = leaf of isovalue t
+  DevBuf union_cells, union_mask; // NEXT-3: union leaf list (Morton order) and its masks
+  int64_t n_union = 0;
   DevBuf pmc_counters;           // [0]: samples finished in phase 2 of k_pmc
   int64_t last_pmc_phase2 = 0;
   int64_t last_brick_runs = 0;   // brick runs of the last posterior (0: per-cell path)
@@ -139,6 +142,12 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* y, int64_t m, int
 lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth);
 lcp_status_t pmc_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double theta, int64_t N,
                       uint64_t seed, uint32_t iso, float* out_dev);
+lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells_dev, int64_t n, const double* thetas, int T,
+                            const uint32_t* mask_dev, int64_t N, uint64_t seed, uint32_t stream, float* out_dev,
+                            int64_t stride);
+lcp_status_t run_field_multi_impl(Ctx& c, const double* thetas, int T, double alpha, int max_depth, int64_t N,
+                                  uint64_t seed, uint32_t stream, float* fields_dev, int64_t* n_leaf_out,
+                                  int64_t* n_union_out);
 lcp_status_t posterior_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double* post_dev);
 lcp_status_t point_marginals_impl(Ctx& c, const double* xyz_dev, int64_t n, const int32_t* bkt,
                                   double* mu_dev, double* var_dev);

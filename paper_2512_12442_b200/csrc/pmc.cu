@@ -9,6 +9,7 @@
 //                (R5, R24).  LCP = count / N.
 //  a9  k_scatter : dense field, zero off the leaves.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -156,26 +157,39 @@ constexpr float ZMAX = 5.7684f;
 constexpr int PMC_WARPS = 8;
 constexpr int QCAP = 64;            // pending samples per warp
 
-// k_pmc: exact two-phase evaluation of the PMC count.
+// k_pmc<T>: exact two-phase evaluation of the PMC count for
+// T isovalues at once (T = 1: the single-isovalue pass; T > 1: NEXT-3, R27).
+// Corner values are taken relative to the first isovalue, m_c = mu_c - th_0
+// (FP64 difference rounded once); isovalue t is the offset dl_t = th_t - th_0
+// (dl_0 = 0), and a sample crosses t iff min_c y_c <= dl_t <= max_c y_c.
 // Phase 1 draws the first Philox block (normals z0..z3) of sample s and forms
 // y_c exactly for the first four corners and y_c - R_c for the other four,
 // where |R_c| = |sum_{d>=4} L_cd z_d| <= B_c = ZMAX sum_{d>=4} |L_cd| (+ rounding
-// slack).  If the bounds already fix the outcome (all below / all above / one
-// surely >= 0 and one surely <= 0) the sample is counted; otherwise it is queued
-// in shared memory and, 32 at a time, phase 2 draws the second Philox block
-// (z4..z7) and finishes the sample.  Every sample is decided exactly as the
-// one-pass FP32 evaluation decides it; the count is the same estimator.
+// slack).  That brackets max_c y_c in [LMX, UMX] and min_c y_c in [LMN, UMN].
+// If for every isovalue the bounds fix the outcome (dl > UMX or dl < LMN: no
+// crossing; UMN <= dl <= LMX: crossing) the sample is counted; otherwise it is
+// queued in shared memory and, 32 at a time, phase 2 draws the second Philox
+// block (z4..z7), finishes the sample and counts every isovalue exactly.  Every
+// sample is decided exactly as the one-pass FP32 evaluation decides it; the
+// count is the same estimator.
 #ifndef PMC_MINBLOCKS
 #define PMC_MINBLOCKS 2
 #endif
 #ifndef PMC_ILP
 #define PMC_ILP 2
 #endif
-__global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int64_t* __restrict__ cells,
-                                                        const double* __restrict__ post, int64_t n, double theta,
-                                                        uint32_t N, const PhiloxKeys K, uint32_t iso,
-                                                        float* __restrict__ out,
-                                                        unsigned long long* __restrict__ n_phase2) {
+constexpr int MAX_ISO = 16;
+struct IsoOffsets {
+  float dl[MAX_ISO];   // th_t - th_0 (padding: +inf, never crosses)
+  int n_out;           // isovalues written (T is padded up to an instantiated size)
+};
+
+template <int T>
+__global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
+    k_pmc(const int64_t* __restrict__ cells, const double* __restrict__ post, int64_t n, double theta,
+          const IsoOffsets D, uint32_t N, const PhiloxKeys K, uint32_t iso, const uint32_t* __restrict__ mask,
+          int64_t out_stride, float* __restrict__ out, unsigned long long* __restrict__ n_phase2) {
+  constexpr int ILP = (T <= 4) ? PMC_ILP : 1;
   __shared__ float sq_y[PMC_WARPS][6][QCAP];   // yp4..yp7, max(y0..y3), min(y0..y3)
   __shared__ uint32_t sq_s[PMC_WARPS][QCAP];
   __shared__ unsigned int s_p2;
@@ -217,8 +231,12 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int
 #pragma unroll
     for (int c = 0; c < 4; ++c) B[c] = 0.0f;
   }
+  // isovalue offsets: literal 0 for the first (single-isovalue code = T == 1)
+  auto dl = [&](int t) -> float { return t == 0 ? 0.0f : D.dl[t]; };
   const uint32_t Nl = live ? N : 0u;
-  uint32_t cnt = 0;
+  uint32_t cnt[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) cnt[t] = 0;
   int qn = 0;   // warp-uniform queue length
   unsigned p2 = 0;
   float* qy = &sq_y[wid][0][0];
@@ -249,9 +267,18 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int
       lo_max = fmaxf(lo_max, lo);
       hi_min = fminf(hi_min, hi);
     }
-    const bool cross = lo_max >= 0.0f && hi_min <= 0.0f;
-    const bool decided = hi_max < 0.0f || lo_min > 0.0f || cross;
-    cnt += cross ? 1u : 0u;
+    bool decided = true;
+    bool cross[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const float d = dl(t);
+      cross[t] = lo_max >= d && hi_min <= d;
+      decided = decided && (hi_max < d || lo_min > d || cross[t]);
+    }
+    if (decided) {
+#pragma unroll
+      for (int t = 0; t < T; ++t) cnt[t] += cross[t] ? 1u : 0u;
+    }
     yq[0] = yp[4]; yq[1] = yp[5]; yq[2] = yp[6]; yq[3] = yp[7]; yq[4] = mx03; yq[5] = mn03;
     return !decided;
   };
@@ -282,7 +309,8 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int
         mx = fmaxf(mx, y);
         mn = fminf(mn, y);
       }
-      cnt += (mx >= 0.0f && mn <= 0.0f) ? 1u : 0u;
+#pragma unroll
+      for (int t = 0; t < T; ++t) cnt[t] += (mx >= dl(t) && mn <= dl(t)) ? 1u : 0u;
     }
   };
   auto drain = [&]() {
@@ -296,7 +324,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int
   };
   uint32_t base = 0;
   // two samples per lane per iteration (instruction-level parallelism)
-  for (; PMC_ILP == 2 && base + 64u <= Nl; base += 64u) {
+  for (; ILP == 2 && base + 64u <= Nl; base += 64u) {
     float ya[6], yb[6];
     const bool pa = phase1(base + lane, ya);
     const bool pb = phase1(base + 32u + lane, yb);
@@ -318,11 +346,13 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS) k_pmc(const int
     phase2(lane, lane < qn);
     p2 += qn;
   }
-  cnt = warp_sum(cnt);
-  if (live && lane == 0) {
-    out[q] = (float)((double)cnt / (double)N);
-    atomicAdd(&s_p2, p2);
+  const uint32_t mk = (live && mask) ? mask[q] : 0xffffffffu;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const uint32_t ct = warp_sum(cnt[t]);
+    if (live && lane == 0 && t < D.n_out) out[t * out_stride + q] = ((mk >> t) & 1u) ? (float)((double)ct / (double)N) : 0.0f;
   }
+  if (live && lane == 0) atomicAdd(&s_p2, p2);
   __syncthreads();
   if (threadIdx.x == 0 && s_p2) atomicAdd(n_phase2, (unsigned long long)s_p2);
 }
@@ -381,11 +411,24 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
   return LCP_OK;
 }
 
-lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int64_t N, uint64_t seed,
-                      uint32_t iso, float* out) {
+template <int T>
+static void launch_pmc(Ctx& c, unsigned grid, const int64_t* cells, const double* post, int64_t n, double theta,
+                       const IsoOffsets& D, uint32_t N, const PhiloxKeys& keys, uint32_t iso, const uint32_t* mask,
+                       int64_t stride, float* out) {
+  k_pmc<T><<<grid, PMC_WARPS * 32, 0, c.stream>>>(cells, post, n, theta, D, N, keys, iso, mask, stride, out,
+                                                  c.pmc_counters.as<unsigned long long>());
+}
+
+// leaf pass for T isovalues (T = 1: lcp_pmc_cells; T > 1: NEXT-3).  out[t * stride + q].
+lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const double* thetas, int T,
+                            const uint32_t* mask, int64_t N, uint64_t seed, uint32_t iso, float* out,
+                            int64_t stride) {
   if (!c.fitted) return set_err(c, LCP_ESTATE, "pmc before fit");
   if (N < 1 || N > ((int64_t)1 << 31)) return set_err(c, LCP_EINVAL, "pmc: need 1 <= n_samples <= 2^31");
   if (n < 0) return set_err(c, LCP_EINVAL, "pmc: negative cell count");
+  if (T < 1 || T > MAX_ISO) return set_err(c, LCP_EINVAL, "pmc: need 1 <= n_iso <= 16");
+  for (int t = 0; t < T; ++t)
+    if (!std::isfinite(thetas[t])) return set_err(c, LCP_EINVAL, "pmc: isovalue not finite");
   if (n == 0) return LCP_OK;
   cudaError_t e;
 #define CK(x)                                        \
@@ -408,6 +451,10 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
     keys.k[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
     keys.k[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
   }
+  IsoOffsets D;
+  for (int t = 0; t < MAX_ISO; ++t) D.dl[t] = t < T ? (float)(thetas[t] - thetas[0]) : INFINITY;
+  D.n_out = T;
+  const int Tp = T <= 4 ? T : (T <= 6 ? 6 : (T <= 8 ? 8 : (T <= 12 ? 12 : 16)));
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     int64_t nn = std::min(chunk, n - s0);
     cudaEventRecord(c.ev[0], c.stream);
@@ -417,8 +464,14 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
     k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(post, nn);
     ++c.n_launch;
     cudaEventRecord(c.ev[2], c.stream);
-    k_pmc<<<(unsigned)((nn + PMC_WARPS - 1) / PMC_WARPS), PMC_WARPS * 32, 0, c.stream>>>(
-        cells + s0, post, nn, theta, (uint32_t)N, keys, iso, out + s0, c.pmc_counters.as<unsigned long long>());
+    const unsigned gr = (unsigned)((nn + PMC_WARPS - 1) / PMC_WARPS);
+    const uint32_t* mk = mask ? mask + s0 : nullptr;
+    switch (Tp) {
+#define LP(TT) \
+  case TT: launch_pmc<TT>(c, gr, cells + s0, post, nn, thetas[0], D, (uint32_t)N, keys, iso, mk, stride, out + s0); break
+      LP(1); LP(2); LP(3); LP(4); LP(6); LP(8); LP(12); LP(16);
+#undef LP
+    }
     ++c.n_launch;
     cudaEventRecord(c.ev[3], c.stream);
     CK(cudaGetLastError());
@@ -437,6 +490,11 @@ lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int
   CK(cudaMemcpy(&c.last_pmc_phase2, c.pmc_counters.p, sizeof(int64_t), cudaMemcpyDeviceToHost));
 #undef CK
   return check_device_errors(c);
+}
+
+lcp_status_t pmc_impl(Ctx& c, const int64_t* cells, int64_t n, double theta, int64_t N, uint64_t seed,
+                      uint32_t iso, float* out) {
+  return pmc_multi_impl(c, cells, n, &theta, 1, nullptr, N, seed, iso, out, n);
 }
 
 cudaError_t launch_scatter(Ctx& c, const int64_t* cells, const float* lcp, int64_t n, float* field) {

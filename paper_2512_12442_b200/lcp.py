@@ -27,7 +27,8 @@ FP64, FP32 = 0, 1
 EXPORTS = ["lcp_create", "lcp_destroy", "lcp_last_error", "lcp_fit_local", "lcp_octree_refine",
            "lcp_pmc_cells", "lcp_scatter_field", "lcp_run_field", "lcp_node_records",
            "lcp_cell_posterior", "lcp_point_marginals", "lcp_bucket_sets", "lcp_get_info",
-           "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field", "lcp_fit_sgpr"]
+           "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field", "lcp_fit_sgpr",
+           "lcp_pmc_cells_multi", "lcp_run_field_multi", "lcp_union_cells"]
 
 
 class LcpError(RuntimeError):
@@ -94,6 +95,9 @@ def load_library() -> C.CDLL:
     L.lcp_set_level_field.argtypes = [P, P]
     L.lcp_fit_sgpr.argtypes = [P, P, P, P, i64, i32, C.POINTER(KernelT), i32, C.POINTER(GridT),
                                C.POINTER(OptsT)]
+    L.lcp_pmc_cells_multi.argtypes = [P, P, i64, P, i32, P, i64, u64, u32, P]
+    L.lcp_run_field_multi.argtypes = [P, P, i32, dbl, i32, i64, u64, u32, P, i32, P, C.POINTER(i64)]
+    L.lcp_union_cells.argtypes = [P, C.POINTER(i64), C.POINTER(P), C.POINTER(P)]
     for name in EXPORTS:
         if name not in ("lcp_destroy", "lcp_last_error"):
             getattr(L, name).restype = C.c_int
@@ -257,6 +261,50 @@ class Context:
                                    _is_dev(field), C.byref(n))
         self._check(st, "lcp_run_field")
         return field, n.value
+
+    # -- NEXT-3: fused multi-isovalue leaf pass
+    def pmc_cells_multi(self, cells, isovalues: Sequence[float], n_samples: int, seed: int, stream: int = 0,
+                        mask=None, out=None):
+        """(T, n) float32 CUDA tensor: one sample stream per cell, every isovalue tested.
+        cells: int64 CUDA tensor; mask: uint32-valued CUDA tensor (int32 storage) or None."""
+        torch = self._torch
+        th = np.ascontiguousarray(isovalues, np.float64)
+        n = len(cells)
+        if out is None:
+            out = torch.empty((len(th), n), dtype=torch.float32, device=cells.device)
+        st = self._L.lcp_pmc_cells_multi(self._h, C.c_void_p(_ptr(cells)), n, C.c_void_p(th.ctypes.data),
+                                         len(th), C.c_void_p(_ptr(mask)), int(n_samples), int(seed),
+                                         int(stream), C.c_void_p(_ptr(out)))
+        self._check(st, "lcp_pmc_cells_multi")
+        return out
+
+    def run_field_multi(self, isovalues: Sequence[float], threshold, max_depth, n_samples, seed, stream=0,
+                        fields=None):
+        """Returns (fields (T, nx*ny*nz) float32, leaf counts per isovalue, union size)."""
+        torch = self._torch
+        th = np.ascontiguousarray(isovalues, np.float64)
+        if fields is None:
+            nx, ny, nz = self.grid[2]
+            fields = torch.empty((len(th), nx * ny * nz), dtype=torch.float32, device=f"cuda:{self.device}")
+        nl = np.zeros(len(th), np.int64)
+        nu = C.c_int64()
+        st = self._L.lcp_run_field_multi(self._h, C.c_void_p(th.ctypes.data), len(th), float(threshold),
+                                         int(max_depth), int(n_samples), int(seed), int(stream),
+                                         C.c_void_p(_ptr(fields)), _is_dev(fields), C.c_void_p(nl.ctypes.data),
+                                         C.byref(nu))
+        self._check(st, "lcp_run_field_multi")
+        return fields, nl, nu.value
+
+    def union_cells(self):
+        """(cells int64, mask int64) of the last run_field_multi (copies)."""
+        n = C.c_int64()
+        pc, pm = C.c_void_p(), C.c_void_p()
+        self._check(self._L.lcp_union_cells(self._h, C.byref(n), C.byref(pc), C.byref(pm)), "lcp_union_cells")
+        cells = self._wrap_dev(pc.value, n.value, self._torch.int64)
+        raw = self._wrap_dev(pm.value, 4 * n.value, self._torch.uint8)
+        mask = raw.view(self._torch.int32).to(self._torch.int64) & 0xFFFFFFFF if n.value else raw.to(
+            self._torch.int64)
+        return cells, mask
 
     def set_level_field(self, level=None):
         """NEXT-4: register a torch uint8 CUDA tensor (nx*ny*nz) that every later

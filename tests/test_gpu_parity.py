@@ -422,3 +422,96 @@ def test_sgpr_parity(name, dev):
     lcp_o = M.pmc_cells(leaves.cpu().numpy()[sel], th, 1000, cfg.mc_seed)
     frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1000)
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+# ------------------------------------------------------------------ NEXT-3
+def _morton(cells, nx, ny):
+    def spread(v):
+        out = np.zeros_like(v)
+        for b in range(21):
+            out |= ((v >> b) & 1) << (3 * b)
+        return out
+    x = cells % nx
+    y = (cells // nx) % ny
+    z = cells // (nx * ny)
+    return spread(x) | (spread(y) << 1) | (spread(z) << 2)
+
+
+@pytest.mark.parametrize("name,thetas", [("t1", None), ("t2", [-0.3, 0.0, 0.2, 0.45, 0.9]),
+                                         ("c2", [-0.2, 0.1, 0.3]),
+                                         ("c1", list(np.linspace(-1.0, 1.0, 9)))])
+def test_multi_iso_run_field(name, thetas, dev):
+    # NEXT-3 (R27): per-isovalue octree leaf sets, their union in Morton order with
+    # the isovalue masks, and the fused one-stream leaf pass, against the oracle.
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    if thetas is None:
+        thetas = [w.thetas[0] - 0.25, w.thetas[0], w.thetas[0] + 0.3]
+    T = len(thetas)
+    N, seed, stream = min(cfg.n_samples, 2000), cfg.mc_seed, 7
+    fields, nl, nu = ctx.run_field_multi(thetas, cfg.alpha, cfg.max_depth, N, seed, stream)
+    cells_g, mask_g = ctx.union_cells()
+    cells_g, mask_g = cells_g.cpu().numpy(), mask_g.cpu().numpy()
+    assert len(cells_g) == nu
+    key = _morton(cells_g, cfg.cells[0], cfg.cells[1])
+    assert np.all(np.diff(key) > 0), "union not in Morton order"
+    want_mask = {}
+    for t, th in enumerate(thetas):
+        leaves_g = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy()
+        assert len(leaves_g) == nl[t]
+        on = cells_g[(mask_g >> t) & 1 == 1]
+        np.testing.assert_array_equal(np.sort(on), np.sort(leaves_g))
+        _, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+        np.testing.assert_array_equal(np.sort(leaves_g), leaves_o)
+        for c in leaves_o:
+            want_mask[int(c)] = want_mask.get(int(c), 0) | (1 << t)
+    assert sorted(want_mask) == sorted(cells_g.tolist())
+    sel = np.arange(len(cells_g)) if len(cells_g) <= 3000 else np.linspace(0, len(cells_g) - 1, 3000).astype(int)
+    lcp_o = M.pmc_cells_multi(cells_g[sel], thetas, N, seed, stream, mask=mask_g[sel].astype(np.uint32))
+    F = fields.cpu().numpy()
+    for t in range(T):
+        got = F[t][cells_g[sel]]
+        frac, mean, mx = lcp_parity(got, lcp_o[t], N)
+        assert frac >= 0.999 and mean <= 1e-4, (t, frac, mean, mx)
+        off = np.ones(F.shape[1], bool)
+        off[cells_g[(mask_g >> t) & 1 == 1]] = False
+        assert np.all(F[t][off] == 0)
+
+
+def test_multi_iso_first_row_is_single_pass(dev):
+    # row 0 of the fused pass is bit-identical to lcp_pmc_cells with iso_index = stream;
+    # the other rows agree with their single passes within the FP32 rounding of y - theta (R25)
+    w, ctx, _ = _ctx("c2", dev, keep_records=False)
+    cfg = w.cfg
+    cells = torch.from_numpy(random_cells("c2", 20000, 4)).to(dev)
+    th = [0.1, -0.15, 0.35, 0.6]
+    N = 1500
+    multi = ctx.pmc_cells_multi(cells, th, N, 11, stream=3)
+    for t, tv in enumerate(th):
+        single = ctx.pmc_cells(cells, tv, N, 11, 3)
+        if t == 0:
+            assert torch.equal(multi[0], single)
+        else:
+            frac, mean, mx = lcp_parity(multi[t].cpu().numpy(), single.cpu().numpy(), N)
+            assert frac >= 0.999 and mean <= 1e-5, (t, frac, mean, mx)
+
+
+def test_multi_iso_c4_full_size_sampled(dev):
+    # BASELINE c4 (three isovalues) at full size through the fused path: sampled
+    # union cells against the oracle's one-stream multi-isovalue MC.
+    w, ctx, M = _ctx("c4", dev, keep_records=False)
+    cfg = w.cfg
+    thetas = list(w.thetas)
+    fields, nl, nu = ctx.run_field_multi(thetas, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, 0)
+    cells_g, mask_g = ctx.union_cells()
+    cells_g, mask_g = cells_g.cpu().numpy(), mask_g.cpu().numpy()
+    assert nu == len(cells_g) and nu >= max(nl)
+    for t in range(len(thetas)):
+        assert int(((mask_g >> t) & 1).sum()) == nl[t]
+    sel = np.random.default_rng(3).choice(nu, 64, replace=False)
+    lcp_o = M.pmc_cells_multi(cells_g[sel], thetas, cfg.n_samples, cfg.mc_seed, 0,
+                              mask=mask_g[sel].astype(np.uint32))
+    F = fields.cpu().numpy()
+    for t in range(len(thetas)):
+        frac, mean, mx = lcp_parity(F[t][cells_g[sel]], lcp_o[t], cfg.n_samples)
+        assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
