@@ -17,6 +17,9 @@
 
 namespace lcp {
 
+// The constant -sqrt(2 ln 2) of Box-Muller's R = sqrt(-2 ln 2 lg2(u_a)) (and its sign)
+// is carried by L' (k_chol8 stores FOLD_SCALE L'), so k_pmc draws z / FOLD_SCALE.
+constexpr double FOLD_SCALE = -1.1774100225154747;
 constexpr int64_t PMC_CHUNK = (int64_t)1 << 23;   // cells per posterior/MC chunk (2.9 GB of records)
 
 __global__ void k_cell_bucket(Geom g, const int64_t* __restrict__ cells, int64_t n, int32_t* __restrict__ bkt,
@@ -94,7 +97,7 @@ __global__ void k_chol8(double* __restrict__ post, int64_t n) {
   for (int i = 0; i < 8; ++i) rec[i] = mu[i];
   float* Lf = reinterpret_cast<float*>(rec + 8);
 #pragma unroll
-  for (int p = 0; p < 36; ++p) Lf[p] = (float)L[p];
+  for (int p = 0; p < 36; ++p) Lf[p] = (float)(FOLD_SCALE * L[p]);
 }
 
 // Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9, passed as a kernel
@@ -137,18 +140,51 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
-// Box-Muller: (R cos 2 pi ub, R sin 2 pi ub), R = sqrt(-2 ln ua).  The angle
-// is taken in (-pi, pi) as 2 pi (ub - 1/2), which flips both signs; with
-// F = 1 + (r mod 2^23) 2^-23 it is one FFMA: 2 pi F - 2 pi (3/2 - 2^-24).
+// Box-Muller (R13) with the scale folded into L': returns (z0, z1) / FOLD_SCALE =
+// (r cos 2 pi ub, r sin 2 pi ub), r = sqrt(-lg2 ua) = R / sqrt(2 ln 2).  The angle
+// is taken in (-pi, pi) as 2 pi (ub - 1/2), which flips both signs (absorbed by
+// FOLD_SCALE < 0); with F = 1 + (r mod 2^23) 2^-23 it is one FFMA:
+// 2 pi F - 2 pi (3/2 - 2^-24).
 __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, float& z1) {
   float ua = u23(ra);
   float fb = __uint_as_float(0x3f800000u | (rb & 0x7fffffu));
-  float r2 = fmaxf(-1.3862943611198906f * lg2_approx(ua), 0.0f);
-  float nR = -sqrt_approx(r2);
+  float r = sqrt_approx(fmaxf(-lg2_approx(ua), 0.0f));
   float s, co;
   __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
-  z0 = nR * co;
-  z1 = nR * s;
+  z0 = r * co;
+  z1 = r * s;
+}
+
+// Packed FP32x2 arithmetic (sm_100a FFMA2 / FMUL2): two lanes of FP32 per
+// instruction, each rounded exactly as the scalar fmaf / multiply; a pair built
+// from one scalar twice is issued as a broadcast operand.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(f2_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2_t ffma2(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2_t fmul2(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// box_muller with the two products r cos, r sin in one FMUL2: returns pk(z0, z1)
+__device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb) {
+  float ua = u23(ra);
+  float fb = __uint_as_float(0x3f800000u | (rb & 0x7fffffu));
+  float r = sqrt_approx(fmaxf(-lg2_approx(ua), 0.0f));
+  float s, co;
+  __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
+  return fmul2(pk(co, s), pk(r, r));
 }
 
 // Largest |z| Box-Muller can produce: u_a >= 2^-24 gives R <= sqrt(48 ln 2) = 5.7668;
@@ -156,6 +192,7 @@ __device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, 
 constexpr float ZMAX = 5.7684f;
 constexpr int PMC_WARPS = 8;
 constexpr int QCAP = 64;            // pending samples per warp
+constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are branch-free
 
 // k_pmc<T>: exact two-phase evaluation of the PMC count for
 // T isovalues at once (T = 1: the single-isovalue pass; T > 1: NEXT-3, R27).
@@ -190,20 +227,23 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
           const IsoOffsets D, uint32_t N, const PhiloxKeys K, uint32_t iso, const uint32_t* __restrict__ mask,
           int64_t out_stride, float* __restrict__ out, unsigned long long* __restrict__ n_phase2) {
   constexpr int ILP = (T <= 4) ? PMC_ILP : 1;
-  __shared__ float sq_y[PMC_WARPS][6][QCAP];   // yp4..yp7, max(y0..y3), min(y0..y3)
-  __shared__ uint32_t sq_s[PMC_WARPS][QCAP];
+  // queue, slot-major: (lo4..lo7), (max y0..3, min y0..3, s, -)
+  __shared__ float4 sq[PMC_WARPS][QROWS][2];
   __shared__ unsigned int s_p2;
   if (threadIdx.x == 0) s_p2 = 0;
   __syncthreads();
   const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool live = q < n;
-  float m[8], L[36], B[4];
+  // m[c] = mu_c - th_0 (c < 4); mB[c] = mu_c - th_0 - B_c for the last four corners
+  float m[4], mB[4], L[36], B[4];
   uint32_t c1 = 0, c2 = 0;
+  constexpr float ZB = (float)(ZMAX / 1.1774100225154747);   // bound on |z / FOLD_SCALE|
   if (live) {
     const double* rec = post + 44 * q;
+    float mm[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) m[c] = (float)(rec[c] - theta);
+    for (int c = 0; c < 8; ++c) mm[c] = (float)(rec[c] - theta);
     const float4* L4 = reinterpret_cast<const float4*>(rec + 8);
 #pragma unroll
     for (int t = 0; t < 9; ++t) {
@@ -214,22 +254,25 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     c1 = (uint32_t)(uint64_t)cell;
     c2 = (uint32_t)((uint64_t)cell >> 32);
 #pragma unroll
+    for (int c = 0; c < 4; ++c) m[c] = mm[c];
+#pragma unroll
     for (int c = 4; c < 8; ++c) {
-      float tail = 0.0f, all = fabsf(m[c]);
+      float tail = 0.0f, all = fabsf(mm[c]);
 #pragma unroll
       for (int d = 0; d <= c; ++d) {
-        all += ZMAX * fabsf(L[c * (c + 1) / 2 + d]);
+        all += ZB * fabsf(L[c * (c + 1) / 2 + d]);
         if (d >= 4) tail += fabsf(L[c * (c + 1) / 2 + d]);
       }
-      B[c - 4] = ZMAX * tail * (1.0f + 1e-5f) + 1e-6f * all;
+      // |sum_{d>=4} L'_cd z_d| <= ZB tail; the slack covers the FP32 rounding of the
+      // partial sums, so phase-1 decisions equal the one-pass FP32 decisions
+      B[c - 4] = ZB * tail * (1.0f + 1e-5f) + 1e-6f * all;
+      mB[c - 4] = mm[c] - B[c - 4];
     }
   } else {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) m[c] = 0.0f;
+    for (int c = 0; c < 4; ++c) m[c] = mB[c] = B[c] = 0.0f;
 #pragma unroll
     for (int p = 0; p < 36; ++p) L[p] = 0.0f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) B[c] = 0.0f;
   }
   // isovalue offsets: literal 0 for the first (single-isovalue code = T == 1)
   auto dl = [&](int t) -> float { return t == 0 ? 0.0f : D.dl[t]; };
@@ -239,34 +282,54 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   for (int t = 0; t < T; ++t) cnt[t] = 0;
   int qn = 0;   // warp-uniform queue length
   unsigned p2 = 0;
-  float* qy = &sq_y[wid][0][0];
-  uint32_t* qs = sq_s[wid];
-  // phase 1 of sample s: returns true (and the stash) if the sample is undecided
-  auto phase1 = [&](uint32_t s, float (&yq)[6]) -> bool {
+  float4* qv = &sq[wid][0][0];
+  // L' as FFMA2 operands: corner pairs (0,1) (2,3) (4,5) (6,7) per normal d
+  f2_t P01 = pk(L[0], L[1]), P23[3], P45[4], P67[4];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) P23[d] = pk(L[3 + d], L[6 + d]);
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    P45[d] = pk(L[10 + d], L[15 + d]);
+    P67[d] = pk(L[21 + d], L[28 + d]);
+  }
+  const float L11 = L[2], L33 = L[9];
+  const f2_t M01 = pk(m[0], m[1]), M23 = pk(m[2], m[3]), MB45 = pk(mB[0], mB[1]), MB67 = pk(mB[2], mB[3]);
+  const f2_t B45 = pk(B[0], B[1]), B67 = pk(B[2], B[3]), TWO = pk(2.0f, 2.0f);
+  // phase 1 of sample s: returns true (and the stash) if the sample is undecided.
+  // y_c for c < 4 exactly; lo_c = y_c - B_c - R_c and hi_c = lo_c + 2 B_c for c >= 4.
+  // Same FP32 operations in the same order as the scalar chains y = fma(L'_cd, z_d, y).
+  auto phase1 = [&](uint32_t s, float4& st0, float4& st1) -> bool {
     uint32_t r0, r1, r2, r3;
     philox4x32_10(2u * s, c1, c2, iso, K, r0, r1, r2, r3);
+    const f2_t zA = box_muller2(r0, r1), zB = box_muller2(r2, r3);
     float z[4];
-    box_muller(r0, r1, z[0], z[1]);
-    box_muller(r2, r3, z[2], z[3]);
-    float yp[8];
+    upk(zA, z[0], z[1]);
+    upk(zB, z[2], z[3]);
+    f2_t A01 = ffma2(P01, pk(z[0], z[0]), M01);
+    f2_t A23 = M23, A45 = MB45, A67 = MB67;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      float y = m[c];
-#pragma unroll
-      for (int d = 0; d < 4 && d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
-      yp[c] = y;
+    for (int d = 0; d < 4; ++d) {
+      const f2_t zd = pk(z[d], z[d]);
+      if (d < 3) A23 = ffma2(P23[d], zd, A23);
+      A45 = ffma2(P45[d], zd, A45);
+      A67 = ffma2(P67[d], zd, A67);
     }
-    const float mx03 = fmaxf(fmaxf(yp[0], yp[1]), fmaxf(yp[2], yp[3]));
-    const float mn03 = fminf(fminf(yp[0], yp[1]), fminf(yp[2], yp[3]));
-    float hi_max = mx03, lo_min = mn03, lo_max = mx03, hi_min = mn03;
-#pragma unroll
-    for (int c = 4; c < 8; ++c) {
-      const float lo = yp[c] - B[c - 4], hi = yp[c] + B[c - 4];
-      hi_max = fmaxf(hi_max, hi);
-      lo_min = fminf(lo_min, lo);
-      lo_max = fmaxf(lo_max, lo);
-      hi_min = fminf(hi_min, hi);
-    }
+    float y[4], lo[4], hi[4];
+    upk(A01, y[0], y[1]);
+    upk(A23, y[2], y[3]);
+    y[1] = fmaf(L11, z[1], y[1]);
+    y[3] = fmaf(L33, z[3], y[3]);
+    upk(A45, lo[0], lo[1]);
+    upk(A67, lo[2], lo[3]);
+    upk(ffma2(TWO, B45, A45), hi[0], hi[1]);
+    upk(ffma2(TWO, B67, A67), hi[2], hi[3]);
+    // 3-input chains (FMNMX3)
+    const float mx03 = fmaxf(fmaxf(fmaxf(y[0], y[1]), y[2]), y[3]);
+    const float mn03 = fminf(fminf(fminf(y[0], y[1]), y[2]), y[3]);
+    const float hi_max = fmaxf(fmaxf(fmaxf(fmaxf(mx03, hi[0]), hi[1]), hi[2]), hi[3]);
+    const float hi_min = fminf(fminf(fminf(fminf(mn03, hi[0]), hi[1]), hi[2]), hi[3]);
+    const float lo_max = fmaxf(fmaxf(fmaxf(fmaxf(mx03, lo[0]), lo[1]), lo[2]), lo[3]);
+    const float lo_min = fminf(fminf(fminf(fminf(mn03, lo[0]), lo[1]), lo[2]), lo[3]);
     bool decided = true;
     bool cross[T];
 #pragma unroll
@@ -279,35 +342,46 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
 #pragma unroll
       for (int t = 0; t < T; ++t) cnt[t] += cross[t] ? 1u : 0u;
     }
-    yq[0] = yp[4]; yq[1] = yp[5]; yq[2] = yp[6]; yq[3] = yp[7]; yq[4] = mx03; yq[5] = mn03;
+    st0 = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    st1 = make_float4(mx03, mn03, __uint_as_float(s), 0.0f);
     return !decided;
   };
-  auto push = [&](bool pend, uint32_t s, const float (&yq)[6]) {
+  // phase-2 operands: columns 4..7 of corners 4..7
+  const f2_t Q45[1] = {pk(L[14], L[19])};
+  const f2_t Q67[3] = {pk(L[25], L[32]), pk(L[26], L[33]), pk(L[27], L[34])};
+  const float L55 = L[20], L77 = L[35];
+  // branch-free enqueue: pending lanes take consecutive slots, the others their trash row
+  auto push = [&](bool pend, const float4& st0, const float4& st1) {
     const unsigned pm = __ballot_sync(0xffffffffu, pend);
-    if (pend) {
-      const int slot = qn + __popc(pm & ((1u << lane) - 1u));
-      qs[slot] = s;
-#pragma unroll
-      for (int t = 0; t < 6; ++t) qy[t * QCAP + slot] = yq[t];
-    }
+    const int slot = pend ? qn + __popc(pm & ((1u << lane) - 1u)) : QCAP + lane;
+    qv[2 * slot] = st0;
+    qv[2 * slot + 1] = st1;
     qn += __popc(pm);
   };
   auto phase2 = [&](int slot, bool act) {
     if (act) {
-      uint32_t s = qs[slot];
+      const float4 va = qv[2 * slot], vb = qv[2 * slot + 1];
+      const uint32_t s = __float_as_uint(vb.z);
       uint32_t r4, r5, r6, r7;
       philox4x32_10(2u * s + 1u, c1, c2, iso, K, r4, r5, r6, r7);
       float z[8];
-      box_muller(r4, r5, z[4], z[5]);
-      box_muller(r6, r7, z[6], z[7]);
-      float mx = qy[4 * QCAP + slot], mn = qy[5 * QCAP + slot];
+      upk(box_muller2(r4, r5), z[4], z[5]);
+      upk(box_muller2(r6, r7), z[6], z[7]);
+      float mx = vb.x, mn = vb.y;
+      // y_c = (lo_c + B_c) + sum_{d>=4} L'_cd z_d, pairs (4,5) and (6,7)
+      f2_t Y45 = ffma2(Q45[0], pk(z[4], z[4]), pk(va.x + B[0], va.y + B[1]));
+      f2_t Y67 = pk(va.z + B[2], va.w + B[3]);
 #pragma unroll
-      for (int c = 4; c < 8; ++c) {
-        float y = qy[(c - 4) * QCAP + slot];
+      for (int d = 4; d < 7; ++d) Y67 = ffma2(Q67[d - 4], pk(z[d], z[d]), Y67);
+      float y[4];
+      upk(Y45, y[0], y[1]);
+      upk(Y67, y[2], y[3]);
+      y[1] = fmaf(L55, z[5], y[1]);
+      y[3] = fmaf(L77, z[7], y[3]);
 #pragma unroll
-        for (int d = 4; d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
-        mx = fmaxf(mx, y);
-        mn = fminf(mn, y);
+      for (int c = 0; c < 4; ++c) {
+        mx = fmaxf(mx, y[c]);
+        mn = fminf(mn, y[c]);
       }
 #pragma unroll
       for (int t = 0; t < T; ++t) cnt[t] += (mx >= dl(t) && mn <= dl(t)) ? 1u : 0u;
@@ -325,20 +399,20 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   uint32_t base = 0;
   // two samples per lane per iteration (instruction-level parallelism)
   for (; ILP == 2 && base + 64u <= Nl; base += 64u) {
-    float ya[6], yb[6];
-    const bool pa = phase1(base + lane, ya);
-    const bool pb = phase1(base + 32u + lane, yb);
-    push(pa, base + lane, ya);
+    float4 a0, a1, b0, b1;
+    const bool pa = phase1(base + lane, a0, a1);
+    const bool pb = phase1(base + 32u + lane, b0, b1);
+    push(pa, a0, a1);
     drain();
-    push(pb, base + 32u + lane, yb);
+    push(pb, b0, b1);
     drain();
   }
   for (; base < Nl; base += 32u) {
-    float ya[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
     const uint32_t s = base + lane;
     bool pa = false;
-    if (s < Nl) pa = phase1(s, ya);
-    push(pa, s, ya);
+    if (s < Nl) pa = phase1(s, a0, a1);
+    push(pa, a0, a1);
     drain();
   }
   if (qn > 0) {

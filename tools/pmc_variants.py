@@ -29,10 +29,14 @@ def build(name, flags):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
         raise SystemExit(r.stderr)
+    regs, cur = [], None
     for line in r.stderr.splitlines():
-        if "k_pmc" in line or ("registers" in line and "Used" in line):
-            pass
-    regs = [ln for ln in r.stderr.splitlines() if "Used" in ln]
+        if "Compiling entry function" in line:
+            cur = line.split("'")[1]
+        elif "Used" in line and cur and "k_pmcILi1E" in cur:
+            regs.append(line.strip())
+        elif "spill" in line and cur and "k_pmcILi1E" in cur:
+            regs.append(line.strip())
     objs = [os.path.join(B.BUILD, f) for f in sorted(os.listdir(B.BUILD))
             if f.endswith(".o") and f != "pmc.cu.o"] + [obj]
     subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-o", os.path.join(out, "liblcp.so"), *objs, "-lcudart"])

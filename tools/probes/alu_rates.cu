@@ -4,6 +4,7 @@
 // at the measured time (4.0 = one per SMSP per clock = full issue).
 #include <cstdint>
 #include <cstdio>
+#include "warm.cuh"
 
 #define CHAINS 8
 #define DEFK(name, T, init, ...)                                          \
@@ -52,6 +53,7 @@ typedef void (*kfn_u)(uint32_t*, int, uint32_t);
 typedef void (*kfn_f)(float*, int, float);
 
 int main() {
+  const double clk_mhz = warm_and_clock_mhz();
   void* d;
   cudaMalloc(&d, 64);
   cudaEvent_t e0, e1;
@@ -63,7 +65,7 @@ int main() {
   const int threads = 256, blocks = sms * 8, iters = 4096;
   auto report = [&](const char* name, float ms, double instr_per_step) {
     double warp_instr = instr_per_step * CHAINS * (double)iters * blocks * (threads / 32);
-    double per_sm_clk = warp_instr / (ms * 1e-3) / sms / 1.965e9;
+    double per_sm_clk = warp_instr / (ms * 1e-3) / sms / (clk_mhz * 1e6);
     printf("%-14s %7.3f ms  %.3f warp-instr/SM/clk (at 1.965 GHz)\n", name, ms, per_sm_clk);
   };
   struct U { const char* n; kfn_u f; double ipc; } us[] = {
