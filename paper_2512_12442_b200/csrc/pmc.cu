@@ -190,8 +190,10 @@ __device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb) {
 // Largest |z| Box-Muller can produce: u_a >= 2^-24 gives R <= sqrt(48 ln 2) = 5.7668;
 // 5.7684 adds the lg2/sqrt approximation error.
 constexpr float ZMAX = 5.7684f;
-constexpr int PMC_WARPS = 8;
-constexpr int QCAP = 64;            // pending samples per warp
+#ifndef PMC_WARPS
+#define PMC_WARPS 8
+#endif
+constexpr int QCAP = 96;            // pending samples per warp (< 32 + two pushes of 32)
 constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are branch-free
 
 // k_pmc<T>: exact two-phase evaluation of the PMC count for
@@ -350,7 +352,24 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   const f2_t Q45[1] = {pk(L[14], L[19])};
   const f2_t Q67[3] = {pk(L[25], L[32]), pk(L[26], L[33]), pk(L[27], L[34])};
   const float L55 = L[20], L77 = L[35];
-  // branch-free enqueue: pending lanes take consecutive slots, the others their trash row
+  // branch-free enqueue of two samples per lane: pending lanes take consecutive
+  // slots (all a's, then all b's), the others their trash row
+  const unsigned lt = (1u << lane) - 1u;
+  auto push2 = [&](bool pa, const float4& a0, const float4& a1, bool pb, const float4& b0, const float4& b1) {
+    unsigned ma, mb;
+    asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; vote.sync.ballot.b32 %0, p, 0xffffffff;}"
+                 : "=r"(ma) : "r"((unsigned)pa));
+    asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; vote.sync.ballot.b32 %0, p, 0xffffffff;}"
+                 : "=r"(mb) : "r"((unsigned)pb));
+    const int na = __popc(ma);
+    const int sa = pa ? qn + __popc(ma & lt) : QCAP + lane;
+    const int sb = pb ? qn + na + __popc(mb & lt) : QCAP + lane;
+    qv[2 * sa] = a0;
+    qv[2 * sa + 1] = a1;
+    qv[2 * sb] = b0;
+    qv[2 * sb + 1] = b1;
+    qn += na + __popc(mb);
+  };
   auto push = [&](bool pend, const float4& st0, const float4& st1) {
     const unsigned pm = __ballot_sync(0xffffffffu, pend);
     const int slot = pend ? qn + __popc(pm & ((1u << lane) - 1u)) : QCAP + lane;
@@ -402,9 +421,8 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     float4 a0, a1, b0, b1;
     const bool pa = phase1(base + lane, a0, a1);
     const bool pb = phase1(base + 32u + lane, b0, b1);
-    push(pa, a0, a1);
+    push2(pa, a0, a1, pb, b0, b1);
     drain();
-    push(pb, b0, b1);
     drain();
   }
   for (; base < Nl; base += 32u) {
