@@ -259,14 +259,19 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     for (int c = 0; c < 4; ++c) m[c] = mm[c];
 #pragma unroll
     for (int c = 4; c < 8; ++c) {
-      float tail = 0.0f, all = fabsf(mm[c]);
+      float all = fabsf(mm[c]);
 #pragma unroll
-      for (int d = 0; d <= c; ++d) {
-        all += ZB * fabsf(L[c * (c + 1) / 2 + d]);
-        if (d >= 4) tail += fabsf(L[c * (c + 1) / 2 + d]);
-      }
-      // |sum_{d>=4} L'_cd z_d| <= ZB tail; the slack covers the FP32 rounding of the
-      // partial sums, so phase-1 decisions equal the one-pass FP32 decisions
+      for (int d = 0; d <= c; ++d) all += ZB * fabsf(L[c * (c + 1) / 2 + d]);
+      // z4, z5 (and z6, z7) are one Box-Muller pair r (cos, sin) with r <= ZB, so
+      // |L'_c4 z4 + L'_c5 z5| <= ZB ||(L'_c4, L'_c5)||_2 (same for 6, 7): the tail is
+      // bounded by ZB (||.|| + ||.||); the slack covers the sin/cos approximation
+      // and the FP32 rounding of the partial sums, so phase-1 decisions equal the
+      // one-pass FP32 decisions
+      const float l4 = L[c * (c + 1) / 2 + 4];
+      const float l5 = c >= 5 ? L[c * (c + 1) / 2 + 5] : 0.0f;
+      const float l6 = c >= 6 ? L[c * (c + 1) / 2 + 6] : 0.0f;
+      const float l7 = c >= 7 ? L[c * (c + 1) / 2 + 7] : 0.0f;
+      const float tail = sqrtf(l4 * l4 + l5 * l5) + sqrtf(l6 * l6 + l7 * l7);
       B[c - 4] = ZB * tail * (1.0f + 1e-5f) + 1e-6f * all;
       mB[c - 4] = mm[c] - B[c - 4];
     }
