@@ -265,7 +265,8 @@ def run_ours(args):
     leaves_tot = 0
     mc_ms_tot = 0.0
     p2_tot = 0
-    st_phase = {"fit_ms": 0.0, "refine_ms": 0.0, "posterior_ms": 0.0, "chol_ms": 0.0, "mc_ms": 0.0}
+    st_phase = {"fit_ms": 0.0, "refine_ms": 0.0, "brick_pass_ms": 0.0, "posterior_ms": 0.0, "chol_ms": 0.0,
+                "mc_ms": 0.0}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for _ in range(args.steps):

@@ -129,6 +129,12 @@ lcp_status_t lcp_create(int32_t device, void* cuda_stream, lcp_ctx_t** out) {
     return LCP_ENOMEM;
   }
   cudaMemsetAsync(c.derr.p, 0, sizeof(int) * 4, c.stream);
+  if (cudaMallocHost(&c.h_counters, sizeof(int64_t) * 16) != cudaSuccess) {
+    c.h_counters = nullptr;
+    c.derr.release();
+    delete h;
+    return LCP_ENOMEM;
+  }
   for (int i = 0; i < 8; ++i) cudaEventCreate(&c.ev[i]);
   c.ev_init = true;
   *out = h;
@@ -146,7 +152,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
-                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.crec, &c.brick_done, &c.brick_unit, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)
@@ -371,17 +377,18 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
   CTX_GUARD(ctx);
   if (!buf || cap == 0) return LCP_EINVAL;
   std::string s = "{";
-  char tmp[512];
+  char tmp[1024];
   std::snprintf(tmp, sizeof tmp,
                 "\"fit_ms\": %.6f, \"refine_ms\": %.6f, \"posterior_ms\": %.6f, \"chol_ms\": %.6f, \"mc_ms\": %.6f, "
                 "\"scatter_ms\": %.6f, \"leaves\": %lld, \"pmc_cells\": %lld, \"pmc_samples\": %lld, "
                 "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld, "
-                "\"launches\": %lld, \"brick_runs\": %lld, \"pmc_phase2_samples\": %lld",
+                "\"launches\": %lld, \"brick_runs\": %lld, \"pmc_phase2_samples\": %lld, \"brick_pass_ms\": %.6f, "
+                "\"fused\": %d, \"pmc_used_records\": %d",
                 c.t.fit_ms, c.t.refine_ms, c.t.posterior_ms, c.t.chol_ms, c.t.mc_ms, c.t.scatter_ms,
                 (long long)c.n_leaves, (long long)c.last_pmc_cells, (long long)c.last_pmc_samples,
                 (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m,
                 (long long)c.n_launch, (long long)c.last_brick_runs,
-                (long long)c.last_pmc_phase2);
+                (long long)c.last_pmc_phase2, c.t.brick_ms, c.fused ? 1 : 0, c.last_pmc_records ? 1 : 0);
   s += tmp;
   auto arr = [&](const char* name, const std::vector<int64_t>& v) {
     s += ", \"";

@@ -13,6 +13,9 @@
 // staged while consecutive runs stay in the same bucket.  Identical arithmetic
 // to k_cell_posterior up to FP64 rounding order.
 #include <algorithm>
+#include <cstdlib>
+
+#include "chol8.cuh"
 
 #include "ctx.h"
 
@@ -61,10 +64,26 @@ __global__ void k_brick_starts(const int64_t* __restrict__ flag, const int64_t* 
   if (q < n && flag[q]) start[runidx[q]] = q;
 }
 
+// Work unit of k_brick: a run of leaf cells of one brick (FUSED = false: the leaf
+// pass of an arbitrary Morton-ordered list, output post[q]) or a whole brick given
+// by its level-(Lfull-2) octree node key (FUSED = true: the refine-time brick pass,
+// output post[64 u + local cell] for every in-grid cell of the brick, plus the
+// vertex marginals of the brick's own-bucket vertices into the vertex cache).
+struct BrickOut {
+  double* post;               // 44 doubles per output slot
+  double2* vcache;            // FUSED: (mu, 1 / (sigma sqrt 2)) per grid vertex
+  uint32_t* vmask;            // FUSED: vertex "requested / cached" bits
+  const uint64_t* bricks;     // FUSED: node keys (i | j << 21 | k << 42) at level Lfull - 2
+  uint8_t* bdone;             // FUSED: per brick (Morton index of the node): pass done
+  uint8_t* ucomp;             // FUSED: per unit of this launch: computed here (else skipped)
+  double var_floor;
+  int* derr;
+};
+
+template <bool FUSED>
 __global__ void __launch_bounds__(BRICK_THREADS, 1)
-    k_brick_posterior(BrickArgs a, const int64_t* __restrict__ cells, const int64_t* __restrict__ run_start,
-                      int64_t nruns, unsigned long long* __restrict__ work, double* __restrict__ post,
-                      int* __restrict__ derr) {
+    k_brick(BrickArgs a, const int64_t* __restrict__ cells, const int64_t* __restrict__ run_start, int64_t nruns,
+            unsigned long long* __restrict__ work, BrickOut o) {
   extern __shared__ double smem[];
   const int k = a.k, KP = a.kp8;
   const int64_t LA = la_size(k);
@@ -75,6 +94,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
   double* KV = smem + head;                     // KP x VSTR
   double* sMu = KV + (int64_t)KP * VSTR;        // NVP
   __shared__ int64_t s_r0;
+  __shared__ int s_skip;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geom& g = a.g;
   int staged = -1;
@@ -85,11 +105,29 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
     if (r0 >= nruns) break;
     const int64_t r1 = min(nruns, r0 + BRICK_CHUNK);
     for (int64_t r = r0; r < r1; ++r) {
-      const int64_t q0 = run_start[r], q1 = run_start[r + 1];
-      int ci, cj, ck;
-      cell_ijk(g, cells[q0], ci, cj, ck);
-      const int i0 = ci & ~(BK - 1), j0 = cj & ~(BK - 1), k0 = ck & ~(BK - 1);
-      const int b = bucket_id(g, vbucket_axis(g, 0, ci), vbucket_axis(g, 1, cj), vbucket_axis(g, 2, ck));
+      int i0, j0, k0;
+      int64_t q0 = 0, q1 = 0;
+      if (FUSED) {
+        int bi, bj, bk;
+        node_unkey(o.bricks[r], bi, bj, bk);
+        i0 = BK * bi; j0 = BK * bj; k0 = BK * bk;
+        if (tid == 0) {
+          uint8_t* d = o.bdone + morton3(bi, bj, bk);
+          s_skip = *d;
+          *d = 1;
+          o.ucomp[r] = s_skip ? 0 : 1;
+        }
+        __syncthreads();
+        if (s_skip) continue;   // uniform: done by an earlier refine (another isovalue)
+      } else {
+        q0 = run_start[r];
+        q1 = run_start[r + 1];
+        int ci, cj, ck;
+        cell_ijk(g, cells[q0], ci, cj, ck);
+        i0 = ci & ~(BK - 1); j0 = cj & ~(BK - 1); k0 = ck & ~(BK - 1);
+      }
+      // all cells of a brick lie in one bucket (bucket side >= BK)
+      const int b = bucket_id(g, vbucket_axis(g, 0, i0), vbucket_axis(g, 1, j0), vbucket_axis(g, 2, k0));
       if (b != staged) {
         const double2* src = reinterpret_cast<const double2*>(a.bdata + (int64_t)b * a.bstride);
         double2* dst = reinterpret_cast<double2*>(smem);
@@ -156,11 +194,41 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         }
       }
       __syncthreads();
-      // phase 3: Sigma_C = K_CC - V_C^T V_C per leaf cell (warp per cell)
-      for (int64_t q = q0 + wid; q < q1; q += BRICK_THREADS / 32) {
-        int64_t cell = cells[q];
+      if (FUSED && tid < NVB) {
+        // vertex marginals (R10) of the brick's vertices whose own bucket is b:
+        // var = k(v,v) - ||V_{:,v}||^2, cached as (mu, 1 / (sigma sqrt 2))
+        const int va = tid % (BK + 1), vb = (tid / (BK + 1)) % (BK + 1), vc = tid / ((BK + 1) * (BK + 1));
+        const int vi = i0 + va, vj = j0 + vb, vk = k0 + vc;
+        if (vi <= g.cells[0] && vj <= g.cells[1] && vk <= g.cells[2] &&
+            bucket_id(g, vbucket_axis(g, 0, vi), vbucket_axis(g, 1, vj), vbucket_axis(g, 2, vk)) == b) {
+          const int64_t vid = vertex_id(g, vi, vj, vk);
+          const uint32_t bit = 1u << (vid & 31);
+          if (!(atomicOr(&o.vmask[vid >> 5], bit) & bit)) {
+            double s2 = 0.0;
+            for (int j = 0; j < k; ++j) {
+              const double v = KV[(int64_t)j * VSTR + tid];
+              s2 = fma(v, v, s2);
+            }
+            const double var = a.kp.var - s2;
+            if (var < a.var_err) atomicOr(o.derr, DERR_NUMERIC);
+            const double vf = var > o.var_floor ? var : o.var_floor;
+            o.vcache[vid] = make_double2(sMu[tid], 1.0 / (sqrt(vf) * SQRT2));
+          }
+        }
+      }
+      // phase 3: Sigma_C = K_CC - V_C^T V_C per cell (warp per cell)
+      const int64_t nq = FUSED ? BK * BK * BK : q1 - q0;
+      for (int64_t qq = wid; qq < nq; qq += BRICK_THREADS / 32) {
         int xi, xj, xk;
-        cell_ijk(g, cell, xi, xj, xk);
+        int64_t slot;
+        if (FUSED) {
+          xi = i0 + (int)(qq & 3); xj = j0 + (int)((qq >> 2) & 3); xk = k0 + (int)(qq >> 4);
+          if (xi >= g.cells[0] || xj >= g.cells[1] || xk >= g.cells[2]) continue;
+          slot = 64 * r + qq;   // unit r of this launch
+        } else {
+          cell_ijk(g, cells[q0 + qq], xi, xj, xk);
+          slot = q0 + qq;
+        }
         const int cr = lr;   // corner of this lane's A row / B column
         const int lv = (xi - i0 + (cr & 1)) + (BK + 1) * ((xj - j0 + ((cr >> 1) & 1)) + (BK + 1) * (xk - k0 + (cr >> 2)));
         double d0 = 0.0, d1 = 0.0;
@@ -168,24 +236,108 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
           double v = KV[(int64_t)(s + lc) * VSTR + lv];
           dmma(v, v, d0, d1);
         }
-        double* rec = post + 44 * q;
+        double* rec = o.post + 44 * slot;
         // lane holds D[cr][2 lc], D[cr][2 lc + 1]
         const int c0 = 2 * lc, c1 = 2 * lc + 1;
         if (c0 <= cr) {
           double s0 = a.kcc[cr * 8 + c0] - d0;
           rec[8 + cr * (cr + 1) / 2 + c0] = s0;
-          if (c0 == cr && s0 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+          if (c0 == cr && s0 < a.var_err) atomicOr(o.derr, DERR_NUMERIC);
         }
         if (c1 <= cr) {
           double s1 = a.kcc[cr * 8 + c1] - d1;
           rec[8 + cr * (cr + 1) / 2 + c1] = s1;
-          if (c1 == cr && s1 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+          if (c1 == cr && s1 < a.var_err) atomicOr(o.derr, DERR_NUMERIC);
         }
         if (lc == 0) rec[cr] = sMu[lv];
       }
       __syncthreads();
     }
   }
+}
+
+static BrickArgs brick_args(const Ctx& c) {
+  BrickArgs a;
+  a.kp = c.kp;
+  a.g = c.g;
+  a.k = c.k;
+  a.kp8 = (c.k + 7) & ~7;
+  a.bstride = c.bstride;
+  a.bdata = c.bdata.as<double>();
+  for (int p = 0; p < 8; ++p)
+    for (int q = 0; q < 8; ++q) a.kcc[p * 8 + q] = c.kcc[p >= q ? p * (p + 1) / 2 + q : q * (q + 1) / 2 + p];
+  a.var_err = -1e-8 * c.kp.var;
+  return a;
+}
+
+static size_t brick_smem(int k) {
+  const int kp8 = (k + 7) & ~7;
+  const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
+  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP);
+}
+
+bool fused_brick_supported(const Ctx& c) {
+  return c.k <= 128 && c.g.bs >= BK && brick_smem(c.k) <= 227 * 1024 && c.opts.precision != LCP_FP32 &&
+         c.g.lfull >= 2;
+}
+
+// Enable the refine-time brick pass for this fit when the kernel supports the model
+// and the records (208 B per cell of the virtual cube) fit in free HBM with 4 GB
+// to spare; LCP_FUSED=0 in the environment disables it (A/B measurements).
+lcp_status_t fused_setup(Ctx& c) {
+  c.fused = false;
+  static const bool env_off = [] {
+    const char* v = std::getenv("LCP_FUSED");
+    return v && v[0] == '0';
+  }();
+  if (env_off || !fused_brick_supported(c)) return LCP_OK;
+  const int64_t ncodes = (int64_t)1 << (3 * c.g.lfull);
+  const int64_t nbr = (int64_t)1 << (3 * (c.g.lfull - 2));
+  const size_t need = sizeof(CellRec) * (size_t)ncodes;
+  if (c.crec.cap < need) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return LCP_OK;
+    if (need + ((size_t)4 << 30) > fr) return LCP_OK;
+  }
+  cudaError_t e;
+  if ((e = c.crec.ensure(need)) != cudaSuccess) {
+    cudaGetLastError();
+    return LCP_OK;   // not enough memory after all: the per-leaf path stays
+  }
+  if ((e = c.brick_done.ensure(nbr)) != cudaSuccess) return cuda_err(c, e, "brick_done");
+  if ((e = c.brick_unit.ensure(BRICK_PASS_CHUNK)) != cudaSuccess) return cuda_err(c, e, "brick_unit");
+  if ((e = cudaMemsetAsync(c.brick_done.p, 0, nbr, c.stream)) != cudaSuccess) return cuda_err(c, e, "brick_done");
+  c.fused = true;
+  return LCP_OK;
+}
+
+// FUSED brick pass over nb frontier nodes of level Lfull - 2 (node keys), writing
+// the 8-corner posteriors of their cells into post (44 doubles per slot, slot =
+// 64 u + local cell for unit u) and their own-bucket vertex marginals into the
+// vertex cache.  Bricks already done (bdone) are skipped (their slots untouched).
+cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double* post) {
+  if (nb <= 0) return cudaSuccess;
+  cudaError_t err;
+  if ((err = c.counters.ensure(sizeof(unsigned long long) * 16)) != cudaSuccess) return err;
+  unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  if ((err = cudaMemsetAsync(dcnt + 13, 0, sizeof(unsigned long long), c.stream)) != cudaSuccess) return err;
+  const size_t smem = brick_smem(c.k);
+  if ((err = cudaFuncSetAttribute(k_brick<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return err;
+  BrickOut o;
+  o.post = post;
+  o.vcache = c.vcache.as<double2>();
+  o.vmask = c.vstate.as<uint32_t>();
+  o.bricks = bricks;
+  o.bdone = c.brick_done.as<uint8_t>();
+  o.ucomp = c.brick_unit.as<uint8_t>();
+  o.var_floor = 1e-12 * c.kp.var;
+  o.derr = c.derr.as<int>();
+  unsigned grid = (unsigned)std::min<int64_t>((nb + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count);
+  k_brick<true><<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), nullptr, nullptr, nb, dcnt + 13, o);
+  ++c.n_launch;
+  return cudaGetLastError();
 }
 
 // Returns true when the brick path handled the list (Morton-like order with
@@ -221,23 +373,15 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
   if ((err = cudaMemcpyAsync(start + nruns, &n, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream)) != cudaSuccess)
     return false;
   if ((err = cudaMemsetAsync(dcnt + 13, 0, sizeof(unsigned long long), c.stream)) != cudaSuccess) return false;
-  BrickArgs a;
-  a.kp = c.kp;
-  a.g = c.g;
-  a.k = k;
-  a.kp8 = kp8;
-  a.bstride = c.bstride;
-  a.bdata = c.bdata.as<double>();
-  for (int p = 0; p < 8; ++p)
-    for (int q = 0; q < 8; ++q) a.kcc[p * 8 + q] = c.kcc[p >= q ? p * (p + 1) / 2 + q : q * (q + 1) / 2 + p];
-  a.var_err = -1e-8 * c.kp.var;
-  if ((err = cudaFuncSetAttribute(k_brick_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+  if ((err = cudaFuncSetAttribute(k_brick<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
       cudaSuccess)
     return false;
+  BrickOut o{};
+  o.post = post;
+  o.derr = c.derr.as<int>();
   int blocks_per_sm = smem <= 110 * 1024 ? 2 : 1;
   unsigned grid = (unsigned)std::min<int64_t>((nruns + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count * blocks_per_sm);
-  k_brick_posterior<<<grid, BRICK_THREADS, smem, c.stream>>>(a, cells, start, nruns, dcnt + 13, post,
-                                                             c.derr.as<int>());
+  k_brick<false><<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), cells, start, nruns, dcnt + 13, o);
   ++c.n_launch;
   err = cudaGetLastError();
   c.last_brick_runs = nruns;

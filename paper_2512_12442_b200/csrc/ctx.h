@@ -51,8 +51,11 @@ struct DevBuf {
   T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+constexpr int64_t BRICK_PASS_CHUNK = (int64_t)1 << 17;   // bricks per brick-pass launch (8.4 M cells)
+
 struct PhaseTimes {
   double fit_ms = 0, refine_ms = 0, posterior_ms = 0, chol_ms = 0, mc_ms = 0, scatter_ms = 0;
+  double brick_ms = 0;   // refine-time brick pass (part of refine_ms)
 };
 
 struct Ctx {
@@ -114,11 +117,18 @@ struct Ctx {
   // leaf pass scratch
   DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
   DevBuf brick_flag, brick_idx, brick_start;
+  // refine-time brick pass (brick.cu k_brick<true>): MC records of every cell of the
+  // level-(Lfull-2) frontier bricks, indexed by the cell's Morton code
+  bool fused = false;            // enabled for this fit (supported and records fit in HBM)
+  DevBuf crec;                   // CellRec per Morton code of the virtual 2^Lfull cube
+  DevBuf brick_done;             // uint8 per brick (Morton code of the level-(Lfull-2) node)
+  DevBuf brick_unit;             // uint8 per unit of a brick-pass launch: computed by it
   DevBuf cellmask;               // NEXT-3: uint16 per cell, bit t = leaf of isovalue t
   DevBuf union_cells, union_mask; // NEXT-3: union leaf list (Morton order) and its masks
   int64_t n_union = 0;
   DevBuf pmc_counters;           // [0]: samples finished in phase 2 of k_pmc
   int64_t last_pmc_phase2 = 0;
+  bool last_pmc_records = false; // the last pmc read the brick-pass records
   int64_t last_brick_runs = 0;   // brick runs of the last posterior (0: per-cell path)
 
   // host pinned staging for counters
@@ -161,6 +171,10 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
 cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* perm,
                                   const int32_t* bkt_sorted, int64_t n, double* post);
 bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err);
+bool fused_brick_supported(const Ctx& c);
+cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double* post);
+cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post);
+lcp_status_t fused_setup(Ctx& c);
 
 lcp_status_t set_err(Ctx& c, lcp_status_t st, const std::string& msg);
 lcp_status_t cuda_err(Ctx& c, cudaError_t e, const char* where);

@@ -738,7 +738,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   c.vcache_valid = true;
   c.fitted = true;
 #undef CK
-  return LCP_OK;
+  return fused_setup(c);
 }
 
 }  // namespace lcp

@@ -379,6 +379,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
   int64_t nF = 1;
   c.n_leaves = 0;
   c.n_recs = 0;
+  c.t.brick_ms = 0;
   c.last_requests = 0;
   c.level_nodes.clear();
   c.level_refined.clear();
@@ -414,6 +415,29 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     CK(c.perm.ensure(sizeof(int64_t) * cap));
     CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * 16, c.stream));
     const uint64_t* F = c.front[cur].as<uint64_t>();
+    if (c.fused && h == 2) {
+      // refine-time brick pass: the frontier nodes of this level are the aligned 4^3-cell
+      // bricks; one pass computes their vertex marginals (the bound's lattice, R6, R10)
+      // and the MC records of all their cells (a7-a8), reused by every later leaf pass
+      cudaEvent_t b0, b1;
+      cudaEventCreate(&b0);
+      cudaEventCreate(&b1);
+      cudaEventRecord(b0, c.stream);
+      const int64_t ch = std::min<int64_t>(nF, BRICK_PASS_CHUNK);
+      CK(c.post.ensure(sizeof(double) * 44 * 64 * ch));
+      for (int64_t off = 0; off < nF; off += ch) {
+        const int64_t nb = std::min(ch, nF - off);
+        CK(launch_brick_pass(c, F + off, nb, c.post.as<double>()));
+        CK(launch_chol8_rec(c, F + off, nb, c.post.as<double>()));
+      }
+      cudaEventRecord(b1, c.stream);
+      CK(cudaEventSynchronize(b1));
+      float bms = 0;
+      cudaEventElapsedTime(&bms, b0, b1);
+      c.t.brick_ms += bms;
+      cudaEventDestroy(b0);
+      cudaEventDestroy(b1);
+    }
     const int G = h == 0 ? 1 : (h == 1 ? 4 : (h == 2 ? 8 : 32));
     unsigned gw = (unsigned)((nF * G + 255) / 256);
 #define PRELIM(GG)                                                                                              \

@@ -13,13 +13,13 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "chol8.cuh"
 #include "ctx.h"
 
 namespace lcp {
 
 // The constant -sqrt(2 ln 2) of Box-Muller's R = sqrt(-2 ln 2 lg2(u_a)) (and its sign)
-// is carried by L' (k_chol8 stores FOLD_SCALE L'), so k_pmc draws z / FOLD_SCALE.
-constexpr double FOLD_SCALE = -1.1774100225154747;
+// is carried by L' (chol8.cuh stores FOLD_SCALE L), so k_pmc draws z / FOLD_SCALE.
 constexpr int64_t PMC_CHUNK = (int64_t)1 << 23;   // cells per posterior/MC chunk (2.9 GB of records)
 
 __global__ void k_cell_bucket(Geom g, const int64_t* __restrict__ cells, int64_t n, int32_t* __restrict__ bkt,
@@ -51,53 +51,77 @@ __global__ void k_gather_bkt(const int32_t* __restrict__ bkt, const int64_t* __r
 
 // a8: in-place: rec = [mu (8 double) | Sigma packed (36 double)] ->
 //                     [mu_pi (8 double) | L' packed row-major lower (36 float) | unused]
-// with L' = chol(Sigma[pi][pi]) in the corner order pi = (0,3,5,6,1,2,4,7) (R13b):
-// even-parity corners first, so the last four corners have small conditional
-// spread given the first four (used by the exact early decision of k_pmc).
+// (chol8.cuh).  The tetrahedral corner order makes the last four corners' conditional
+// spread small given the first four (used by the exact early decision of k_pmc).
 __global__ void k_chol8(double* __restrict__ post, int64_t n) {
-  constexpr int kPi8[8] = {0, 3, 5, 6, 1, 2, 4, 7};
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   double* rec = post + 44 * q;
-  double S[36], mu[8];
+  double mu[8], sig[36], mo[8];
+  float Lf[36];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int pi = kPi8[i];
-    mu[i] = rec[pi];
+  for (int i = 0; i < 8; ++i) mu[i] = rec[i];
 #pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      const int pj = kPi8[j];
-      const int r = pi > pj ? pi : pj, c = pi > pj ? pj : pi;
-      S[i * (i + 1) / 2 + j] = rec[8 + r * (r + 1) / 2 + c];
-    }
+  for (int p = 0; p < 36; ++p) sig[p] = rec[8 + p];
+  chol8_factor(mu, sig, mo, Lf);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) rec[i] = mo[i];
+  float4* L4 = reinterpret_cast<float4*>(rec + 8);
+#pragma unroll
+  for (int t = 0; t < 9; ++t) L4[t] = make_float4(Lf[4 * t], Lf[4 * t + 1], Lf[4 * t + 2], Lf[4 * t + 3]);
+}
+
+// refine-time brick pass output (44-double slots, 64 per brick unit) -> MC records
+// indexed by the cell's Morton code in the virtual 2^Lfull cube
+__global__ void k_chol8_rec(Geom g, const uint64_t* __restrict__ bricks, int64_t nb,
+                            const uint8_t* __restrict__ ucomp, const double* __restrict__ post,
+                            CellRec* __restrict__ recs) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 64 * nb) return;
+  const int64_t u = t >> 6;
+  if (!ucomp[u]) return;   // brick done by an earlier refine: its record stands
+  const int qq = (int)(t & 63);
+  int bi, bj, bk;
+  node_unkey(bricks[u], bi, bj, bk);
+  const int xi = 4 * bi + (qq & 3), xj = 4 * bj + ((qq >> 2) & 3), xk = 4 * bk + (qq >> 4);
+  if (xi >= g.cells[0] || xj >= g.cells[1] || xk >= g.cells[2]) return;
+  const double* rec = post + 44 * t;
+  double mu[8], sig[36];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mu[i] = rec[i];
+#pragma unroll
+  for (int p = 0; p < 36; ++p) sig[p] = rec[8 + p];
+  CellRec& out = recs[morton3(xi, xj, xk)];
+  double mo[8];
+  float Lf[36];
+  chol8_factor(mu, sig, mo, Lf);
+  double2* m2 = reinterpret_cast<double2*>(out.mu);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) m2[i] = make_double2(mo[2 * i], mo[2 * i + 1]);
+  float4* L4 = reinterpret_cast<float4*>(out.L);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) L4[i] = make_float4(Lf[4 * i], Lf[4 * i + 1], Lf[4 * i + 2], Lf[4 * i + 3]);
+}
+
+cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post) {
+  if (nb <= 0) return cudaSuccess;
+  k_chol8_rec<<<(unsigned)((64 * nb + 127) / 128), 128, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(),
+                                                                      post, c.crec.as<CellRec>());
+  ++c.n_launch;
+  return cudaGetLastError();
+}
+
+// 1 in cov[0] if some cell's brick has no record (the list needs the posterior path)
+__global__ void k_cells_covered(Geom g, const int64_t* __restrict__ cells, int64_t n,
+                                const uint8_t* __restrict__ bdone, unsigned long long* __restrict__ cov) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool miss = false;
+  if (q < n) {
+    int i, j, k;
+    cell_ijk(g, cells[q], i, j, k);
+    miss = !bdone[morton3(i >> 2, j >> 2, k >> 2)];
   }
-  double md = 0.0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) md = fmax(md, S[c * (c + 3) / 2]);
-  const double tol = 1e-12 * md;
-  double L[36];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    double s = S[j * (j + 3) / 2];
-#pragma unroll
-    for (int p = 0; p < j; ++p) s -= L[j * (j + 1) / 2 + p] * L[j * (j + 1) / 2 + p];
-    bool live = s > tol;
-    double ljj = live ? sqrt(s) : 0.0;
-    double inv = live ? 1.0 / ljj : 0.0;
-    L[j * (j + 3) / 2] = ljj;
-#pragma unroll
-    for (int i = j + 1; i < 8; ++i) {
-      double t = S[i * (i + 1) / 2 + j];
-#pragma unroll
-      for (int p = 0; p < j; ++p) t -= L[i * (i + 1) / 2 + p] * L[j * (j + 1) / 2 + p];
-      L[i * (i + 1) / 2 + j] = live ? t * inv : 0.0;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) rec[i] = mu[i];
-  float* Lf = reinterpret_cast<float*>(rec + 8);
-#pragma unroll
-  for (int p = 0; p < 36; ++p) Lf[p] = (float)(FOLD_SCALE * L[p]);
+  if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(cov, 1ull);
 }
 
 // Philox4x32-10 round keys (k0 + r W0, k1 + r W1), r = 0..9, passed as a kernel
@@ -225,8 +249,9 @@ struct IsoOffsets {
 
 template <int T>
 __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
-    k_pmc(const int64_t* __restrict__ cells, const double* __restrict__ post, int64_t n, double theta,
-          const IsoOffsets D, uint32_t N, const PhiloxKeys K, uint32_t iso, const uint32_t* __restrict__ mask,
+    k_pmc(const Geom g, const int64_t* __restrict__ cells, const double* __restrict__ post, int64_t rec_stride,
+          int rec_by_morton,
+          int64_t n, double theta, const IsoOffsets D, uint32_t N, const PhiloxKeys K, uint32_t iso, const uint32_t* __restrict__ mask,
           int64_t out_stride, float* __restrict__ out, unsigned long long* __restrict__ n_phase2) {
   constexpr int ILP = (T <= 4) ? PMC_ILP : 1;
   // queue, slot-major: (lo4..lo7), (max y0..3, min y0..3, s, -)
@@ -242,7 +267,16 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   uint32_t c1 = 0, c2 = 0;
   constexpr float ZB = (float)(ZMAX / 1.1774100225154747);   // bound on |z / FOLD_SCALE|
   if (live) {
-    const double* rec = post + 44 * q;
+    const int64_t cell = cells[q];
+    c1 = (uint32_t)(uint64_t)cell;
+    c2 = (uint32_t)((uint64_t)cell >> 32);
+    int64_t ri = q;
+    if (rec_by_morton) {
+      int ci, cj, ck;
+      cell_ijk(g, cell, ci, cj, ck);
+      ri = (int64_t)morton3(ci, cj, ck);
+    }
+    const double* rec = post + rec_stride * ri;
     float mm[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) mm[c] = (float)(rec[c] - theta);
@@ -252,9 +286,6 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
       float4 v = L4[t];
       L[4 * t] = v.x; L[4 * t + 1] = v.y; L[4 * t + 2] = v.z; L[4 * t + 3] = v.w;
     }
-    int64_t cell = cells[q];
-    c1 = (uint32_t)(uint64_t)cell;
-    c2 = (uint32_t)((uint64_t)cell >> 32);
 #pragma unroll
     for (int c = 0; c < 4; ++c) m[c] = mm[c];
 #pragma unroll
@@ -509,11 +540,11 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
 }
 
 template <int T>
-static void launch_pmc(Ctx& c, unsigned grid, const int64_t* cells, const double* post, int64_t n, double theta,
-                       const IsoOffsets& D, uint32_t N, const PhiloxKeys& keys, uint32_t iso, const uint32_t* mask,
-                       int64_t stride, float* out) {
-  k_pmc<T><<<grid, PMC_WARPS * 32, 0, c.stream>>>(cells, post, n, theta, D, N, keys, iso, mask, stride, out,
-                                                  c.pmc_counters.as<unsigned long long>());
+static void launch_pmc(Ctx& c, unsigned grid, const int64_t* cells, const double* post, int64_t rec_stride,
+                       int by_morton, int64_t n, double theta, const IsoOffsets& D, uint32_t N,
+                       const PhiloxKeys& keys, uint32_t iso, const uint32_t* mask, int64_t stride, float* out) {
+  k_pmc<T><<<grid, PMC_WARPS * 32, 0, c.stream>>>(c.g, cells, post, rec_stride, by_morton, n, theta, D, N, keys, iso,
+                                                  mask, stride, out, c.pmc_counters.as<unsigned long long>());
 }
 
 // leaf pass for T isovalues (T = 1: lcp_pmc_cells; T > 1: NEXT-3).  out[t * stride + q].
@@ -537,11 +568,8 @@ lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const doubl
     for (int i = 0; i < 8; ++i) cudaEventCreate(&c.ev[i]);
     c.ev_init = true;
   }
-  int64_t chunk = std::min(n, PMC_CHUNK);
-  CK(c.post.ensure(sizeof(double) * 44 * chunk));
   CK(c.pmc_counters.ensure(sizeof(unsigned long long) * 2));
   CK(cudaMemsetAsync(c.pmc_counters.p, 0, sizeof(unsigned long long) * 2, c.stream));
-  double* post = c.post.as<double>();
   float tp = 0, tc = 0, tm = 0;
   PhiloxKeys keys;
   for (int r = 0; r < 10; ++r) {
@@ -552,20 +580,44 @@ lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const doubl
   for (int t = 0; t < MAX_ISO; ++t) D.dl[t] = t < T ? (float)(thetas[t] - thetas[0]) : INFINITY;
   D.n_out = T;
   const int Tp = T <= 4 ? T : (T <= 6 ? 6 : (T <= 8 ? 8 : (T <= 12 ? 12 : 16)));
+  // records of the refine-time brick pass cover the list? (e.g. every leaf of a refine)
+  bool use_rec = false;
+  if (c.fused) {
+    CK(c.counters.ensure(sizeof(unsigned long long) * 16));
+    unsigned long long* dcnt = c.counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(dcnt + 12, 0, sizeof(unsigned long long), c.stream));
+    k_cells_covered<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.g, cells, n, c.brick_done.as<uint8_t>(),
+                                                                      dcnt + 12);
+    ++c.n_launch;
+    CK(cudaMemcpyAsync(c.h_counters + 12, dcnt + 12, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    use_rec = c.h_counters[12] == 0;
+  }
+  const int64_t chunk = use_rec ? n : std::min(n, PMC_CHUNK);
+  if (!use_rec) CK(c.post.ensure(sizeof(double) * 44 * chunk));
   for (int64_t s0 = 0; s0 < n; s0 += chunk) {
     int64_t nn = std::min(chunk, n - s0);
+    const double* rec = use_rec ? c.crec.as<double>() : c.post.as<double>();
     cudaEventRecord(c.ev[0], c.stream);
-    lcp_status_t st = posterior_impl(c, cells + s0, nn, post);
-    if (st != LCP_OK) return st;
+    if (!use_rec) {
+      lcp_status_t st = posterior_impl(c, cells + s0, nn, c.post.as<double>());
+      if (st != LCP_OK) return st;
+    }
     cudaEventRecord(c.ev[1], c.stream);
-    k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(post, nn);
-    ++c.n_launch;
+    if (!use_rec) {
+      k_chol8<<<(unsigned)((nn + 127) / 128), 128, 0, c.stream>>>(c.post.as<double>(), nn);
+      ++c.n_launch;
+    }
     cudaEventRecord(c.ev[2], c.stream);
     const unsigned gr = (unsigned)((nn + PMC_WARPS - 1) / PMC_WARPS);
     const uint32_t* mk = mask ? mask + s0 : nullptr;
+    const int64_t rs = use_rec ? (int64_t)(sizeof(CellRec) / sizeof(double)) : 44;
     switch (Tp) {
-#define LP(TT) \
-  case TT: launch_pmc<TT>(c, gr, cells + s0, post, nn, thetas[0], D, (uint32_t)N, keys, iso, mk, stride, out + s0); break
+#define LP(TT)                                                                                                  \
+  case TT:                                                                                                      \
+    launch_pmc<TT>(c, gr, cells + s0, rec, rs, use_rec ? 1 : 0, nn, thetas[0], D, (uint32_t)N, keys, iso, mk,  \
+                   stride, out + s0);                                                                           \
+    break
       LP(1); LP(2); LP(3); LP(4); LP(6); LP(8); LP(12); LP(16);
 #undef LP
     }
@@ -579,6 +631,7 @@ lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const doubl
     cudaEventElapsedTime(&d, c.ev[2], c.ev[3]);
     tp += a; tc += b; tm += d;
   }
+  c.last_pmc_records = use_rec;
   c.t.posterior_ms = tp;
   c.t.chol_ms = tc;
   c.t.mc_ms = tm;

@@ -515,3 +515,28 @@ def test_multi_iso_c4_full_size_sampled(dev):
     for t in range(len(thetas)):
         frac, mean, mx = lcp_parity(F[t][cells_g[sel]], lcp_o[t], cfg.n_samples)
         assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_brick_pass_records_equal_leaf_posterior_path(name, dev):
+    # the refine-time brick pass (vertex marginals + MC records of every frontier brick)
+    # feeds the leaf pass; a list with one pruned cell takes the per-leaf posterior
+    # path instead.  Both must give bit-identical LCPs on the common leaves.
+    w, ctx, M = _ctx(name, dev, keep_records=False)
+    cfg = w.cfg
+    th = w.thetas[0]
+    field, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    st = ctx.stats()
+    assert st["fused"] == 1 and st["pmc_used_records"] == 1 and st["brick_pass_ms"] > 0, st
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).clone()
+    allc = torch.arange(int(np.prod(cfg.cells)), device=dev, dtype=torch.int64)
+    lcp_all = ctx.pmc_cells(allc, th, cfg.n_samples, cfg.mc_seed)
+    if len(leaves) < len(allc):
+        assert ctx.stats()["pmc_used_records"] == 0
+    assert torch.equal(lcp_all[leaves], field[leaves])
+    # and the records agree with the oracle on a sample of leaves
+    lv = leaves.cpu().numpy()
+    sel = np.random.default_rng(2).choice(len(lv), 200, replace=False)
+    lcp_o = M.pmc_cells(lv[sel], th, cfg.n_samples, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(field.cpu().numpy()[lv[sel]], lcp_o, cfg.n_samples)
+    assert frac >= 0.99 and mean <= 1e-4, (frac, mean, mx)
