@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--extreme", type=int, default=0,
                     help="NEXT-1: continuous extreme-search iterations at coarse octree nodes (0 = lattice)")
+    ap.add_argument("--separate-iso", action="store_true",
+                    help="multi-isovalue workloads: one run_field per isovalue instead of the fused NEXT-3 pass")
     ap.add_argument("--dense", choices=["exact", "local"], default=None,
                     help="pruning-free baseline, PMC of every cell: 'exact' = exact GP (k = m, one bucket; "
                          "BASELINE c3), 'local' = the configured bucket-local GP (isolates the pruning)")
@@ -113,10 +115,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_traffic(kernel="k_pmc"):
+def load_traffic(cells_per_launch, kernel="k_pmc"):
+    """DRAM bytes per launch of the dominant kernel: the per-cell traffic of an
+    `ncu --set full` capture (profiles/traffic.json) times the cells one bench launch
+    processes (k_pmc is one launch over all leaves)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(kernel)
+        return json.load(open(p))[kernel]["dram_bytes_per_cell"] * cells_per_launch
     except Exception:
         return None
 
@@ -209,6 +214,8 @@ def run_ours(args):
     y = torch.from_numpy(np.array(w.y)).to(dev)
     ncell = int(np.prod(cfg.cells))
     field = torch.empty(ncell, dtype=torch.float32, device=dev)
+    multi_fields = (torch.empty((len(w.thetas), ncell), dtype=torch.float32, device=dev)
+                    if len(w.thetas) > 1 else None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     slab = dict(slab_rank=rank, slab_count=world, slab_level=3) if world > 1 else {}
     if args.dense:
@@ -235,6 +242,19 @@ def run_ours(args):
         leaves = 0
         mc_ms = 0.0
         p2 = 0
+        if len(w.thetas) > 1 and not args.dense and not args.separate_iso:
+            # NEXT-3: all isovalues in one fused leaf pass (one posterior, one sample stream)
+            fields_out = multi_fields
+            _, nl, nu = ctx.run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed,
+                                            0, fields=fields_out)
+            st = ctx.stats()
+            if world > 1:
+                for t in range(len(w.thetas)):
+                    gather_field(fields_out[t], cfg.cells, 3)
+            if host is not None and rank == 0:
+                host[2].copy_(fields_out.reshape(-1)[: host[2].numel()], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            return int(nu), st["mc_ms"], st["pmc_phase2_samples"]
         for it, th in enumerate(w.thetas):
             if args.dense:
                 ctx.pmc_cells(dense_cells, th, cfg.n_samples, cfg.mc_seed, it, out=dense_lcp)
@@ -305,7 +325,8 @@ def run_ours(args):
     if not args.no_e2e:
         Xh = torch.from_numpy(np.array(w.X)).pin_memory().numpy()
         yh = torch.from_numpy(np.array(w.y)).pin_memory().numpy()
-        fh = torch.empty(ncell, dtype=torch.float32).pin_memory()
+        fh = torch.empty(ncell * (len(w.thetas) if multi_fields is not None and not args.separate_iso else 1),
+                         dtype=torch.float32).pin_memory()
         host = (Xh, yh, fh)
         step(host)
         barrier()
@@ -320,7 +341,9 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": cells_per_step / float(te[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes),
-               "d2h_bytes_per_step": int(fh.numel() * 4 * len(w.thetas)), "seconds_per_step": float(te[0])}
+               "d2h_bytes_per_step": int(fh.numel() * 4 * (1 if fh.numel() > ncell or len(w.thetas) == 1
+                                                             else len(w.thetas))),
+               "seconds_per_step": float(te[0])}
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -331,7 +354,7 @@ def run_ours(args):
     p2_step = float(lv[2]) / args.steps
     ops_step = samples_step * OPS_PHASE1 + p2_step * OPS_PHASE2
     achieved = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
-    traffic = load_traffic()
+    traffic = load_traffic(leaves_step / max(world, 1) / max(len(w.thetas) if args.dense or args.separate_iso else 1, 1))
     roofline = {"bound": "alu", "kernel": "k_pmc", "achieved": achieved, "peak": peak,
                 "unit": "Tlane-op/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "ops_per_sample": ops_step / samples_step if samples_step else None,
@@ -353,7 +376,9 @@ def run_ours(args):
            "vs_baseline": None, "dtype": "f64/f32", "data": "synthetic",
            "config": {"workload": workload_desc(cfg, w.thetas) + (
                           f" | DENSE baseline ({args.dense} GP), every cell" if args.dense else ""),
-                      "mode": f"dense-{args.dense}" if args.dense else "octree-pruned", "extreme_iters": args.extreme, "cells": ncell, "m": cfg.m, "k": k,
+                      "mode": f"dense-{args.dense}" if args.dense else "octree-pruned",
+                      "isovalue_pass": ("fused multi-isovalue leaf pass (NEXT-3)" if len(w.thetas) > 1 and not
+                                        args.dense and not args.separate_iso else "one pass per isovalue"), "extreme_iters": args.extreme, "cells": ncell, "m": cfg.m, "k": k,
                       "n_samples": cfg.n_samples, "alpha": cfg.alpha, "max_depth": cfg.max_depth,
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                       "l2": "flushed between timed steps (256 MB write, outside the step events)"},

@@ -74,6 +74,9 @@ typedef struct {
     int32_t keep_records;  /* parity tap: keep per-node records of levels < keep_records (0 = none) */
     int32_t extreme_iters; /* NEXT-1 (R26): iterations of the continuous extreme search at nodes
                               coarser than h_full; 0 = lattice only */
+    int32_t brick_pass;    /* refine-time brick pass (vertex marginals + MC records of every
+                              level-(Lfull-2) frontier brick): 0 = on when supported and the
+                              records (208 B per cell) fit in free HBM, -1 = off */
 } lcp_opts_t;
 
 /* per evaluated octree node (Alg. 1) */

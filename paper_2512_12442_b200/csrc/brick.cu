@@ -290,7 +290,7 @@ lcp_status_t fused_setup(Ctx& c) {
     const char* v = std::getenv("LCP_FUSED");
     return v && v[0] == '0';
   }();
-  if (env_off || !fused_brick_supported(c)) return LCP_OK;
+  if (env_off || c.opts.brick_pass < 0 || !fused_brick_supported(c)) return LCP_OK;
   const int64_t ncodes = (int64_t)1 << (3 * c.g.lfull);
   const int64_t nbr = (int64_t)1 << (3 * (c.g.lfull - 2));
   const size_t need = sizeof(CellRec) * (size_t)ncodes;

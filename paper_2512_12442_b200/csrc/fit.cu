@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     A = vv + k;
     Li = A + tri;
   } else {
-    A = gscratch + (int64_t)b * 2 * tri;
+    A = gscratch + (int64_t)b * (tri + (int64_t)k * (k + 1));
     Li = A + tri;
   }
   const int32_t* Sb = S + (int64_t)b * k;
@@ -319,33 +319,38 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     if (tid == 0) atomicOr(derr, DERR_FACTOR);
     return;
   }
-  // L^-1: column j solves L x = e_j by forward substitution (independent per column)
-  for (int j = tid; j < k; j += bd) {
-    double* Lc = Li + tri_col(j, k) - j;
-    Lc[j] = 1.0 / A[tri_col(j, k)];
-    for (int i = j + 1; i < k; ++i) {
-      double s0 = 0.0, s1 = 0.0;
-      int p = j;
-      for (; p + 1 < i; p += 2) {
-        s0 = fma(A[tri_col(p, k) + i - p], Lc[p], s0);
-        s1 = fma(A[tri_col(p + 1, k) + i - p - 1], Lc[p + 1], s1);
-      }
-      if (p < i) s0 = fma(A[tri_col(p, k) + i - p], Lc[p], s0);
-      Lc[i] = -(s0 + s1) / A[tri_col(i, k)];
+  // L^-1 = X by a right-looking sweep on a dense row-major X (row stride k + 1):
+  // X starts as I; at step p row p is final once divided by L_pp, then every
+  // later row subtracts L_ip X[p][:] (warp per row, lanes over columns j <= p)
+  const int ldx = k + 1;
+  for (int64_t e = tid; e < (int64_t)k * ldx; e += bd) Li[e] = 0.0;
+  __syncthreads();
+  for (int j = tid; j < k; j += bd) Li[(int64_t)j * ldx + j] = 1.0;
+  for (int p = 0; p < k; ++p) {
+    __syncthreads();
+    const double lpp = A[tri_col(p, k)];
+    double* xp = Li + (int64_t)p * ldx;
+    for (int j = tid; j <= p; j += bd) xp[j] = xp[j] / lpp;
+    __syncthreads();
+    const double* colp = A + tri_col(p, k) - p;
+    for (int i = p + 1 + wid; i < k; i += nw) {
+      const double lip = colp[i];
+      double* xi = Li + (int64_t)i * ldx;
+      for (int j = lane; j <= p; j += 32) xi[j] = fma(-lip, xp[j], xi[j]);
     }
   }
   __syncthreads();
   // alpha = L^-T (L^-1 r)
   for (int i = tid; i < k; i += bd) {
+    const double* xi = Li + (int64_t)i * ldx;
     double s = 0.0;
-    for (int j = 0; j <= i; ++j) s = fma(Li[tri_col(j, k) + i - j], rr[j], s);
+    for (int j = 0; j <= i; ++j) s = fma(xi[j], rr[j], s);
     vv[i] = s;
   }
   __syncthreads();
   for (int j = tid; j < k; j += bd) {
-    const double* Lc = Li + tri_col(j, k) - j;
     double s = 0.0;
-    for (int i = j; i < k; ++i) s = fma(Lc[i], vv[i], s);
+    for (int i = j; i < k; ++i) s = fma(Li[(int64_t)i * ldx + j], vv[i], s);
     out[LA + j] = s;
   }
   for (int64_t e = tid; e < LA; e += bd) {
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     while ((int64_t)rt * (rt + 1) > blk) --rt;
     const int js = (int)(blk - (int64_t)rt * (rt + 1));
     const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
-    out[e] = (i < k && j <= i) ? Li[tri_col(j, k) + i - j] : 0.0;
+    out[e] = (i < k && j <= i) ? Li[(int64_t)i * ldx + j] : 0.0;
   }
 }
 
@@ -699,12 +704,12 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     CK(cudaGetLastError());
   } else {
     size_t head = sizeof(double) * 5 * (size_t)k;
-    size_t full = head + sizeof(double) * 2 * (size_t)tri;
-    int use_smem = full <= 200 * 1024;
+    size_t full = head + sizeof(double) * ((size_t)tri + (size_t)k * (k + 1));
+    int use_smem = full <= 220 * 1024;
     size_t smem = use_smem ? full : head;
     double* gs = nullptr;
     if (!use_smem) {
-      CK(c.fscratch.ensure(sizeof(double) * 2 * (size_t)tri * nbk));
+      CK(c.fscratch.ensure(sizeof(double) * ((size_t)tri + (size_t)k * (k + 1)) * nbk));
       gs = c.fscratch.as<double>();
     }
     CK(cudaFuncSetAttribute(k_bucket_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

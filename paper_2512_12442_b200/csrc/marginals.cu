@@ -481,9 +481,21 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
   size_t smem;
   plan_tile(c, staged, warps, smem);
   if (warps == 0) return cudaErrorInvalidConfiguration;
+  int tile = std::min(8 * warps * 8, TILE_MAX);
+  if (n_dev == nullptr && n < 8 * (int64_t)c.g.nbuckets && c.g.nbuckets > 1) {
+    // sparse items (few per bucket, e.g. the observation marginals of a fine bucket
+    // grid): staging a whole bucket block per item would dominate, so L^-1 is read
+    // straight from global memory by small CTAs (2 warps, 16 items each)
+    const int64_t k = c.k;
+    const int64_t ks = k + ((4 - k % 16) + 16) % 16;
+    const size_t per_warp = sizeof(double) * (8 * ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24);
+    staged = 0;
+    warps = 2;
+    smem = sizeof(double) * (4 * k + 1) + warps * per_warp;
+    tile = 16;
+  }
   a.staged = staged;
   cudaFuncSetAttribute(k_marginals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int tile = std::min(8 * warps * 8, TILE_MAX);
   unsigned grid = (unsigned)((n + tile - 1) / tile);
   k_marginals<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
                                                     out_mu, out_sd, write_var, c.vcache.as<double2>(),

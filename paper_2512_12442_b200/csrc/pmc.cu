@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
           int64_t out_stride, float* __restrict__ out, unsigned long long* __restrict__ n_phase2) {
   constexpr int ILP = (T <= 4) ? PMC_ILP : 1;
   // queue, slot-major: (lo4..lo7), (max y0..3, min y0..3, s, -)
-  __shared__ float4 sq[PMC_WARPS][QROWS][2];
+  __shared__ float4 sq[PMC_WARPS][2][QROWS];   // SoA: 16-B stores of consecutive slots are contiguous
   __shared__ unsigned int s_p2;
   if (threadIdx.x == 0) s_p2 = 0;
   __syncthreads();
@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   int qn = 0;   // warp-uniform queue length
   unsigned p2 = 0;
   float4* qv = &sq[wid][0][0];
+  float4* qw = &sq[wid][1][0];
   // L' as FFMA2 operands: corner pairs (0,1) (2,3) (4,5) (6,7) per normal d
   f2_t P01 = pk(L[0], L[1]), P23[3], P45[4], P67[4];
 #pragma unroll
@@ -400,22 +401,22 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     const int na = __popc(ma);
     const int sa = pa ? qn + __popc(ma & lt) : QCAP + lane;
     const int sb = pb ? qn + na + __popc(mb & lt) : QCAP + lane;
-    qv[2 * sa] = a0;
-    qv[2 * sa + 1] = a1;
-    qv[2 * sb] = b0;
-    qv[2 * sb + 1] = b1;
+    qv[sa] = a0;
+    qw[sa] = a1;
+    qv[sb] = b0;
+    qw[sb] = b1;
     qn += na + __popc(mb);
   };
   auto push = [&](bool pend, const float4& st0, const float4& st1) {
     const unsigned pm = __ballot_sync(0xffffffffu, pend);
     const int slot = pend ? qn + __popc(pm & ((1u << lane) - 1u)) : QCAP + lane;
-    qv[2 * slot] = st0;
-    qv[2 * slot + 1] = st1;
+    qv[slot] = st0;
+    qw[slot] = st1;
     qn += __popc(pm);
   };
   auto phase2 = [&](int slot, bool act) {
     if (act) {
-      const float4 va = qv[2 * slot], vb = qv[2 * slot + 1];
+      const float4 va = qv[slot], vb = qw[slot];
       const uint32_t s = __float_as_uint(vb.z);
       uint32_t r4, r5, r6, r7;
       philox4x32_10(2u * s + 1u, c1, c2, iso, K, r4, r5, r6, r7);

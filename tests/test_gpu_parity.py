@@ -520,8 +520,10 @@ def test_multi_iso_c4_full_size_sampled(dev):
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_brick_pass_records_equal_leaf_posterior_path(name, dev):
     # the refine-time brick pass (vertex marginals + MC records of every frontier brick)
-    # feeds the leaf pass; a list with one pruned cell takes the per-leaf posterior
-    # path instead.  Both must give bit-identical LCPs on the common leaves.
+    # feeds the leaf pass; with it switched off (opts.brick_pass = -1) the level-(Lfull-2)
+    # marginals come from k_marginals and the leaves take the per-leaf posterior path.
+    # Same node decisions, and bit-identical LCPs on the leaves.
+    from paper_2512_12442_b200 import Context, config_args
     w, ctx, M = _ctx(name, dev, keep_records=False)
     cfg = w.cfg
     th = w.thetas[0]
@@ -529,14 +531,42 @@ def test_brick_pass_records_equal_leaf_posterior_path(name, dev):
     st = ctx.stats()
     assert st["fused"] == 1 and st["pmc_used_records"] == 1 and st["brick_pass_ms"] > 0, st
     leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).clone()
-    allc = torch.arange(int(np.prod(cfg.cells)), device=dev, dtype=torch.int64)
-    lcp_all = ctx.pmc_cells(allc, th, cfg.n_samples, cfg.mc_seed)
-    if len(leaves) < len(allc):
-        assert ctx.stats()["pmc_used_records"] == 0
-    assert torch.equal(lcp_all[leaves], field[leaves])
+    kernel, grid, k, b, hf = config_args(cfg)
+    off = Context(0).fit_local(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(np.array(w.y)).to(dev),
+                               kernel, k, grid, bucket_log2=b, h_full=hf, brick_pass=-1)
+    field2, n2 = off.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    st2 = off.stats()
+    assert st2["fused"] == 0 and st2["pmc_used_records"] == 0, st2
+    leaves2 = off.octree_refine(th, cfg.alpha, cfg.max_depth)
+    assert n == n2 and torch.equal(leaves, leaves2)
+    assert torch.equal(field, field2)
     # and the records agree with the oracle on a sample of leaves
     lv = leaves.cpu().numpy()
     sel = np.random.default_rng(2).choice(len(lv), 200, replace=False)
     lcp_o = M.pmc_cells(lv[sel], th, cfg.n_samples, cfg.mc_seed)
     frac, mean, mx = lcp_parity(field.cpu().numpy()[lv[sel]], lcp_o, cfg.n_samples)
     assert frac >= 0.99 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_brick_pass_multi_iso_and_shallow_depth(dev):
+    # multi-isovalue refines share the brick records (bricks are done once); a refine
+    # whose max_depth stops above Lfull - 2 never reaches the brick level, so its
+    # leaves (whole nodes) take the per-leaf posterior path -- both against the oracle
+    w, ctx, M = _ctx("t2", dev, keep_records=False)
+    cfg = w.cfg
+    th = [w.thetas[0] - 0.2, w.thetas[0], w.thetas[0] + 0.25]
+    fields, nl, nu = ctx.run_field_multi(th, cfg.alpha, cfg.max_depth, 800, 5, 1)
+    cells, mask = ctx.union_cells()
+    assert ctx.stats()["pmc_used_records"] == 1
+    sel = np.linspace(0, nu - 1, 400).astype(int)
+    c_np, m_np = cells.cpu().numpy()[sel], mask.cpu().numpy()[sel].astype(np.uint32)
+    lcp_o = M.pmc_cells_multi(c_np, th, 800, 5, 1, mask=m_np)
+    F = fields.cpu().numpy()
+    for t in range(3):
+        frac, mean, mx = lcp_parity(F[t][c_np], lcp_o[t], 800)
+        assert frac >= 0.999 and mean <= 1e-4, (t, frac, mean, mx)
+    lf = ctx.info()["lfull"]
+    shallow = max(0, lf - 3)
+    leaves = ctx.octree_refine(th[1], cfg.alpha, shallow)
+    _, leaves_o = M.octree(th[1], cfg.alpha, shallow)
+    np.testing.assert_array_equal(np.sort(leaves.cpu().numpy()), leaves_o)

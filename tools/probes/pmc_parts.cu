@@ -113,6 +113,55 @@ __global__ void __launch_bounds__(256, 2) k_ws(const float* __restrict__ Lg, uin
   if (lane == 0) out[1 + cell % 1024] = acc;
 }
 
+// I: one warp per CTA, so the cell index (blockIdx.x) and its L, m, B are
+// warp-uniform: the compiler may keep them in uniform registers (UR operands of
+// FFMA / FFMA2), freeing vector-register bandwidth and capacity.
+__global__ void __launch_bounds__(32) k_uniform(const float* __restrict__ Lcells, uint32_t N, Keys K,
+                                                uint32_t* __restrict__ out) {
+  const int lane = threadIdx.x;
+  const uint32_t cell = blockIdx.x;
+  const float* Lg = Lcells + 48 * (cell & 1023);
+  float L[36], m[8], B[4];
+#pragma unroll
+  for (int q = 0; q < 36; ++q) L[q] = Lg[q];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) m[c] = Lg[36 + c];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) B[c] = Lg[44 + c];
+  uint32_t acc = 0;
+  auto one = [&](uint32_t s) {
+    uint32_t r[4];
+    philox(2u * s, cell, 0u, 0u, K, r);
+    float z[4];
+    bm(r[0], r[1], z[0], z[1]);
+    bm(r[2], r[3], z[2], z[3]);
+    float yp[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float y = m[c];
+#pragma unroll
+      for (int d = 0; d < 4 && d <= c; ++d) y = fmaf(L[c * (c + 1) / 2 + d], z[d], y);
+      yp[c] = y;
+    }
+    const float mx03 = fmaxf(fmaxf(yp[0], yp[1]), fmaxf(yp[2], yp[3]));
+    const float mn03 = fminf(fminf(yp[0], yp[1]), fminf(yp[2], yp[3]));
+    float hi_max = mx03, lo_min = mn03, lo_max = mx03, hi_min = mn03;
+#pragma unroll
+    for (int c = 4; c < 8; ++c) {
+      const float lo = yp[c] - B[c - 4], hi = yp[c] + B[c - 4];
+      hi_max = fmaxf(hi_max, hi); lo_min = fminf(lo_min, lo);
+      lo_max = fmaxf(lo_max, lo); hi_min = fminf(hi_min, hi);
+    }
+    const bool cross = lo_max >= 0.0f && hi_min <= 0.0f;
+    const bool decided = hi_max < 0.0f || lo_min > 0.0f || cross;
+    acc += cross ? 1u : 0u;
+    acc += decided ? 0u : 65536u;
+  };
+  for (uint32_t b = 0; b < N; b += 64) { one(b + lane); one(b + 32 + lane); }
+  if (acc == 0x12345) out[0] = acc;
+  if (lane == 0) out[1 + cell % 1024] = acc;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 2) k_part(const float* __restrict__ Lg, uint32_t N, Keys K,
                                                  uint32_t* __restrict__ out) {
@@ -211,6 +260,22 @@ int main() {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const char* names[7] = {"A philox", "B +box-muller", "C +Lz+decision", "D C with ILP2",
                           "E D, hash not philox", "F D, no box-muller", "G D software-pipelined"};
+  {
+    float* dLc;
+    cudaMalloc(&dLc, sizeof(float) * 48 * 1024);
+    float hc[48 * 1024];
+    for (int c = 0; c < 1024; ++c) for (int q = 0; q < 48; ++q) hc[48 * c + q] = hL[q] * (1.0f + 1e-3f * (c % 7));
+    cudaMemcpy(dLc, hc, sizeof hc, cudaMemcpyHostToDevice);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      k_uniform<<<cells, 32>>>(dLc, N, K, dout);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1);
+      double sps = (double)cells * N / (ms * 1e-3);
+      if (rep) printf("I warp-per-CTA uniform L %8.3f ms  %.3e samples/s  %.1f SMSP-cycles per warp-step\n", ms, sps,
+                      148.0 * 4 * (clk_mhz * 1e6) / (sps / 32));
+    }
+  }
   for (int rep = 0; rep < 2; ++rep)
     for (int ilp = 1; ilp <= 2; ++ilp) {
       // warp-specialised: 4 cells per block of 8 warps -> half the blocks' cells per launch
