@@ -149,10 +149,15 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         KV[(int64_t)j * VSTR + v] = val;
       }
       __syncthreads();
-      if (tid < NVP) {
+      {
+        // mu_v = m0 + sum_j K[j][v] alpha_j: 4 threads per vertex column (rows j = part
+        // mod 4, conflict-free), combined as ((s0 + s1) + (s2 + s3))
+        const int v = tid >> 2, part = tid & 3;
         double s = 0.0;
-        for (int j = 0; j < k; ++j) s = fma(KV[(int64_t)j * VSTR + tid], sAlpha[j], s);
-        sMu[tid] = a.kp.m0 + s;
+        for (int j = part; j < k; j += 4) s = fma(KV[(int64_t)j * VSTR + v], sAlpha[j], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (part == 0) sMu[v] = a.kp.m0 + s;
       }
       // phase 2: V = L^-1 K with DMMA; warp = (row set rs, column block cb)
       const int rs = wid >> 2, cb = wid & 3;
@@ -163,10 +168,13 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
       const int lr = lane >> 2, lc = lane & 3;
+      // row tiles rt(t) zig-zag over the 4 row sets so that every warp gets the same
+      // triangular work (rs = 0: 0, 7, 8, 15; rs = 3: 3, 4, 11, 12)
+      auto rtile = [&](int t) { return (t & 1) ? (3 - rs) + 4 * t : rs + 4 * t; };
       int last_rt = -1;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
-        if (rs + 4 * t < nrt) last_rt = rs + 4 * t;
+        if (rtile(t) < nrt) last_rt = max(last_rt, rtile(t));
       const int jend = last_rt < 0 ? 0 : min(KP, 8 * last_rt + 8);
       for (int j = 0; j < jend; j += 4) {
         const int jj = j + lc;
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         for (int u = 0; u < 4; ++u) bf[u] = KV[(int64_t)jj * VSTR + 32 * cb + 8 * u + lr];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const int rt = rs + 4 * t;
+          const int rt = rtile(t);
           if (rt >= nrt || 8 * rt + 7 < j) continue;   // warp-uniform: zero block of L^-1
           const double af = sLA[la_block(rt, j >> 2) + lane];
 #pragma unroll
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       __syncthreads();   // every warp has read K
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        const int rt = rs + 4 * t;
+        const int rt = rtile(t);
         if (rt >= nrt) continue;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -194,25 +202,32 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         }
       }
       __syncthreads();
-      if (FUSED && tid < NVB) {
+      if (FUSED) {
         // vertex marginals (R10) of the brick's vertices whose own bucket is b:
-        // var = k(v,v) - ||V_{:,v}||^2, cached as (mu, 1 / (sigma sqrt 2))
-        const int va = tid % (BK + 1), vb = (tid / (BK + 1)) % (BK + 1), vc = tid / ((BK + 1) * (BK + 1));
-        const int vi = i0 + va, vj = j0 + vb, vk = k0 + vc;
-        if (vi <= g.cells[0] && vj <= g.cells[1] && vk <= g.cells[2] &&
-            bucket_id(g, vbucket_axis(g, 0, vi), vbucket_axis(g, 1, vj), vbucket_axis(g, 2, vk)) == b) {
-          const int64_t vid = vertex_id(g, vi, vj, vk);
-          const uint32_t bit = 1u << (vid & 31);
-          if (!(atomicOr(&o.vmask[vid >> 5], bit) & bit)) {
-            double s2 = 0.0;
-            for (int j = 0; j < k; ++j) {
-              const double v = KV[(int64_t)j * VSTR + tid];
-              s2 = fma(v, v, s2);
+        // var = k(v,v) - ||V_{:,v}||^2 (4 threads per column as for mu), cached as
+        // (mu, 1 / (sigma sqrt 2))
+        const int v = tid >> 2, part = tid & 3;
+        double s2 = 0.0;
+        if (v < NVB)
+          for (int j = part; j < k; j += 4) {
+            const double x = KV[(int64_t)j * VSTR + v];
+            s2 = fma(x, x, s2);
+          }
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+        if (part == 0 && v < NVB) {
+          const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
+          const int vi = i0 + va, vj = j0 + vb, vk = k0 + vc;
+          if (vi <= g.cells[0] && vj <= g.cells[1] && vk <= g.cells[2] &&
+              bucket_id(g, vbucket_axis(g, 0, vi), vbucket_axis(g, 1, vj), vbucket_axis(g, 2, vk)) == b) {
+            const int64_t vid = vertex_id(g, vi, vj, vk);
+            const uint32_t bit = 1u << (vid & 31);
+            if (!(atomicOr(&o.vmask[vid >> 5], bit) & bit)) {
+              const double var = a.kp.var - s2;
+              if (var < a.var_err) atomicOr(o.derr, DERR_NUMERIC);
+              const double vf = var > o.var_floor ? var : o.var_floor;
+              o.vcache[vid] = make_double2(sMu[v], 1.0 / (sqrt(vf) * SQRT2));
             }
-            const double var = a.kp.var - s2;
-            if (var < a.var_err) atomicOr(o.derr, DERR_NUMERIC);
-            const double vf = var > o.var_floor ? var : o.var_floor;
-            o.vcache[vid] = make_double2(sMu[tid], 1.0 / (sqrt(vf) * SQRT2));
           }
         }
       }

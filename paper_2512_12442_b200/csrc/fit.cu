@@ -235,11 +235,14 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g
 
 // a3: per-bucket factor.  Block layout in bdata: [L^-1 in the DMMA A-fragment
 // layout (la_size(k), common.cuh)] [alpha (k)] [x (k)] [y (k)] [z (k)].
+// USE_SMEM is a template parameter so that the factor and L^-1 live in pointers the
+// compiler knows to be shared (LDS/STS); a runtime choice makes them generic (LD/ST).
+template <bool USE_SMEM>
 __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, int k, const double* __restrict__ X,
                                                                 const double* __restrict__ yobs,
                                                                 const int32_t* __restrict__ S,
                                                                 double* __restrict__ bdata, int64_t bstride,
-                                                                double* __restrict__ gscratch, int use_smem,
+                                                                double* __restrict__ gscratch,
                                                                 int* __restrict__ derr) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
   double* vv = rr + k;
   double* A;
   double* Li;
-  if (use_smem) {
+  if (USE_SMEM) {
     A = vv + k;
     Li = A + tri;
   } else {
@@ -306,10 +309,23 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
       double piv = s_piv;
       for (int i = j + 1 + tid; i < k; i += bd) colj[i] = colj[i] / piv;
       __syncthreads();
-      for (int l = j + 1 + wid; l < k; l += nw) {
-        double* coll = A + tri_col(l, k) - l;
-        double ljl = colj[l];
-        for (int i = l + lane; i < k; i += 32) coll[i] = fma(-colj[i], ljl, coll[i]);
+      // trailing update, 4 columns per warp pass (colj[i] shared, 4 independent
+      // load-FMA-store chains per lane)
+      for (int l0 = j + 1 + 4 * wid; l0 < k; l0 += 4 * nw) {
+        double lj[4];
+        double* cl[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int l = min(l0 + c, k - 1);
+          lj[c] = colj[l];
+          cl[c] = A + tri_col(l, k) - l;
+        }
+        for (int i = l0 + lane; i < k; i += 32) {
+          const double ci = colj[i];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (l0 + c <= i) cl[c][i] = fma(-ci, lj[c], cl[c][i]);
+        }
       }
     }
     __syncthreads();
@@ -333,10 +349,22 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
     for (int j = tid; j <= p; j += bd) xp[j] = xp[j] / lpp;
     __syncthreads();
     const double* colp = A + tri_col(p, k) - p;
-    for (int i = p + 1 + wid; i < k; i += nw) {
-      const double lip = colp[i];
-      double* xi = Li + (int64_t)i * ldx;
-      for (int j = lane; j <= p; j += 32) xi[j] = fma(-lip, xp[j], xi[j]);
+    // 4 rows per warp pass (xp[j] shared, 4 independent chains per lane)
+    for (int i0 = p + 1 + 4 * wid; i0 < k; i0 += 4 * nw) {
+      double li[4];
+      double* xr[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = min(i0 + r, k - 1);
+        li[r] = colp[i];
+        xr[r] = Li + (int64_t)i * ldx;
+      }
+      for (int j = lane; j <= p; j += 32) {
+        const double xpj = xp[j];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (i0 + r < k) xr[r][j] = fma(-li[r], xpj, xr[r][j]);
+      }
     }
   }
   __syncthreads();
@@ -712,10 +740,17 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       CK(c.fscratch.ensure(sizeof(double) * ((size_t)tri + (size_t)k * (k + 1)) * nbk));
       gs = c.fscratch.as<double>();
     }
-    CK(cudaFuncSetAttribute(k_bucket_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_bucket_factor<<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
-                                                           c.bdata.as<double>(), c.bstride, gs, use_smem,
-                                                           c.derr.as<int>());
+    if (use_smem) {
+      CK(cudaFuncSetAttribute(k_bucket_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_bucket_factor<true><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                                   c.bdata.as<double>(), c.bstride, gs,
+                                                                   c.derr.as<int>());
+    } else {
+      CK(cudaFuncSetAttribute(k_bucket_factor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_bucket_factor<false><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                                    c.bdata.as<double>(), c.bstride, gs,
+                                                                    c.derr.as<int>());
+    }
     ++c.n_launch;
     CK(cudaGetLastError());
   }

@@ -159,7 +159,7 @@ __device__ __forceinline__ int item_bucket(const TileArgs& a, int mode, int64_t 
 // and share one staging of the bucket block.
 constexpr int TILE_MAX = 2048;
 
-template <typename Body>
+template <int STAGED, typename Body>
 __device__ __forceinline__ void tile_loop(const TileArgs& a, int64_t t0, int64_t t1, double* smem,
                                           const int32_t* __restrict__ runb, Body body) {
   __shared__ int s_starts[TILE_MAX + 1];
@@ -201,13 +201,14 @@ __device__ __forceinline__ void tile_loop(const TileArgs& a, int64_t t0, int64_t
     const int b = runb[q];
     if (b != staged_bucket) {
       const double* src = a.bdata + (int64_t)b * blk;
-      if (a.staged) stage_copy(smem, src, blk);
+      if (STAGED) stage_copy(smem, src, blk);
       else stage_copy(smem, src + a.la, 4 * (int64_t)a.k);
       staged_bucket = b;
     }
     __syncthreads();
-    const double* Linv = a.staged ? smem : a.bdata + (int64_t)b * blk;
-    const double* tail = a.staged ? smem + a.la : smem;
+    // STAGED is a template parameter so that Linv is a known shared (or global) pointer
+    const double* Linv = STAGED ? smem : a.bdata + (int64_t)b * blk;
+    const double* tail = STAGED ? smem + a.la : smem;
     body(b, q, qe, Linv, tail, tail + a.k);
     __syncthreads();
   }
@@ -217,6 +218,7 @@ __device__ __forceinline__ void tile_loop(const TileArgs& a, int64_t t0, int64_t
 // items_sorted[q]: vertex id (Q_VERTEX), observation index (Q_OBS) or point
 // index (Q_POINT); bkt_sorted[q]: its bucket.  Output indexed by the item
 // (vertex cache slot, observation, point).
+template <int STAGED>
 __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const int64_t* __restrict__ items,
                                                    const int32_t* __restrict__ bkt_sorted, int64_t n,
                                                    const int64_t* __restrict__ n_dev, int tile,
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
   int64_t t1 = min(n, t0 + tile);
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.k;
-  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  int64_t head = STAGED ? a.bstride : 4 * (int64_t)k;
   head = (head + 1) & ~1ll;
   const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
   double* wbuf = smem + head + wid * per_warp;
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
   double* sV = wbuf + 8 * a.ks;
   double* sQ = wbuf + per_warp - 24;
   const Geom& g = a.g;
-  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
+  tile_loop<STAGED>(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
                                               const double* alpha, const double* Xs) {
     for (int64_t base = q0 + 8 * wid; base < q1; base += 8 * warps) {
       int nq = (int)min((int64_t)8, q1 - base);
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(512) k_marginals(TileArgs a, int mode, const i
 
 // ------------------------------------------------------------------- a7
 // post[q] (44 doubles): mu[8] then Sigma packed lower (pair p = c(c+1)/2 + d).
+template <int STAGED>
 __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_t* __restrict__ cells,
                                                         const int64_t* __restrict__ perm,
                                                         const int32_t* __restrict__ bkt_sorted, int64_t n,
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
   int64_t t1 = min(n, t0 + tile);
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.k;
-  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  int64_t head = STAGED ? a.bstride : 4 * (int64_t)k;
   head = (head + 1) & ~1ll;
   const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
   double* wbuf = smem + head + wid * per_warp;
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
   double* sV = wbuf + 8 * a.ks;
   double* sQ = wbuf + per_warp - 24;
   const Geom& g = a.g;
-  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
+  tile_loop<STAGED>(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* Linv,
                                               const double* alpha, const double* Xs) {
     for (int64_t q = q0 + wid; q < q1; q += warps) {
       int64_t slot = perm ? perm[q] : q;
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(512) k_cell_posterior(TileArgs a, const int64_
 // the solve V = L^-1 K and Sigma = K_cc - V^T V in FP32 (CUDA-core FFMA) from the
 // FP64-built bucket factor (cast on load); mu and Sigma are stored widened to FP64
 // and the 8x8 Cholesky stays FP64 (k_chol8).  Warp per cell, k <= 128.
+template <int STAGED>
 __global__ void __launch_bounds__(512) k_cell_posterior_f32(TileArgs a, const int64_t* __restrict__ cells,
                                                             const int64_t* __restrict__ perm,
                                                             const int32_t* __restrict__ bkt_sorted, int64_t n,
@@ -348,12 +352,12 @@ __global__ void __launch_bounds__(512) k_cell_posterior_f32(TileArgs a, const in
   int64_t t1 = min(n, t0 + tile);
   const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = a.k;
-  int64_t head = a.staged ? a.bstride : 4 * (int64_t)k;
+  int64_t head = STAGED ? a.bstride : 4 * (int64_t)k;
   head = (head + 1) & ~1ll;
   const int64_t per_warp = 8 * (int64_t)a.ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24;
   float* sKf = reinterpret_cast<float*>(smem + head + wid * per_warp);   // [j][8] floats
   const Geom& g = a.g;
-  tile_loop(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* LA,
+  tile_loop<STAGED>(a, t0, t1, smem, bkt_sorted, [&](int b, int64_t q0, int64_t q1, const double* LA,
                                               const double* alpha, const double* Xs) {
     for (int64_t q = q0 + wid; q < q1; q += warps) {
       int64_t slot = perm ? perm[q] : q;
@@ -495,9 +499,10 @@ cudaError_t launch_marginals(Ctx& c, int mode, const int64_t* items_sorted, cons
     tile = 16;
   }
   a.staged = staged;
-  cudaFuncSetAttribute(k_marginals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = staged ? k_marginals<1> : k_marginals<0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned grid = (unsigned)((n + tile - 1) / tile);
-  k_marginals<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
+  kern<<<grid, 32 * warps, smem, c.stream>>>(a, mode, items_sorted, bkt_sorted, n, n_dev, tile, points,
                                                     out_mu, out_sd, write_var, c.vcache.as<double2>(),
                                                     c.vstate.as<uint8_t>(), c.derr.as<int>());
   ++c.n_launch;
@@ -514,10 +519,11 @@ cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* p
     plan_tile(c, staged, warps, smem);
     if (warps == 0) return cudaErrorInvalidConfiguration;
     a.staged = staged;
-    cudaFuncSetAttribute(k_cell_posterior_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kf = staged ? k_cell_posterior_f32<1> : k_cell_posterior_f32<0>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int tile = warps * 16;
     unsigned grid = (unsigned)((n + tile - 1) / tile);
-    k_cell_posterior_f32<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
+    kf<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
                                                                c.derr.as<int>());
     ++c.n_launch;
     return cudaGetLastError();
@@ -529,10 +535,11 @@ cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* p
   plan_tile(c, staged, warps, smem);
   if (warps == 0) return cudaErrorInvalidConfiguration;
   a.staged = staged;
-  cudaFuncSetAttribute(k_cell_posterior, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kc = staged ? k_cell_posterior<1> : k_cell_posterior<0>;
+  cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int tile = warps * 16;
   unsigned grid = (unsigned)((n + tile - 1) / tile);
-  k_cell_posterior<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
+  kc<<<grid, 32 * warps, smem, c.stream>>>(a, cells, perm, bkt_sorted, n, tile, post,
                                                          c.derr.as<int>());
   ++c.n_launch;
   return cudaGetLastError();
