@@ -570,3 +570,33 @@ def test_brick_pass_multi_iso_and_shallow_depth(dev):
     leaves = ctx.octree_refine(th[1], cfg.alpha, shallow)
     _, leaves_o = M.octree(th[1], cfg.alpha, shallow)
     np.testing.assert_array_equal(np.sort(leaves.cpu().numpy()), leaves_o)
+
+
+def test_multi_iso_edges_and_errors(dev):
+    # empty leaf sets (isovalues far outside the field), host output buffers,
+    # the 16-isovalue limit and non-finite isovalues
+    from paper_2512_12442_b200 import LcpError
+    w, ctx, M = _ctx("t1", dev, keep_records=False)
+    cfg = w.cfg
+    ncell = int(np.prod(cfg.cells))
+    fields, nl, nu = ctx.run_field_multi([50.0, -50.0], cfg.alpha, cfg.max_depth, 300, 3)
+    assert nu == 0 and list(nl) == [0, 0] and torch.count_nonzero(fields) == 0
+    host = np.full((3, ncell), -1.0, np.float32)
+    th = [w.thetas[0], 50.0, w.thetas[0] + 0.1]
+    f_host, nl, nu = ctx.run_field_multi(th, cfg.alpha, cfg.max_depth, 300, 3, 0, fields=host)
+    f_dev, nl2, nu2 = ctx.run_field_multi(th, cfg.alpha, cfg.max_depth, 300, 3, 0)
+    assert nu == nu2 and list(nl) == list(nl2) and nl[1] == 0
+    np.testing.assert_array_equal(host, f_dev.cpu().numpy())
+    assert np.all(host[1] == 0)
+    with pytest.raises(LcpError):
+        ctx.run_field_multi(list(np.linspace(-1, 1, 17)), cfg.alpha, cfg.max_depth, 300, 3)
+    with pytest.raises(LcpError):
+        ctx.pmc_cells_multi(torch.arange(10, device=dev), [0.0, float("nan")], 100, 1)
+    # 16 isovalues (the largest instantiation) against the oracle on a few cells
+    th16 = list(np.linspace(-0.8, 0.8, 16))
+    cells = torch.from_numpy(random_cells("t1", 64, 9)).to(dev)
+    got = ctx.pmc_cells_multi(cells, th16, 700, 21, stream=4).cpu().numpy()
+    want = M.pmc_cells_multi(cells.cpu().numpy(), th16, 700, 21, 4)
+    for t in range(16):
+        frac, mean, mx = lcp_parity(got[t], want[t], 700)
+        assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
