@@ -10,6 +10,7 @@
 //      alpha = K_y^-1 (y_S - m0) (Eq. 1; jitter R15).
 //  a4  observation marginals (R10) via k_marginals.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -393,6 +394,229 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
   }
 }
 
+// a3, blocked (k <= 128): the same factor with 8x8 blocks on the FP64 tensor cores.
+// Dense row-major K_y in smem (row stride KP + 4 = 4 mod 8 doubles: the DMMA
+// fragment loads are bank-conflict free), padding rows/columns = identity.
+//   Cholesky, right-looking, panel J: (1) warp 0 factors the 8x8 diagonal block
+//   (lane r owns row r; shuffles) and its inverse T_J; (2) panel A_IJ <- A_IJ T_J^T;
+//   (3) trailing A_{I1,I2} -= A_{I1,J} A_{I2,J}^T -- 2 DMMA.8x8x4 per block.
+//   L^-1 = X in place, block row I: S_J = sum_{K=J}^{I-1} L_IK X_KJ (DMMA), then
+//   X_IJ = -T_I S_J, X_II = T_I.
+// 3 + 2 barriers per block (vs 5 per column unblocked).  Same jitter retry (R15).
+constexpr int FB = 8;                  // block size
+__device__ __forceinline__ void dmma_f(double a, double b, double& d0, double& d1) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams kp, int k,
+                                                                    const double* __restrict__ X,
+                                                                    const double* __restrict__ yobs,
+                                                                    const int32_t* __restrict__ S,
+                                                                    double* __restrict__ bdata, int64_t bstride,
+                                                                    int* __restrict__ derr) {
+  extern __shared__ double sm[];
+  __shared__ int s_ok;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = bd >> 5;
+  const int KP = (k + FB - 1) & ~(FB - 1), nb = KP / FB, ST = KP + 4;
+  const int64_t LA = la_size(k);
+  double* sx = sm;
+  double* sy = sx + KP;
+  double* sz = sy + KP;
+  double* rr = sz + KP;
+  double* vv = rr + KP;
+  double* sT = vv + KP;                  // nb blocks of 8 x 12 (stride 12: conflict-free)
+  double* A = sT + nb * FB * 12;         // KP x ST
+  const int lr = lane >> 2, lc = lane & 3;
+  const int32_t* Sb = S + (int64_t)b * k;
+  double* out = bdata + (int64_t)b * bstride;
+  for (int a = tid; a < k; a += bd) {
+    int64_t o = Sb[a];
+    sx[a] = X[3 * o];
+    sy[a] = X[3 * o + 1];
+    sz[a] = X[3 * o + 2];
+    rr[a] = yobs[o] - kp.m0;
+    out[LA + k + a] = sx[a];
+    out[LA + 2 * k + a] = sy[a];
+    out[LA + 3 * k + a] = sz[a];
+  }
+  auto Ab = [&](int I, int J) { return A + (int64_t)(FB * I) * ST + FB * J; };   // block (I, J)
+  bool ok = false;
+  for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
+    const double jit = attempt == 0 ? 0.0 : 1e-10 * kp.var * (attempt == 1 ? 1.0 : attempt == 2 ? 10.0 : 100.0);
+    __syncthreads();
+    for (int e = tid; e < KP * KP; e += bd) {
+      const int i = e / KP, j = e - i * KP;
+      if (j > i) continue;
+      double v;
+      if (i < k) {
+        const double r2 = kern_r2(kp, sx[i] - sx[j], sy[i] - sy[j], sz[i] - sz[j]);
+        v = kern_from_r2(kp, r2) + (i == j ? kp.nugget + jit : 0.0);
+      } else {
+        v = i == j ? 1.0 : 0.0;
+      }
+      A[(int64_t)i * ST + j] = v;
+    }
+    if (tid == 0) s_ok = 1;
+    __syncthreads();
+    for (int J = 0; J < nb; ++J) {
+      // (1) diagonal block: Cholesky + inverse by warp 0, lane r < 8 owns row r
+      if (wid == 0) {
+        double d[FB];
+        double* D = Ab(J, J);
+#pragma unroll
+        for (int c = 0; c < FB; ++c) d[c] = (lane < FB && c <= lane) ? D[lane * ST + c] : 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < FB; ++j) {
+          const double pj = __shfl_sync(0xffffffffu, d[j], j);
+          if (!(pj > 0.0)) bad = true;
+          const double piv = sqrt(pj);
+          if (lane == j) d[j] = piv;
+          else if (lane > j && lane < FB) d[j] = d[j] / piv;
+#pragma unroll
+          for (int c = j + 1; c < FB; ++c) {
+            const double lcj = __shfl_sync(0xffffffffu, d[j], c);
+            if (lane >= c && lane < FB) d[c] = fma(-d[j], lcj, d[c]);
+          }
+        }
+        if (lane < FB) {
+#pragma unroll
+          for (int c = 0; c < FB; ++c)
+            if (c <= lane) D[lane * ST + c] = d[c];
+        }
+        // T = L_JJ^-1, lane c < 8 solves column c: L t = e_c (rows p = c..7)
+        __syncwarp();
+        if (lane < FB) {
+          double t[FB];
+#pragma unroll
+          for (int p = 0; p < FB; ++p) {
+            double sacc = (p == lane) ? 1.0 : 0.0;
+#pragma unroll
+            for (int q = 0; q < p; ++q) sacc = fma(-D[p * ST + q], t[q], sacc);
+            t[p] = p < lane ? 0.0 : sacc / D[p * ST + p];
+          }
+          double* T = sT + J * FB * 12;
+#pragma unroll
+          for (int p = 0; p < FB; ++p) T[p * 12 + lane] = t[p];
+        }
+        if (bad && lane == 0) s_ok = 0;
+      }
+      __syncthreads();
+      if (!s_ok) break;
+      // (2) panel: A_IJ <- A_IJ T_J^T  (D[r][c] = sum_t A_IJ[r][t] T[c][t])
+      const double* T = sT + J * FB * 12;
+      for (int I = J + 1 + wid; I < nb; I += nw) {
+        double* P = Ab(I, J);
+        const double a0 = P[lr * ST + lc], a1 = P[lr * ST + 4 + lc];
+        const double b0 = T[lr * 12 + lc], b1 = T[lr * 12 + 4 + lc];
+        double d0 = 0.0, d1 = 0.0;
+        dmma_f(a0, b0, d0, d1);
+        dmma_f(a1, b1, d0, d1);
+        __syncwarp();
+        P[lr * ST + 2 * lc] = d0;
+        P[lr * ST + 2 * lc + 1] = d1;
+      }
+      __syncthreads();
+      // (3) trailing: A_{I1,I2} -= A_{I1,J} A_{I2,J}^T for J < I2 <= I1
+      {
+        const int m = nb - J - 1;
+        int idx = 0;
+        for (int i1 = 0; i1 < m; ++i1)
+          for (int i2 = 0; i2 <= i1; ++i2, ++idx) {
+            if ((idx % nw) != wid) continue;
+            const int I1 = J + 1 + i1, I2 = J + 1 + i2;
+            const double* P1 = Ab(I1, J);
+            const double* P2 = Ab(I2, J);
+            double* C = Ab(I1, I2);
+            double d0 = C[lr * ST + 2 * lc], d1 = C[lr * ST + 2 * lc + 1];
+            dmma_f(-P1[lr * ST + lc], P2[lr * ST + lc], d0, d1);
+            dmma_f(-P1[lr * ST + 4 + lc], P2[lr * ST + 4 + lc], d0, d1);
+            C[lr * ST + 2 * lc] = d0;
+            C[lr * ST + 2 * lc + 1] = d1;
+          }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    ok = s_ok != 0;
+  }
+  if (!ok) {
+    if (tid == 0) atomicOr(derr, DERR_FACTOR);
+    return;
+  }
+  // L^-1 in place, block row by block row
+  for (int I = 0; I < nb; ++I) {
+    // S_J = sum_{K=J}^{I-1} L_IK X_KJ for J < I (warp w: J = w, w + nw, ...)
+    // (nw = 8 warps, nb <= 16: at most two J per warp, held in s0 / s1)
+    double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0};
+    for (int J = wid, nj = 0; J < I; J += nw, ++nj) {
+      double d0 = 0.0, d1 = 0.0;
+      for (int K = J; K < I; ++K) {
+        const double* Lb = Ab(I, K);
+        const double* Xb = Ab(K, J);
+        // B[t][c] = X_KJ[t][c]: lane holds X_KJ[t0 + lc][lr]
+        dmma_f(Lb[lr * ST + lc], Xb[lc * ST + lr], d0, d1);
+        dmma_f(Lb[lr * ST + 4 + lc], Xb[(4 + lc) * ST + lr], d0, d1);
+      }
+      if (nj == 0) { s0[0] = d0; s0[1] = d1; } else { s1[0] = d0; s1[1] = d1; }
+    }
+    __syncthreads();   // row I of L is consumed
+    const double* T = sT + I * FB * 12;
+    for (int J = wid, nj = 0; J < I; J += nw, ++nj) {
+      double* Bk = Ab(I, J);
+      Bk[lr * ST + 2 * lc] = nj == 0 ? s0[0] : s1[0];
+      Bk[lr * ST + 2 * lc + 1] = nj == 0 ? s0[1] : s1[1];
+      __syncwarp();
+      double d0 = 0.0, d1 = 0.0;
+      dmma_f(-T[lr * 12 + lc], Bk[lc * ST + lr], d0, d1);
+      dmma_f(-T[lr * 12 + 4 + lc], Bk[(4 + lc) * ST + lr], d0, d1);
+      __syncwarp();
+      Bk[lr * ST + 2 * lc] = d0;
+      Bk[lr * ST + 2 * lc + 1] = d1;
+    }
+    if (wid == nw - 1) {
+      double* Dg = Ab(I, I);
+      for (int e = lane; e < FB * FB; e += 32) {   // full block: T's upper triangle is 0
+        const int r = e >> 3, c = e & 7;
+        Dg[r * ST + c] = T[r * 12 + c];
+      }
+    }
+    __syncthreads();
+  }
+  // alpha = L^-T (L^-1 r)
+  for (int i = tid; i < k; i += bd) {
+    const double* xi = A + (int64_t)i * ST;
+    double sacc = 0.0;
+    for (int j = 0; j <= i; ++j) sacc = fma(xi[j], rr[j], sacc);
+    vv[i] = sacc;
+  }
+  __syncthreads();
+  for (int j = tid; j < k; j += bd) {
+    double sacc = 0.0;
+    for (int i = j; i < k; ++i) sacc = fma(A[(int64_t)i * ST + j], vv[i], sacc);
+    out[LA + j] = sacc;
+  }
+  for (int64_t e = tid; e < LA; e += bd) {
+    const int64_t blk = e >> 5;
+    const int ln = (int)(e & 31);
+    int rt = (int)((sqrt(4.0 * (double)blk + 1.0) - 1.0) * 0.5);
+    while ((int64_t)(rt + 1) * (rt + 2) <= blk) ++rt;
+    while ((int64_t)rt * (rt + 1) > blk) --rt;
+    const int js = (int)(blk - (int64_t)rt * (rt + 1));
+    const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
+    out[e] = (i < k && j <= i) ? A[(int64_t)i * ST + j] : 0.0;
+  }
+}
+
+size_t bucket_factor_blk_smem(int k) {
+  const int KP = (k + FB - 1) & ~(FB - 1), nb = KP / FB;
+  return sizeof(double) * (5 * (size_t)KP + (size_t)nb * FB * 12 + (size_t)KP * (KP + 4));
+}
+
 // NEXT-2: SGPR bucket factor.  Eq. 1 restricted to the bucket's k nearest
 // inducing points S:  mu(x) = m0 + k_x^T W (mu_S - m0),
 //   Sigma = K - k^T C k,  C = W - W A_SS W,  W = (K_SS + jitter)^-1.
@@ -740,7 +964,16 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       CK(c.fscratch.ensure(sizeof(double) * ((size_t)tri + (size_t)k * (k + 1)) * nbk));
       gs = c.fscratch.as<double>();
     }
-    if (use_smem) {
+    static const bool blk_off = [] {
+      const char* v = std::getenv("LCP_FACTOR_BLOCKED");
+      return v && v[0] == '0';
+    }();
+    if (k <= 128 && FACT_THREADS == 256 && !blk_off) {   // nb <= 16 blocks over 8 warps
+      const size_t sb = bucket_factor_blk_smem(k);
+      CK(cudaFuncSetAttribute(k_bucket_factor_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+      k_bucket_factor_blk<<<nbk, FACT_THREADS, sb, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                               c.bdata.as<double>(), c.bstride, c.derr.as<int>());
+    } else if (use_smem) {
       CK(cudaFuncSetAttribute(k_bucket_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_bucket_factor<true><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
                                                                    c.bdata.as<double>(), c.bstride, gs,
