@@ -170,7 +170,7 @@ lcp_status_t lcp_run_field(lcp_ctx_t* ctx, double isovalue, double threshold, in
 /* NEXT-3 fused multi-isovalue leaf pass (the paper's isovalue sweep,
  * PAPER.md:346, :386; reading R27).  For n_iso <= 16 isovalues: the 8-corner
  * posterior and its 8x8 Cholesky once per cell, and ONE Philox sample stream
- * per cell -- counter word 3 = `stream` (R13) -- whose every sample is tested
+ * per cell -- counter word 1 = `stream` (R13) -- whose every sample is tested
  * against each isovalue (ties cross).  Row t therefore equals
  * lcp_pmc_cells(cells, isovalues[t], ..., iso_index = stream) up to the FP32
  * rounding of y - isovalue (R25).

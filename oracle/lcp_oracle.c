@@ -556,13 +556,14 @@ void orc_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) 
 /* uniform from the low 23 bits: u = (r mod 2^23 + 1/2) 2^-23 in [2^-24, 1 - 2^-24] (R13) */
 static double u23(uint32_t r) { return ((double)(r & 0x7FFFFFu) + 0.5) * (1.0 / 8388608.0); }
 
-/* counter = (2s + j, cell lo32, cell hi32, iso_index), key = (seed lo32, seed hi32);
- * Box-Muller pairs (u_a, u_b): R = sqrt(-2 ln u_a), (R cos 2 pi u_b, R sin 2 pi u_b). */
+/* counter = (cell lo32, iso_index, cell hi32, 2s + j), key = (seed lo32, seed hi32)
+ * (R13; the paper fixes no RNG); Box-Muller pairs (u_a, u_b):
+ * R = sqrt(-2 ln u_a), (R cos 2 pi u_b, R sin 2 pi u_b). */
 void orc_normals8(uint64_t seed, int64_t cell, uint32_t iso_index, int64_t s, double* z) {
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     for (int j = 0; j < 2; ++j) {
-        uint32_t ctr[4] = {(uint32_t)(2 * s + j), (uint32_t)(uint64_t)cell,
-                           (uint32_t)((uint64_t)cell >> 32), iso_index};
+        uint32_t ctr[4] = {(uint32_t)(uint64_t)cell, iso_index, (uint32_t)((uint64_t)cell >> 32),
+                           (uint32_t)(2 * s + j)};
         uint32_t r[4];
         orc_philox4x32_10(ctr, key, r);
         for (int p = 0; p < 2; ++p) {
@@ -627,7 +628,7 @@ int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double 
 
 /* ---------------------------------------------------------------- NEXT-3 --- */
 /* Fused multi-isovalue MC (the paper's isovalue sweep,
- * PAPER.md:346, :386): ONE sample stream per cell -- the counter word 3 is the
+ * PAPER.md:346, :386): ONE sample stream per cell -- the counter word 1 is the
  * caller's `stream` index instead of a per-isovalue index (R27) -- and, for every
  * sample, the crossing test of C11 (ties cross, R24) applied
  * to each of the T isovalues.  counts_out[t] is therefore exactly

@@ -88,7 +88,7 @@ int64_t orc_mc_count(const double* mu, const double* L, double theta, int64_t n_
 int orc_pmc_cells(const orc_model_t* M, const int64_t* cells, int64_t n, double theta,
                   int64_t n_samples, uint64_t seed, uint32_t iso_index, double* lcp_out);
 
-/* NEXT-3 (R27): fused multi-isovalue MC -- one sample stream (counter word 3 =
+/* NEXT-3 (R27): fused multi-isovalue MC -- one sample stream (counter word 1 =
  * stream), the C11 crossing test for each of T thetas.  counts_out[T]. */
 void orc_mc_count_multi(const double* mu, const double* L, const double* thetas, int32_t T,
                         int64_t n_samples, uint64_t seed, int64_t cell, uint32_t stream,

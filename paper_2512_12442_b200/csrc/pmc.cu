@@ -3,7 +3,7 @@
 //  a7  cell posterior (marginals.cu: k_cell_posterior), cells grouped by bucket
 //  a8  k_chol8 : 8x8 Cholesky of Sigma in FP64 with the PSD pivot clamp (R14)
 //      k_pmc   : warp per cell; lane l draws samples s = l, l+32, ...:
-//                Philox4x32-10 on counter (2s+j, cell lo, cell hi, iso), key =
+//                Philox4x32-10 on counter (cell lo, iso, cell hi, 2s+j), key =
 //                seed (R13); uniforms from the low 23 bits; Box-Muller; y = mu +
 //                L z in FP32; crossing = not all y < th and not all y > th
 //                (R5, R24).  LCP = count / N.
@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   // Same FP32 operations in the same order as the scalar chains y = fma(L'_cd, z_d, y).
   auto phase1 = [&](uint32_t s, float4& st0, float4& st1) -> bool {
     uint32_t r0, r1, r2, r3;
-    philox4x32_10(2u * s, c1, c2, iso, K, r0, r1, r2, r3);
+    // counter (cell lo, iso, cell hi, 2s + j) (R13): the sample word enters round 1
+    // only through an XOR, so rounds 1-3 need 2 varying IMAD.WIDE instead of 4
+    philox4x32_10(c1, iso, c2, 2u * s, K, r0, r1, r2, r3);
     const f2_t zA = box_muller2(r0, r1), zB = box_muller2(r2, r3);
     float z[4];
     upk(zA, z[0], z[1]);
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
       const float4 va = qv[slot], vb = qw[slot];
       const uint32_t s = __float_as_uint(vb.z);
       uint32_t r4, r5, r6, r7;
-      philox4x32_10(2u * s + 1u, c1, c2, iso, K, r4, r5, r6, r7);
+      philox4x32_10(c1, iso, c2, 2u * s + 1u, K, r4, r5, r6, r7);
       float z[8];
       upk(box_muller2(r4, r5), z[4], z[5]);
       upk(box_muller2(r6, r7), z[6], z[7]);

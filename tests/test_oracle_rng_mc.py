@@ -67,12 +67,12 @@ def test_philox_vs_curand_host(tmp_path):
 
 
 def test_normals_layout_and_uniform_map():
-    # counter = (2s + j, cell lo, cell hi, iso), key = (seed lo, seed hi); u from low 23 bits
+    # counter = (cell lo, iso, cell hi, 2s + j), key = (seed lo, seed hi); u from low 23 bits
     seed, cell, iso, s = 0x1234567890ABCDEF, (7 << 32) + 99, 2, 5
     z = O.normals8(seed, cell, iso, s)
     key = [seed & 0xFFFFFFFF, seed >> 32]
     for j in range(2):
-        r = O.philox4x32_10([2 * s + j, cell & 0xFFFFFFFF, cell >> 32, iso], key)
+        r = O.philox4x32_10([cell & 0xFFFFFFFF, iso, cell >> 32, 2 * s + j], key)
         u = [((int(x) & 0x7FFFFF) + 0.5) / 2 ** 23 for x in r]
         for p in range(2):
             R = math.sqrt(-2 * math.log(u[2 * p]))
