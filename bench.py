@@ -361,6 +361,12 @@ def run_ours(args):
                 "phase2_fraction": p2_step / samples_step if samples_step else None,
                 "samples_per_s": samples_step / max(world, 1) / mc_s if mc_s > 0 else None,
                 "mc_share_of_step": mc_s / (ms_step / 1000.0),
+                # plain FP32 FLOP/s of the same kernel (FMA = 2): per sample
+                # 26 FMA of the partial L'z, 4 of the bounds, 2 x (angle FMA + 2 products + uniform
+                # add) of Box-Muller = 70 flop; per phase-2 sample 10 FMA + 4 adds + 10 = 34 flop
+                "fp32_tflops": ((samples_step * 70 + p2_step * 34) / max(world, 1) / mc_s / 1e12
+                                if mc_s > 0 else None),
+                "fp32_peak_tflops": 74.4,
                 "peak_note": "148 SMs x 128 lanes x 1.965 GHz issue slots (guide unit counts, max clock)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
