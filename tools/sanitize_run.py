@@ -41,5 +41,26 @@ kernel, grid, k, b, hf = config_args(w.cfg)
 ctx = Context(0).fit_local(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(np.array(w.y)).to(dev),
                            kernel, w.cfg.m, grid, bucket_log2=0)
 f, n = ctx.run_field(w.thetas[0], w.cfg.alpha, w.cfg.max_depth, 64, 7)
+# NEXT-3 fused multi-isovalue pass (union, masks, k_pmc<T>) and the brick pass opt-out
+for name in ("t1", "t2"):
+    w = generate(name)
+    kernel, grid, k, b, hf = config_args(w.cfg)
+    for bp in (0, -1):
+        ctx = Context(0).fit_local(torch.from_numpy(np.array(w.X)).to(dev),
+                                   torch.from_numpy(np.array(w.y)).to(dev), kernel, k, grid,
+                                   bucket_log2=b, h_full=hf, brick_pass=bp)
+        th = [w.thetas[0] - 0.2, w.thetas[0], w.thetas[0] + 0.3, 9.0, -9.0]
+        fields, nl, nu = ctx.run_field_multi(th, w.cfg.alpha, w.cfg.max_depth, 48, 3, 1)
+        cells, mask = ctx.union_cells()
+        lcpm = ctx.pmc_cells_multi(cells, th, 40, 5, 2)
+        print(name, "multi ok", bp, nu, list(nl), float(fields.sum()), float(lcpm.sum()))
+# SGPR input path
+w = generate("t2")
+kernel, grid, k, b, hf = config_args(w.cfg)
+XM = np.array(w.X)[:40]
+muM = np.array(w.y)[:40]
+AM = np.eye(40) * 1e-3
+ctx = Context(0).fit_sgpr(XM, muM, AM, kernel, 16, grid, bucket_log2=b, h_full=hf)
+f, n = ctx.run_field(w.thetas[0], w.cfg.alpha, w.cfg.max_depth, 32, 7)
 torch.cuda.synchronize()
 print("all ok")
