@@ -30,6 +30,53 @@ constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
 constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
 
+// Fast e^{-x} (x >= 0) for the brick's kernel evaluations: n = round(-x log2 e) by
+// the 1.5 2^52 magic add, f = -x - n ln2 (Cody-Waite, |f| <= ln2 / 2), e^f by its
+// degree-12 Taylor polynomial (truncation < 2e-16 relative), times 2^n built from the
+// exponent bits; 0 below 2^-1022.  The coefficients live in the constant bank, so
+// every Horner step is one DFMA with a c[] operand (the libm exp materialises each
+// 64-bit coefficient with two UMOVs per call).
+__constant__ double c_exp_taylor[13] = {
+    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
+    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+    0x1.1eed8eff8d898p-29};
+__constant__ double c_exp_consts[4] = {1.4426950408889634074, 6755399441055744.0, 0x1.62e42fefa39efp-1,
+                                       0x1.abc9e3b39803fp-56};
+
+__device__ __forceinline__ double exp_neg_fast(double x) {
+  const double t = fma(-x, c_exp_consts[0], c_exp_consts[1]);
+  const double n = t - c_exp_consts[1];
+  double f = fma(n, -c_exp_consts[2], -x);
+  f = fma(n, -c_exp_consts[3], f);
+  double p = c_exp_taylor[12];
+#pragma unroll
+  for (int i = 11; i >= 0; --i) p = fma(p, f, c_exp_taylor[i]);
+  const int ni = __double2loint(t);
+  const double scale = __hiloint2double((ni + 1023) << 20, 0);
+  return ni < -1022 ? 0.0 : p * scale;
+}
+
+// branch-free sqrt: MUFU.RSQ64H seed, two Newton steps on 1/sqrt, one on sqrt (~1 ulp);
+// sqrt(0) = 0 by a select (libm sqrt branches to a slow path per element)
+__device__ __forceinline__ double sqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  double r = x * y;
+  r = fma(0.5 * y, fma(-r, r, x), r);
+  return x > 0.0 ? r : 0.0;
+}
+
+// kernel value from r^2 (Matern-5/2 per BASELINE c4/c5) with exp_neg_fast
+__device__ __forceinline__ double kern_from_r2_fast(const KernParams& p, double r2) {
+  if (p.kind == LCP_K_SE) return p.var * exp_neg_fast(0.5 * r2);
+  const double r = sqrt_fast(r2);
+  const double s5 = SQRT5 * r;
+  return p.var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_fast(s5);
+}
+
 struct BrickArgs {
   KernParams kp;
   Geom g;
@@ -93,6 +140,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
   double* sX = sAlpha + k;
   double* KV = smem + head;                     // KP x VSTR
   double* sMu = KV + (int64_t)KP * VSTR;        // NVP
+  double* sT = sMu + NVP;                       // k x 16: separable squared offsets (phase 1)
   __shared__ int64_t s_r0;
   __shared__ int s_skip;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -135,18 +183,29 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         staged = b;
       }
       __syncthreads();
-      // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding
-      for (int idx = tid; idx < KP * NVP; idx += BRICK_THREADS) {
-        int j = idx >> 7, v = idx & (NVP - 1);
-        double val = 0.0;
-        if (j < k && v < NVB) {
-          int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
-          int vi = min(i0 + va, g.cells[0]), vj = min(j0 + vb, g.cells[1]), vk = min(k0 + vc, g.cells[2]);
-          double r2 = kern_r2(a.kp, sX[j] - vpos(g, 0, vi), sX[k + j] - vpos(g, 1, vj),
-                              sX[2 * k + j] - vpos(g, 2, vk));
-          val = kern_from_r2(a.kp, r2);
+      // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding.
+      // r^2 is separable over the lattice: T[j][5d + t] = ((x_jd - v_d(t)) / l_d)^2 for the
+      // 5 lattice positions t per axis d, then r^2 = (T_x + T_y) + T_z per element.
+      for (int e = tid; e < 15 * k; e += BRICK_THREADS) {
+        const int j = e / 15, col = e - 15 * j, d = col / 5, t = col - 5 * d;
+        const int c0 = d == 0 ? i0 : (d == 1 ? j0 : k0);
+        const double diff = (sX[d * k + j] - vpos(g, d, min(c0 + t, g.cells[d]))) * a.kp.inv_ls[d];
+        sT[16 * j + col] = diff * diff;
+      }
+      __syncthreads();
+      {
+        const int v = tid & (NVP - 1);
+        const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
+        const bool vok = v < NVB;
+        // straight-line body (clamped indices, 0/1 mask) so that the unrolled copies
+        // interleave: the Horner chains of exp are latency-bound one at a time
+        const int ta = vok ? va : 0, tb = vok ? 5 + vb : 5, tc = vok ? 10 + vc : 10;
+#pragma unroll 4
+        for (int j = tid >> 7; j < KP; j += BRICK_THREADS / NVP) {
+          const double* tj = sT + 16 * min(j, k - 1);
+          const double val = kern_from_r2_fast(a.kp, (tj[ta] + tj[tb]) + tj[tc]);
+          KV[(int64_t)j * VSTR + v] = (j < k && vok) ? val : 0.0;
         }
-        KV[(int64_t)j * VSTR + v] = val;
       }
       __syncthreads();
       {
@@ -288,7 +347,7 @@ static BrickArgs brick_args(const Ctx& c) {
 static size_t brick_smem(int k) {
   const int kp8 = (k + 7) & ~7;
   const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
-  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP);
+  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP + 16 * (int64_t)k);
 }
 
 bool fused_brick_supported(const Ctx& c) {
@@ -361,9 +420,7 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
   err = cudaSuccess;
   if (c.k > 128 || c.g.bs < BK) return false;
   const int k = c.k;
-  const int kp8 = (k + 7) & ~7;
-  const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
-  size_t smem = sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP);
+  size_t smem = brick_smem(k);
   if (smem > 227 * 1024) return false;
   if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
   if ((err = c.brick_idx.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
