@@ -39,6 +39,18 @@ SM_COUNT = 148
 LANES_PER_SM_CLK = 128
 
 
+# BASELINE.json asks for the paper's quoted timings beside ours, as context only (hardware unstated
+# in the paper; C++/Cython/Python on a CPU; N = 1600 samples)
+PAPER_CONTEXT = {
+    "hardware": "unstated in the paper (CPU implementation, PAPER.md:303)",
+    "dense_reconstruction_m500_128cube": "> 16 min (PAPER.md:15)",
+    "table3_dense_pmc_m500": "1232 s; ours (pruned) 249 s (PAPER.md:459-462)",
+    "table2_ours_by_resolution": "64: 46.7 s, 128: 4.2 min, 256: 20.3 min, 512: 2.17 h, 1024: 14.1 h (PAPER.md:440-442)",
+    "table2_dense_by_resolution": "64: 156.5 s, 128: 20.9 min, 256: 164.9 min, 512: 22.0 h (extrapolated) (PAPER.md:443)",
+    "cited_pmc_256x256x128": "~45 min (original PMC paper, cited at PAPER.md:17)",
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -393,6 +405,7 @@ def run_ours(args):
            "samples_per_step": samples_step,
            "phase_ms_per_step": {k2: v2 / args.steps for k2, v2 in st_phase.items()},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(float(lv[1])),
+           "paper_context": PAPER_CONTEXT,
            "clocks": clk}
     print(json.dumps(out), flush=True)
     if world > 1:
