@@ -88,6 +88,13 @@ CONFIGS = {
                  8, 0.1, 0.25, False, 0.5, 0.0, False, 0.001, "uniform",
                  KERNEL_SE, 0.25, (0.1, 0.1, 0.1), 1e-6, 0.0,
                  (None,), 64, 3, 2, 1600, 1e-3, 7, "fp64", 1201, 2201),
+    # the paper's largest target resolution (Table 2's 1024 column) on the
+    # c5 field: a scale test (the brick-pass records would need 223 GB, so the leaf pass
+    # takes the chunked per-leaf posterior path); not a BASELINE config
+    "x1024": Config("x1024", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), _cube(1024), 20000,
+                    256, 0.01, 0.2, True, 0.0, 0.0, False, 0.01, "mixed",
+                    KERNEL_MATERN52, 1.0, (0.03, 0.03, 0.03), 1e-4, 0.0,
+                    (0.0,), 128, 6, 2, 4096, 1e-5, 10, "fp64", 1005, 2005),
     # ragged parity case: non-power-of-two grid, bucket grid not dividing it
     "t1": Config("t1", (0.0, 0.0, 0.0), (0.92, 0.68, 0.44), (23, 17, 11), 60,
                  6, 0.05, 0.2, False, 0.0, 0.0, False, 0.01, "uniform",
