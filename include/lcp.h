@@ -134,6 +134,11 @@ lcp_status_t lcp_fit_sgpr(lcp_ctx_t* ctx, const double* xyz_M, const double* mu_
  * Nodes with U <= threshold are pruned.  Returns the leaf cells (cells of
  * refined max-depth nodes) in a ctx-owned device array valid until the next
  * fit/refine/destroy.  Blocks the host (one size read-back per level).
+ * With opts.brick_pass on (default when supported), the frontier of level
+ * Lfull-2 -- aligned 4^3-cell bricks -- runs the brick pass: vertex marginals of
+ * the bound lattice plus the isovalue-free 8-corner posterior and 8x8 factor of
+ * every cell of the brick, kept until the next fit and reused by every later
+ * lcp_pmc_cells* call whose cells they cover (any isovalue).
  * Errors: ESTATE before fit; EINVAL unless 0 < threshold < 0.5 and
  * 0 <= max_depth <= Lfull. */
 lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold,
@@ -146,8 +151,10 @@ lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold
  *   cells: n_cells ids (device pointer if cells_on_device, else host);
  *   lcp_out: n_cells floats = count / n_samples (device pointer if
  *   out_on_device, else host: the call then synchronizes).
- * Any cell list is accepted (dense baseline = all ids).  Asynchronous on the
- * ctx stream when both pointers are device pointers.
+ * Any cell list is accepted (dense baseline = all ids).  Cells covered by the
+ * brick-pass records of an earlier refine skip the posterior and factor; the
+ * results are bit-identical either way.  Asynchronous on the ctx stream when
+ * both pointers are device pointers (one 8-byte coverage read-back).
  * Errors: ESTATE, EINVAL (n_samples < 1, cell id out of range -> ENUMERIC-free
  * check on the host only when cells_on_device == 0), ENUMERIC, ECUDA. */
 lcp_status_t lcp_pmc_cells(lcp_ctx_t* ctx, const int64_t* cells, int64_t n_cells,
