@@ -152,7 +152,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
-                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.pmc_counters, &c.crec, &c.brick_done, &c.brick_unit, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
+                    &c.brick_flag, &c.brick_idx, &c.brick_start, &c.vscratch, &c.pmc_counters, &c.crec, &c.brick_done, &c.brick_unit, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
   for (DevBuf* b : bufs) b->release();
   if (c.h_counters) cudaFreeHost(c.h_counters);
   if (c.ev_init)

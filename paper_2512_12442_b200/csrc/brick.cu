@@ -414,6 +414,213 @@ cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- big k
+// k_brick_big: the brick posterior for 128 < k <= BIG_KMAX (e.g. the exact-GP dense
+// baseline, k = m = 500), where neither K (k x 128) nor L^-1 fits in shared memory.
+// Per brick the 125 vertex columns go in 4 chunks of 32: K chunk in smem (row stride
+// 36 = 4 mod 16), V chunk = L^-1 K chunk by DMMA with the A fragments streamed from
+// global memory (L2-resident, each feeding 4 column tiles), V stored column-major in a
+// per-CTA global scratch (L2-resident); then Sigma_C = K_CC - V_C^T V_C per leaf cell
+// of the run by DMMA on the scratch.  Leaves come through a permutation (grouped by
+// brick); results go to post[perm[q]].
+constexpr int BIG_KMAX = 640;
+constexpr int BIG_CH = 32;                   // columns per chunk
+constexpr int BIG_CST = 36;                  // K chunk row stride (doubles)
+
+__global__ void __launch_bounds__(BRICK_THREADS, 1)
+    k_brick_big(BrickArgs a, const int64_t* __restrict__ cells, const int64_t* __restrict__ perm,
+                const int64_t* __restrict__ run_start, int64_t nruns, unsigned long long* __restrict__ work,
+                double* __restrict__ vscratch, double* __restrict__ post, int* __restrict__ derr) {
+  extern __shared__ double smem[];
+  const int k = a.k, KP = a.kp8, NRT = KP >> 3;
+  double* sAlpha = smem;                       // k
+  double* sX = sAlpha + k;                     // 3k
+  double* KC = smem + ((4 * (int64_t)k + 1) & ~1ll);   // KP x BIG_CST
+  double* sMu = KC + (int64_t)KP * BIG_CST;    // NVP
+  double* Vg = vscratch + (int64_t)blockIdx.x * NVP * KP;   // column-major: V[col][row]
+  __shared__ int64_t s_r0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  const Geom& g = a.g;
+  int staged = -1;
+  const int nt = (NRT + 15) / 16;              // row tiles per warp (<= 5 for KP <= 640)
+  for (;;) {
+    if (tid == 0) s_r0 = (int64_t)atomicAdd(work, 1ull);
+    __syncthreads();
+    const int64_t r = s_r0;
+    if (r >= nruns) break;
+    const int64_t q0 = run_start[r], q1 = run_start[r + 1];
+    int ci, cj, ck;
+    cell_ijk(g, cells[perm[q0]], ci, cj, ck);
+    const int i0 = ci & ~(BK - 1), j0 = cj & ~(BK - 1), k0 = ck & ~(BK - 1);
+    const int b = bucket_id(g, vbucket_axis(g, 0, i0), vbucket_axis(g, 1, j0), vbucket_axis(g, 2, k0));
+    const double* blk = a.bdata + (int64_t)b * a.bstride;
+    if (b != staged) {
+      for (int t = tid; t < 4 * k; t += BRICK_THREADS) smem[t] = __ldg(blk + la_size(k) + t);
+      staged = b;
+    }
+    __syncthreads();
+    for (int cc = 0; cc < NVP / BIG_CH; ++cc) {
+      // K chunk: columns v = 32 cc + cl of the brick's (clamped) vertex lattice
+      {
+        const int cl = tid & (BIG_CH - 1), v = BIG_CH * cc + cl;
+        const bool vok = v < NVB;
+        const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
+        const int vi = min(i0 + (vok ? va : 0), g.cells[0]), vj = min(j0 + (vok ? vb : 0), g.cells[1]),
+                  vk = min(k0 + (vok ? vc : 0), g.cells[2]);
+        const double px = vpos(g, 0, vi), py = vpos(g, 1, vj), pz = vpos(g, 2, vk);
+        for (int j = tid / BIG_CH; j < KP; j += BRICK_THREADS / BIG_CH) {
+          const int jj = min(j, k - 1);
+          const double r2 = kern_r2(a.kp, sX[jj] - px, sX[k + jj] - py, sX[2 * k + jj] - pz);
+          const double val = kern_from_r2_fast(a.kp, r2);
+          KC[(int64_t)j * BIG_CST + cl] = (j < k && vok) ? val : 0.0;
+        }
+      }
+      __syncthreads();
+      {
+        // mu of the chunk's columns: 16 threads per column
+        const int cl = tid >> 4, part = tid & 15;
+        double sacc = 0.0;
+        for (int j = part; j < k; j += 16) sacc = fma(KC[(int64_t)j * BIG_CST + cl], sAlpha[j], sacc);
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (part == 0) sMu[BIG_CH * cc + cl] = a.kp.m0 + sacc;
+      }
+      // V chunk = L^-1 K chunk: warp w owns row tiles w + 16 t (zig-zag), all 4 column tiles
+      double acc[5][4][2];
+#pragma unroll
+      for (int t = 0; t < 5; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+      auto rtile = [&](int t) { return (t & 1) ? (15 - wid) + 16 * t : wid + 16 * t; };
+      int last = -1;
+#pragma unroll
+      for (int t = 0; t < 5; ++t)
+        if (t < nt && rtile(t) < NRT) last = max(last, rtile(t));
+      const int jend = last < 0 ? 0 : min(KP, 8 * last + 8);
+      const double* LA = blk;
+      for (int j = 0; j < jend; j += 4) {
+        double bf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bf[u] = KC[(int64_t)(j + lc) * BIG_CST + 8 * u + lr];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const int rt = rtile(t);
+          if (t >= nt || rt >= NRT || 8 * rt + 7 < j) continue;   // warp-uniform
+          const double af = __ldg(LA + la_block(rt, j >> 2) + lane);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int rt = rtile(t);
+        if (t >= nt || rt >= NRT) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int col = BIG_CH * cc + 8 * u + 2 * lc, row = 8 * rt + lr;
+          Vg[(int64_t)col * KP + row] = acc[t][u][0];
+          Vg[(int64_t)(col + 1) * KP + row] = acc[t][u][1];
+        }
+      }
+      __syncthreads();   // KC is rewritten by the next chunk; V chunk visible to the block
+    }
+    // Sigma_C = K_CC - V_C^T V_C per leaf of the run (warp per cell)
+    for (int64_t qq = q0 + wid; qq < q1; qq += BRICK_THREADS / 32) {
+      const int64_t slot = perm[qq];
+      int xi, xj, xk;
+      cell_ijk(g, cells[slot], xi, xj, xk);
+      const int cr = lr;
+      const int lv = (xi - i0 + (cr & 1)) + (BK + 1) * ((xj - j0 + ((cr >> 1) & 1)) + (BK + 1) * (xk - k0 + (cr >> 2)));
+      const double* vcol = Vg + (int64_t)lv * KP;
+      double d0 = 0.0, d1 = 0.0;
+      for (int sidx = 0; sidx < KP; sidx += 4) {
+        const double v = vcol[sidx + lc];
+        dmma(v, v, d0, d1);
+      }
+      double* rec = post + 44 * slot;
+      const int c0 = 2 * lc, c1 = 2 * lc + 1;
+      if (c0 <= cr) {
+        const double s0 = a.kcc[cr * 8 + c0] - d0;
+        rec[8 + cr * (cr + 1) / 2 + c0] = s0;
+        if (c0 == cr && s0 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      }
+      if (c1 <= cr) {
+        const double s1 = a.kcc[cr * 8 + c1] - d1;
+        rec[8 + cr * (cr + 1) / 2 + c1] = s1;
+        if (c1 == cr && s1 < a.var_err) atomicOr(derr, DERR_NUMERIC);
+      }
+      if (lc == 0) rec[cr] = sMu[lv];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_brick_keys(Geom g, const int64_t* __restrict__ cells, int64_t n, int32_t* __restrict__ key) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) key[q] = (int32_t)brick_key(g, cells[q]);
+}
+__global__ void k_brick_flags_perm(const int32_t* __restrict__ key, const int64_t* __restrict__ perm, int64_t n,
+                                   int64_t* __restrict__ flag) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  flag[q] = (q == 0 || key[perm[q]] != key[perm[q - 1]]) ? 1 : 0;
+}
+
+// big-k brick posterior of an arbitrary list: group the cells by brick, then
+// k_brick_big over the runs.  Returns false (no error) when k is out of range or
+// the list has fewer than 8 cells per brick on average.
+bool brick_posterior_big(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err) {
+  err = cudaSuccess;
+  if (c.k <= 128 || c.k > BIG_KMAX || c.g.bs < BK || c.g.lfull < 2 || 3 * (c.g.lfull - 2) > 30) return false;
+  const int k = c.k, kp8 = (k + 7) & ~7;
+  const int64_t nbr = (int64_t)1 << (3 * (c.g.lfull - 2));
+  if ((err = c.cell_bucket.ensure(sizeof(int32_t) * n)) != cudaSuccess) return false;
+  if ((err = c.perm.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
+  if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
+  if ((err = c.brick_idx.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
+  if ((err = c.gcount.ensure(sizeof(int64_t) * (nbr + 1))) != cudaSuccess) return false;
+  if ((err = c.goff.ensure(sizeof(int64_t) * (nbr + 1))) != cudaSuccess) return false;
+  if ((err = c.counters.ensure(sizeof(unsigned long long) * 16)) != cudaSuccess) return false;
+  unsigned long long* dcnt = c.counters.as<unsigned long long>();
+  int32_t* key = c.cell_bucket.as<int32_t>();
+  int64_t* pm = c.perm.as<int64_t>();
+  const unsigned gr = (unsigned)((n + 255) / 256);
+  k_brick_keys<<<gr, 256, 0, c.stream>>>(c.g, cells, n, key);
+  ++c.n_launch;
+  if ((err = group_by_key(c, key, n, nbr, pm)) != cudaSuccess) return false;
+  k_brick_flags_perm<<<gr, 256, 0, c.stream>>>(key, pm, n, c.brick_flag.as<int64_t>());
+  ++c.n_launch;
+  if ((err = exclusive_scan_i64(c, c.brick_flag.as<int64_t>(), c.brick_idx.as<int64_t>(), n,
+                                (int64_t*)(dcnt + 14))) != cudaSuccess)
+    return false;
+  if ((err = cudaMemcpyAsync(c.h_counters + 14, dcnt + 14, sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream)) !=
+      cudaSuccess)
+    return false;
+  if ((err = cudaStreamSynchronize(c.stream)) != cudaSuccess) return false;
+  const int64_t nruns = c.h_counters[14];
+  if (n / std::max<int64_t>(nruns, 1) < 8) return false;
+  if ((err = c.brick_start.ensure(sizeof(int64_t) * (nruns + 1))) != cudaSuccess) return false;
+  int64_t* start = c.brick_start.as<int64_t>();
+  k_brick_starts<<<gr, 256, 0, c.stream>>>(c.brick_flag.as<int64_t>(), c.brick_idx.as<int64_t>(), n, start);
+  ++c.n_launch;
+  if ((err = cudaMemcpyAsync(start + nruns, &n, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream)) != cudaSuccess)
+    return false;
+  if ((err = cudaMemsetAsync(dcnt + 13, 0, sizeof(unsigned long long), c.stream)) != cudaSuccess) return false;
+  const size_t smem = sizeof(double) * (((4 * (int64_t)k + 1) & ~1ll) + (int64_t)kp8 * BIG_CST + NVP);
+  if ((err = cudaFuncSetAttribute(k_brick_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return false;
+  const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)c.sm_count);
+  if ((err = c.vscratch.ensure(sizeof(double) * (size_t)grid * NVP * kp8)) != cudaSuccess) return false;
+  k_brick_big<<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), cells, pm, start, nruns, dcnt + 13,
+                                                       c.vscratch.as<double>(), post, c.derr.as<int>());
+  ++c.n_launch;
+  err = cudaGetLastError();
+  c.last_brick_runs = nruns;
+  return err == cudaSuccess;
+}
+
 // Returns true when the brick path handled the list (Morton-like order with
 // enough leaves per brick and k small enough for shared memory).
 bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err) {

@@ -117,6 +117,7 @@ struct Ctx {
   // leaf pass scratch
   DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
   DevBuf brick_flag, brick_idx, brick_start;
+  DevBuf vscratch;               // k_brick_big: per-CTA V scratch (L2-resident)
   // refine-time brick pass (brick.cu k_brick<true>): MC records of every cell of the
   // level-(Lfull-2) frontier bricks, indexed by the cell's Morton code
   bool fused = false;            // enabled for this fit (supported and records fit in HBM)
@@ -145,6 +146,7 @@ struct Ctx {
 // ---- internal launchers (implemented in the .cu files) ----
 cudaError_t exclusive_scan_i64(Ctx& c, const int64_t* in, int64_t* out, int64_t n, int64_t* total_dev);
 cudaError_t group_by_bucket(Ctx& c, const int32_t* bucket_of_item, int64_t n, int64_t* perm_out);
+cudaError_t group_by_key(Ctx& c, const int32_t* key_of_item, int64_t n, int64_t nkeys, int64_t* perm_out);
 
 lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* y, int64_t m, int on_device,
                       const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts,
@@ -172,6 +174,7 @@ cudaError_t launch_cell_posterior(Ctx& c, const int64_t* cells, const int64_t* p
                                   const int32_t* bkt_sorted, int64_t n, double* post);
 bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err);
 bool fused_brick_supported(const Ctx& c);
+bool brick_posterior_big(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err);
 cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double* post);
 cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post);
 lcp_status_t fused_setup(Ctx& c);

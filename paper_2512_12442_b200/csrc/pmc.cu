@@ -520,6 +520,8 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
     cudaError_t be;
     if (brick_posterior(c, cells, n, post, be)) return LCP_OK;
     if (be != cudaSuccess) return cuda_err(c, be, "brick posterior");
+    if (brick_posterior_big(c, cells, n, post, be)) return LCP_OK;
+    if (be != cudaSuccess) return cuda_err(c, be, "big-k brick posterior");
   }
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
   CK(cudaMemsetAsync(dcnt + 15, 0, sizeof(unsigned long long), c.stream));

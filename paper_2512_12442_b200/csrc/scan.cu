@@ -138,8 +138,13 @@ __global__ void k_bucket_scatter(const int32_t* __restrict__ bkt, int64_t n, int
 // perm_out[n]: item indices grouped by bucket (order inside a bucket is
 // unspecified; every consumer's result is a function of the item alone).
 cudaError_t group_by_bucket(Ctx& c, const int32_t* bucket_of_item, int64_t n, int64_t* perm_out) {
+  return group_by_key(c, bucket_of_item, n, c.g.nbuckets, perm_out);
+}
+
+// counting sort of items by an int32 key in [0, nkeys) (order within a key unspecified)
+cudaError_t group_by_key(Ctx& c, const int32_t* bucket_of_item, int64_t n, int64_t nkeys, int64_t* perm_out) {
   if (n <= 0) return cudaSuccess;
-  int nbk = c.g.nbuckets;
+  int64_t nbk = nkeys;
   cudaError_t e = c.gcount.ensure(sizeof(int64_t) * (nbk + 1));
   if (e != cudaSuccess) return e;
   e = c.goff.ensure(sizeof(int64_t) * (nbk + 1));

@@ -600,3 +600,35 @@ def test_multi_iso_edges_and_errors(dev):
     for t in range(16):
         frac, mean, mx = lcp_parity(got[t], want[t], 700)
         assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
+
+
+def test_big_k_brick_posterior_exact_gp(dev):
+    # k = m = 500 (the c3 exact-GP dense baseline) takes k_brick_big (K and L^-1 do not
+    # fit in shared memory): whole bricks of a dense list, posteriors against the oracle
+    w, ctx, M = _ctx("c3", dev, k=500, bucket_log2=0, keep_records=False)
+    cfg = w.cfg
+    nx, ny, nz = cfg.cells
+    g = np.random.default_rng(4)
+    cells = []
+    for _ in range(24):
+        bi, bj, bk = g.integers(0, nx // 4), g.integers(0, ny // 4), g.integers(0, nz // 4)
+        for kk in range(4):
+            for jj in range(4):
+                for ii in range(4):
+                    cells.append((4 * bi + ii) + nx * ((4 * bj + jj) + ny * (4 * bk + kk)))
+    cells = np.array(cells, np.int64)
+    g.shuffle(cells)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    assert ctx.stats()["brick_runs"] == 24
+    mu_g, cov_g = mu_g.cpu().numpy(), cov_g.cpu().numpy()
+    worst = (0.0, 0.0)
+    for q in g.choice(len(cells), 60, replace=False):
+        mu_o, cov_o = M.cell_posterior(int(cells[q]))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, cfg.variance, 1e-5)
+        worst = (max(worst[0], em), max(worst[1], ec))
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
+    # and the LCP of those cells against the oracle (same streams)
+    lcp_g = ctx.pmc_cells(torch.from_numpy(cells[:200]).to(dev), w.thetas[0], 1500, 9).cpu().numpy()
+    lcp_o = M.pmc_cells(cells[:200], w.thetas[0], 1500, 9)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1500)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
