@@ -410,15 +410,18 @@ __device__ __forceinline__ void dmma_f(double a, double b, double& d0, double& d
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams kp, int k,
+// GMEM: K_y / X live in a per-CTA global scratch (L2-resident) instead of shared
+// memory (k > 128); CTAs loop over buckets.
+template <bool GMEM>
+__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams kp, int k, int nbk,
                                                                     const double* __restrict__ X,
                                                                     const double* __restrict__ yobs,
                                                                     const int32_t* __restrict__ S,
                                                                     double* __restrict__ bdata, int64_t bstride,
+                                                                    double* __restrict__ gscratch,
                                                                     int* __restrict__ derr) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
-  const int b = blockIdx.x;
   const int tid = threadIdx.x, bd = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = bd >> 5;
   const int KP = (k + FB - 1) & ~(FB - 1), nb = KP / FB, ST = KP + 4;
@@ -429,8 +432,11 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
   double* rr = sz + KP;
   double* vv = rr + KP;
   double* sT = vv + KP;                  // nb blocks of 8 x 12 (stride 12: conflict-free)
-  double* A = sT + nb * FB * 12;         // KP x ST
+  double* Srow = sT + nb * FB * 12;      // nb blocks of 8 x 12: S_J of the inverse's block row
+  double* A = GMEM ? gscratch + (int64_t)blockIdx.x * KP * ST : Srow + nb * FB * 12;   // KP x ST
   const int lr = lane >> 2, lc = lane & 3;
+  for (int b = blockIdx.x; b < nbk; b += gridDim.x) {
+  __syncthreads();
   const int32_t* Sb = S + (int64_t)b * k;
   double* out = bdata + (int64_t)b * bstride;
   for (int a = tid; a < k; a += bd) {
@@ -546,14 +552,12 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
   }
   if (!ok) {
     if (tid == 0) atomicOr(derr, DERR_FACTOR);
-    return;
+    continue;
   }
   // L^-1 in place, block row by block row
   for (int I = 0; I < nb; ++I) {
     // S_J = sum_{K=J}^{I-1} L_IK X_KJ for J < I (warp w: J = w, w + nw, ...)
-    // (nw = 8 warps, nb <= 16: at most two J per warp, held in s0 / s1)
-    double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0};
-    for (int J = wid, nj = 0; J < I; J += nw, ++nj) {
+    for (int J = wid; J < I; J += nw) {
       double d0 = 0.0, d1 = 0.0;
       for (int K = J; K < I; ++K) {
         const double* Lb = Ab(I, K);
@@ -562,19 +566,18 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
         dmma_f(Lb[lr * ST + lc], Xb[lc * ST + lr], d0, d1);
         dmma_f(Lb[lr * ST + 4 + lc], Xb[(4 + lc) * ST + lr], d0, d1);
       }
-      if (nj == 0) { s0[0] = d0; s0[1] = d1; } else { s1[0] = d0; s1[1] = d1; }
+      double* Sj = Srow + J * FB * 12;
+      Sj[lr * 12 + 2 * lc] = d0;
+      Sj[lr * 12 + 2 * lc + 1] = d1;
     }
-    __syncthreads();   // row I of L is consumed
+    __syncthreads();   // row I of L is consumed; S_J of this row are in Srow
     const double* T = sT + I * FB * 12;
-    for (int J = wid, nj = 0; J < I; J += nw, ++nj) {
-      double* Bk = Ab(I, J);
-      Bk[lr * ST + 2 * lc] = nj == 0 ? s0[0] : s1[0];
-      Bk[lr * ST + 2 * lc + 1] = nj == 0 ? s0[1] : s1[1];
-      __syncwarp();
+    for (int J = wid; J < I; J += nw) {
+      const double* Sj = Srow + J * FB * 12;
       double d0 = 0.0, d1 = 0.0;
-      dmma_f(-T[lr * 12 + lc], Bk[lc * ST + lr], d0, d1);
-      dmma_f(-T[lr * 12 + 4 + lc], Bk[(4 + lc) * ST + lr], d0, d1);
-      __syncwarp();
+      dmma_f(-T[lr * 12 + lc], Sj[lc * 12 + lr], d0, d1);
+      dmma_f(-T[lr * 12 + 4 + lc], Sj[(4 + lc) * 12 + lr], d0, d1);
+      double* Bk = Ab(I, J);
       Bk[lr * ST + 2 * lc] = d0;
       Bk[lr * ST + 2 * lc + 1] = d1;
     }
@@ -610,11 +613,12 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
     const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
     out[e] = (i < k && j <= i) ? A[(int64_t)i * ST + j] : 0.0;
   }
+  }   // bucket loop
 }
 
-size_t bucket_factor_blk_smem(int k) {
+size_t bucket_factor_blk_smem(int k, bool gmem) {
   const int KP = (k + FB - 1) & ~(FB - 1), nb = KP / FB;
-  return sizeof(double) * (5 * (size_t)KP + (size_t)nb * FB * 12 + (size_t)KP * (KP + 4));
+  return sizeof(double) * (5 * (size_t)KP + 2 * (size_t)nb * FB * 12 + (gmem ? 0 : (size_t)KP * (KP + 4)));
 }
 
 // NEXT-2: SGPR bucket factor.  Eq. 1 restricted to the bucket's k nearest
@@ -968,11 +972,26 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       const char* v = std::getenv("LCP_FACTOR_BLOCKED");
       return v && v[0] == '0';
     }();
-    if (k <= 128 && FACT_THREADS == 256 && !blk_off) {   // nb <= 16 blocks over 8 warps
-      const size_t sb = bucket_factor_blk_smem(k);
-      CK(cudaFuncSetAttribute(k_bucket_factor_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-      k_bucket_factor_blk<<<nbk, FACT_THREADS, sb, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
-                                                               c.bdata.as<double>(), c.bstride, c.derr.as<int>());
+    if (!blk_off && bucket_factor_blk_smem(k, k > 128) <= 220 * 1024) {
+      const bool gm = k > 128;
+      const size_t sb = bucket_factor_blk_smem(k, gm);
+      const int KPf = (k + FB - 1) & ~(FB - 1);
+      unsigned gridf = (unsigned)nbk;
+      double* gsf = nullptr;
+      if (gm) {
+        gridf = (unsigned)std::min<int64_t>(nbk, 2 * (int64_t)c.sm_count);
+        CK(c.fscratch.ensure(sizeof(double) * (size_t)gridf * KPf * (KPf + 4)));
+        gsf = c.fscratch.as<double>();
+        CK(cudaFuncSetAttribute(k_bucket_factor_blk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+        k_bucket_factor_blk<true><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
+                                                                         c.S.as<int32_t>(), c.bdata.as<double>(),
+                                                                         c.bstride, gsf, c.derr.as<int>());
+      } else {
+        CK(cudaFuncSetAttribute(k_bucket_factor_blk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+        k_bucket_factor_blk<false><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
+                                                                          c.S.as<int32_t>(), c.bdata.as<double>(),
+                                                                          c.bstride, nullptr, c.derr.as<int>());
+      }
     } else if (use_smem) {
       CK(cudaFuncSetAttribute(k_bucket_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       k_bucket_factor<true><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
