@@ -632,3 +632,20 @@ def test_big_k_brick_posterior_exact_gp(dev):
     lcp_o = M.pmc_cells(cells[:200], w.thetas[0], 1500, 9)
     frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1500)
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_zero_noise_interpolation_gpu(dev):
+    # BASELINE pin on the CUDA path: with nugget 0 the (exact, k = m) posterior
+    # interpolates the observations with zero variance (PAPER.md:89-95 with A_M = 0)
+    from paper_2512_12442_b200 import Context
+    g = np.random.default_rng(12)
+    pts = np.array([(i, j, l) for i in range(4) for j in range(3) for l in range(3)], float)
+    X = (pts + 0.5 + 0.2 * g.uniform(-1, 1, pts.shape)) / np.array([4.0, 3.0, 3.0])
+    y = np.sin(3 * X[:, 0]) + X[:, 1] * X[:, 2]
+    kernel = (0, 1.0, (0.25, 0.25, 0.25), 0.0, 0.0)
+    grid = ((0.0, 0.0, 0.0), (1.0, 1.0, 1.0), (8, 8, 8))
+    ctx = Context(0).fit_local(torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev), kernel, len(X), grid,
+                               bucket_log2=0)
+    mu, var = ctx.point_marginals(torch.from_numpy(X).to(dev))
+    assert np.abs(mu.cpu().numpy() - y).max() <= 1e-6
+    assert np.abs(var.cpu().numpy()).max() <= 1e-8
