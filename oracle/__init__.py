@@ -68,6 +68,8 @@ def lib():
         L.orc_gp_exact.argtypes = [C.POINTER(Kernel), dp, dp, C.c_int64, dp, C.c_int64, dp, P]
         L.orc_model_create.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, C.c_int64,
                                        C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]
+        L.orc_model_create_box.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, C.c_int64,
+                                           C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(P)]
         L.orc_model_destroy.argtypes = [P]
         L.orc_model_destroy.restype = None
         L.orc_model_nbuckets.argtypes = [P]
@@ -242,6 +244,22 @@ class Model:
         h = C.c_void_p()
         _check(lib().orc_model_create_sgpr(C.byref(kern), C.byref(grid), self.X, self.y, self.A, len(self.X),
                                            int(k), int(bucket_log2), int(h_full), C.byref(h)), "model_create_sgpr")
+        self._h = h
+        return self
+
+    @classmethod
+    def box(cls, kern: Kernel, grid: Grid, X, y, k, bucket_log2, h_full, beta):
+        """R28 (NEXT-2): local set = observations in the bucket box enlarged by beta l_d."""
+        self = cls.__new__(cls)
+        self.kern, self.grid = kern, grid
+        self.X = np.ascontiguousarray(X, np.float64)
+        self.y = np.ascontiguousarray(y, np.float64)
+        self.k = int(k)
+        self.cells = tuple(grid.cells)
+        h = C.c_void_p()
+        _check(lib().orc_model_create_box(C.byref(kern), C.byref(grid), self.X, self.y, len(self.X), int(k),
+                                          int(bucket_log2), int(h_full), float(beta), C.byref(h)),
+               "model_create_box")
         self._h = h
         return self
 

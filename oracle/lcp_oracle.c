@@ -161,7 +161,9 @@ struct orc_model {
     int32_t m, k;
     double* X;            /* m x 3 */
     double* y;            /* m */
-    int32_t* S;           /* nbuckets x k, ascending observation index */
+    int32_t* S;           /* nbuckets x k, ascending observation index (box mode: kb[b] used, -1 after) */
+    int32_t* kb;          /* box mode (R28): per-bucket set size <= k; NULL = k-NN mode (every set has k) */
+    double beta;          /* box mode: enlargement of the bucket box in units of l_d */
     double* L;            /* nbuckets x k x k, lower factor of K_y(S_B) */
     double* alpha;        /* nbuckets x k */
     double* WAW;          /* NEXT-2 SGPR mode: nbuckets x k x k, W A_SS W with W = K_SS^-1 (NULL: GP regression) */
@@ -202,8 +204,13 @@ int32_t orc_cell_bucket(const orc_model_t* M, int64_t cell) {
     return orc_vertex_bucket(M, i, j, k);
 }
 
+/* size of bucket b's local set (k in k-NN mode) */
+static int set_size(const orc_model_t* M, int32_t b) { return M->kb ? M->kb[b] : M->k; }
+
 void orc_model_bucket_set(const orc_model_t* M, int32_t b, int32_t* idx_out) {
-    memcpy(idx_out, M->S + (size_t)b * M->k, sizeof(int32_t) * M->k);
+    int kb = set_size(M, b);
+    memcpy(idx_out, M->S + (size_t)b * M->k, sizeof(int32_t) * kb);
+    for (int a = kb; a < M->k; ++a) idx_out[a] = -1;
 }
 
 typedef struct { double d2; int32_t idx; } knn_item;
@@ -227,10 +234,10 @@ static void vertex_pos(const orc_model_t* M, int32_t i, int32_t j, int32_t k, do
 }
 
 int orc_local_marginal(const orc_model_t* M, int32_t b, const double* x, double* mu, double* var) {
-    int k = M->k;
-    const int32_t* S = M->S + (size_t)b * k;
-    const double* L = M->L + (size_t)b * k * k;
-    const double* al = M->alpha + (size_t)b * k;
+    int ks = M->k, k = set_size(M, b);
+    const int32_t* S = M->S + (size_t)b * ks;
+    const double* L = M->L + (size_t)b * ks * ks;   /* k x k, stride k */
+    const double* al = M->alpha + (size_t)b * ks;
     double* kv = malloc(sizeof(double) * k);
     double* v = malloc(sizeof(double) * k);
     double s = 0.0;
@@ -243,7 +250,7 @@ int orc_local_marginal(const orc_model_t* M, int32_t b, const double* x, double*
     double q = orc_kernel(&M->kern, x, x);
     for (int a = 0; a < k; ++a) q -= v[a] * v[a];
     if (M->WAW) {   /* + K_xS W A_SS W K_Sx (Eq. 1, third term) */
-        const double* C = M->WAW + (size_t)b * k * k;
+        const double* C = M->WAW + (size_t)b * ks * ks;
         for (int a = 0; a < k; ++a)
             for (int c = 0; c < k; ++c) q += kv[a] * C[(size_t)a * k + c] * kv[c];
     }
@@ -260,9 +267,50 @@ static int floor_var(const orc_model_t* M, double var, double* out) {
     return ORC_OK;
 }
 
+/* R28 box mode: bucket b's local set is every observation in the bucket box enlarged
+ * by beta l_d per axis, [lo_b - beta l, hi_b + beta l) (the paper's
+ * beta-l box with beta = 6 at P:423), ascending index; EINVAL if a set exceeds k.
+ * Bounds evaluated left to right without FMA (bit-identical to the GPU's). */
+static int box_set(const orc_model_t* M, int32_t bkt, const double* X, int64_t m, int32_t* S, int32_t k) {
+    int32_t bi[3] = {bkt % M->nb[0], (bkt / M->nb[0]) % M->nb[1], bkt / (M->nb[0] * M->nb[1])};
+    double lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+        double w = M->beta * M->kern.lengthscale[d];
+        lo[d] = (M->grid.lo[d] + (double)(bi[d] * M->bs) * M->h[d]) - w;
+        hi[d] = (M->grid.lo[d] + (double)((bi[d] + 1) * M->bs) * M->h[d]) + w;
+    }
+    int n = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        int in = 1;
+        for (int d = 0; d < 3; ++d) in = in && X[3 * i + d] >= lo[d] && X[3 * i + d] < hi[d];
+        if (in) {
+            if (n >= k) return -1;
+            S[n++] = (int32_t)i;
+        }
+    }
+    return n;
+}
+
+static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
+                        const double* y, int64_t m, int32_t k, int32_t bucket_log2,
+                        int32_t h_full, double beta, orc_model_t** out);
+
 int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                      const double* y, int64_t m, int32_t k, int32_t bucket_log2,
                      int32_t h_full, orc_model_t** out) {
+    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, 0.0, out);
+}
+
+int orc_model_create_box(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
+                         const double* y, int64_t m, int32_t k, int32_t bucket_log2,
+                         int32_t h_full, double beta, orc_model_t** out) {
+    if (!(beta > 0.0)) return ORC_EINVAL;
+    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, beta, out);
+}
+
+static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
+                        const double* y, int64_t m, int32_t k, int32_t bucket_log2,
+                        int32_t h_full, double beta, orc_model_t** out) {
     *out = NULL;
     if (m < 1 || k < 1 || k > m || bucket_log2 < 0 || h_full < 0) return ORC_EINVAL;
     if (kern->variance <= 0 || kern->nugget < 0) return ORC_EINVAL;
@@ -290,6 +338,8 @@ int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const dou
     M->nbuckets = M->nb[0] * M->nb[1] * M->nb[2];
     M->m = (int32_t)m;
     M->k = k;
+    M->beta = beta;
+    if (beta > 0.0) M->kb = malloc(sizeof(int32_t) * (size_t)M->nbuckets);
     M->X = malloc(sizeof(double) * 3 * m);
     M->y = malloc(sizeof(double) * m);
     memcpy(M->X, X, sizeof(double) * 3 * m);
@@ -304,37 +354,51 @@ int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const dou
         int32_t bi[3] = {bkt % M->nb[0], (bkt / M->nb[0]) % M->nb[1], bkt / (M->nb[0] * M->nb[1])};
         double c[3];
         for (int d = 0; d < 3; ++d) c[d] = grid->lo[d] + ((double)bi[d] + 0.5) * ((double)M->bs * M->h[d]);
-        /* k nearest in the metric sum_d ((x_d - c_d) w_d)^2, ties -> lower index (R2) */
-        knn_item* it = malloc(sizeof(knn_item) * m);
-        for (int64_t i = 0; i < m; ++i) {
-            double t0 = (X[3 * i + 0] - c[0]) * M->w[0];
-            double t1 = (X[3 * i + 1] - c[1]) * M->w[1];
-            double t2 = (X[3 * i + 2] - c[2]) * M->w[2];
-            it[i].d2 = t0 * t0 + t1 * t1 + t2 * t2;
-            it[i].idx = (int32_t)i;
-        }
-        qsort(it, m, sizeof(knn_item), knn_cmp);
         int32_t* S = M->S + (size_t)bkt * k;
-        for (int a = 0; a < k; ++a) S[a] = it[a].idx;
-        qsort(S, k, sizeof(int32_t), int_cmp);
-        free(it);
-        /* K_y = K(S,S) + sigma_n^2 I; L = chol(K_y); alpha = K_y^-1 (y_S - m0)  (Eq. 1, R1) */
-        double* A = malloc(sizeof(double) * k * k);
+        int kb = k;
+        if (beta > 0.0) {
+            kb = box_set(M, bkt, X, m, S, k);
+            if (kb < 0) {
+#pragma omp critical
+                status = ORC_EINVAL;
+                kb = 0;
+            }
+            M->kb[bkt] = kb;
+            for (int a = kb; a < k; ++a) S[a] = -1;
+        } else {
+            /* k nearest in the metric sum_d ((x_d - c_d) w_d)^2, ties -> lower index (R2) */
+            knn_item* it = malloc(sizeof(knn_item) * m);
+            for (int64_t i = 0; i < m; ++i) {
+                double t0 = (X[3 * i + 0] - c[0]) * M->w[0];
+                double t1 = (X[3 * i + 1] - c[1]) * M->w[1];
+                double t2 = (X[3 * i + 2] - c[2]) * M->w[2];
+                it[i].d2 = t0 * t0 + t1 * t1 + t2 * t2;
+                it[i].idx = (int32_t)i;
+            }
+            qsort(it, m, sizeof(knn_item), knn_cmp);
+            for (int a = 0; a < k; ++a) S[a] = it[a].idx;
+            qsort(S, k, sizeof(int32_t), int_cmp);
+            free(it);
+        }
+        /* K_y = K(S,S) + sigma_n^2 I; L = chol(K_y); alpha = K_y^-1 (y_S - m0)  (Eq. 1, R1);
+         * box mode: the kb x kb system of the bucket's set (L stored with stride kb) */
+        const int kk = kb;
+        double* A = malloc(sizeof(double) * (kk > 0 ? kk * kk : 1));
         double* Lb = M->L + (size_t)bkt * k * k;
-        for (int a = 0; a < k; ++a)
-            for (int b2 = 0; b2 < k; ++b2)
-                A[a * k + b2] = orc_kernel(kern, X + 3 * (size_t)S[a], X + 3 * (size_t)S[b2]) +
-                                (a == b2 ? kern->nugget : 0.0);
-        int st = chol_jitter(A, Lb, k, kern->variance);
+        for (int a = 0; a < kk; ++a)
+            for (int b2 = 0; b2 < kk; ++b2)
+                A[a * kk + b2] = orc_kernel(kern, X + 3 * (size_t)S[a], X + 3 * (size_t)S[b2]) +
+                                 (a == b2 ? kern->nugget : 0.0);
+        int st = kk > 0 ? chol_jitter(A, Lb, kk, kern->variance) : ORC_OK;
         if (st != ORC_OK) {
 #pragma omp critical
             status = st;
         } else {
-            double* r = malloc(sizeof(double) * k);
-            double* w = malloc(sizeof(double) * k);
-            for (int a = 0; a < k; ++a) r[a] = y[S[a]] - kern->prior_mean;
-            forward_sub(Lb, k, r, w);
-            backward_sub(Lb, k, w, M->alpha + (size_t)bkt * k);
+            double* r = malloc(sizeof(double) * (kk > 0 ? kk : 1));
+            double* w = malloc(sizeof(double) * (kk > 0 ? kk : 1));
+            for (int a = 0; a < kk; ++a) r[a] = y[S[a]] - kern->prior_mean;
+            forward_sub(Lb, kk, r, w);
+            backward_sub(Lb, kk, w, M->alpha + (size_t)bkt * k);
             free(r); free(w);
         }
         free(A);
@@ -361,7 +425,7 @@ int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const dou
 
 void orc_model_destroy(orc_model_t* M) {
     if (!M) return;
-    free(M->X); free(M->y); free(M->S); free(M->L); free(M->alpha); free(M->WAW);
+    free(M->X); free(M->y); free(M->S); free(M->kb); free(M->L); free(M->alpha); free(M->WAW);
     free(M->mu_obs); free(M->var_obs); free(M->obs_cell);
     free(M);
 }
@@ -472,13 +536,13 @@ int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, cons
 
 /* ------------------------------------------------------------------ C8 --- */
 int orc_cell_posterior(const orc_model_t* M, int64_t cell, double* mu, double* cov) {
-    int k = M->k;
     int64_t nx = M->grid.cells[0], ny = M->grid.cells[1];
     int32_t ci = (int32_t)(cell % nx), cj = (int32_t)((cell / nx) % ny), ck = (int32_t)(cell / (nx * ny));
     int32_t b = orc_vertex_bucket(M, ci, cj, ck);
-    const int32_t* S = M->S + (size_t)b * k;
-    const double* L = M->L + (size_t)b * k * k;
-    const double* al = M->alpha + (size_t)b * k;
+    int ks = M->k, k = set_size(M, b);
+    const int32_t* S = M->S + (size_t)b * ks;
+    const double* L = M->L + (size_t)b * ks * ks;
+    const double* al = M->alpha + (size_t)b * ks;
     double xc[8][3];
     for (int c = 0; c < 8; ++c) vertex_pos(M, ci + (c & 1), cj + ((c >> 1) & 1), ck + (c >> 2), xc[c]);
     double* K = malloc(sizeof(double) * 8 * k);
@@ -494,7 +558,7 @@ int orc_cell_posterior(const orc_model_t* M, int64_t cell, double* mu, double* c
         forward_sub(L, k, Kc, V + (size_t)c * k);
     }
     int st = ORC_OK;
-    const double* Cw = M->WAW ? M->WAW + (size_t)b * k * k : NULL;
+    const double* Cw = M->WAW ? M->WAW + (size_t)b * ks * ks : NULL;
     for (int c = 0; c < 8; ++c)
         for (int e = 0; e < 8; ++e) {
             double s = orc_kernel(&M->kern, xc[c], xc[e]);
@@ -721,10 +785,10 @@ static void kernel_grad(const orc_kernel_t* kern, const double* a, const double*
  * grad mu = sum_j grad k_j alpha_j; var = k(x,x) - v.v, v = L^-1 k_x;
  * grad var = -2 v . (L^-1 grad k); sigma = sqrt(max(var, floor)) (flat when floored). */
 static double local_f_grad(const orc_model_t* M, int32_t b, const double* x, double theta, double* gf) {
-    int k = M->k;
-    const int32_t* S = M->S + (size_t)b * k;
-    const double* L = M->L + (size_t)b * k * k;
-    const double* al = M->alpha + (size_t)b * k;
+    int ks = M->k, k = set_size(M, b);
+    const int32_t* S = M->S + (size_t)b * ks;
+    const double* L = M->L + (size_t)b * ks * ks;
+    const double* al = M->alpha + (size_t)b * ks;
     double* kv = malloc(sizeof(double) * k * 4);
     double* v = malloc(sizeof(double) * k * 4);
     double mu = M->kern.prior_mean, gmu[3] = {0, 0, 0};

@@ -56,6 +56,13 @@ int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const dou
                      const double* y, int64_t m, int32_t k, int32_t bucket_log2,
                      int32_t h_full, orc_model_t** out);
 void orc_model_destroy(orc_model_t* M);
+
+/* R28 (NEXT-2): box mode -- bucket b's local set is every observation
+ * inside the bucket box enlarged by beta l_d per axis (ascending index, at most k;
+ * ORC_EINVAL if a box holds more than k). */
+int orc_model_create_box(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
+                         const double* y, int64_t m, int32_t k, int32_t bucket_log2,
+                         int32_t h_full, double beta, orc_model_t** out);
 int32_t orc_model_nbuckets(const orc_model_t* M);
 int32_t orc_model_lfull(const orc_model_t* M);
 /* S_B of bucket b (ascending observation indices), k entries */
