@@ -77,6 +77,12 @@ typedef struct {
     int32_t brick_pass;    /* refine-time brick pass (vertex marginals + MC records of every
                               level-(Lfull-2) frontier brick): 0 = on when supported and the
                               records (208 B per cell) fit in free HBM, -1 = off */
+    int32_t local_mode;    /* bucket local sets: 0 = the k nearest observations to the bucket
+                              centre (R2, BASELINE); 1 = every observation inside the bucket box
+                              enlarged by beta * lengthscale per axis (R28),
+                              at most k of them (EINVAL otherwise), padded to k internally */
+    int32_t pad1_;
+    double beta;           /* local_mode 1: box enlargement in lengthscales (the paper uses 6) */
 } lcp_opts_t;
 
 /* per evaluated octree node (Alg. 1) */

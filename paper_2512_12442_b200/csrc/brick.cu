@@ -54,7 +54,7 @@ __device__ __forceinline__ double exp_neg_fast(double x) {
   for (int i = 11; i >= 0; --i) p = fma(p, f, c_exp_taylor[i]);
   const int ni = __double2loint(t);
   const double scale = __hiloint2double((ni + 1023) << 20, 0);
-  return ni < -1022 ? 0.0 : p * scale;
+  return (ni < -1022 || x > 745.0) ? 0.0 : p * scale;   // x > 745: also guards the magic-add range
 }
 
 // branch-free sqrt: MUFU.RSQ64H seed, two Newton steps on 1/sqrt, one on sqrt (~1 ulp);

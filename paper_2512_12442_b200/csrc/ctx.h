@@ -92,6 +92,7 @@ struct Ctx {
   DevBuf derr;               // device error flags (int)
   DevBuf knn_fail;           // int: buckets whose ring search overflowed
   int knn_fallbacks = 0;
+  int max_set = 0;            // box mode: largest bucket set
   int64_t n_launch = 0;      // kernels this ctx has launched (cumulative)
   int64_t n_vertices = 0;    // (nx+1)(ny+1)(nz+1)
   int64_t last_requests = 0; // vertex marginals computed by the last refine

@@ -234,6 +234,58 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g
   }
 }
 
+// a2, R28 box mode: bucket b's set = every observation inside the
+// bucket box enlarged by beta l_d per axis, ascending index, padded with -1 to k
+// (a padded slot is a decoupled far-away dummy in the factor: exact, see k_bucket_factor*).
+// Bounds left to right without FMA, as the oracle's.  cnt_max: the largest set.
+__global__ void __launch_bounds__(256) k_box_sets(Geom g, const double* __restrict__ X, int64_t m, int k,
+                                                  double bl0, double bl1, double bl2, int32_t* __restrict__ S,
+                                                  int* __restrict__ cnt_max) {
+  __shared__ int s_base;
+  __shared__ int s_wcnt[8];
+  const int b = blockIdx.x;
+  const int bi[3] = {b % g.nb[0], (b / g.nb[0]) % g.nb[1], b / (g.nb[0] * g.nb[1])};
+  const double bw[3] = {bl0, bl1, bl2};
+  double lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = __dsub_rn(__dadd_rn(g.lo[d], __dmul_rn((double)(bi[d] * g.bs), g.h[d])), bw[d]);
+    hi[d] = __dadd_rn(__dadd_rn(g.lo[d], __dmul_rn((double)((bi[d] + 1) * g.bs), g.h[d])), bw[d]);
+  }
+  int32_t* Sb = S + (int64_t)b * k;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int64_t i0 = 0; i0 < m; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    bool in = i < m;
+    for (int d = 0; d < 3 && in; ++d) {
+      const double x = X[3 * i + d];
+      in = x >= lo[d] && x < hi[d];
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) s_wcnt[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      before += w < wid ? s_wcnt[w] : 0;
+      total += s_wcnt[w];
+    }
+    const int slot = s_base + before + __popc(bal & ((1u << lane) - 1u));
+    if (in && slot < k) Sb[slot] = (int32_t)i;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base += total;
+    __syncthreads();
+  }
+  const int n = s_base;
+  for (int a = n + threadIdx.x; a < k; a += blockDim.x) Sb[a] = -1;
+  if (threadIdx.x == 0) atomicMax(cnt_max, n);
+}
+
+// padded slot a of a box set: a far-away dummy observation, decoupled from everything
+// (every kernel value with it is exactly 0, its own variance sigma_f^2 + nugget) with
+// value m0, so alpha_a = 0 and its row of L^-1 K is 0: the factor of the real set exactly
+__device__ __forceinline__ double dummy_coord(int a, int d) { return 1e20 * (double)(a + 1) * (double)(d + 1); }
+
 // a3: per-bucket factor.  Block layout in bdata: [L^-1 in the DMMA A-fragment
 // layout (la_size(k), common.cuh)] [alpha (k)] [x (k)] [y (k)] [z (k)].
 // USE_SMEM is a template parameter so that the factor and L^-1 live in pointers the
@@ -271,10 +323,17 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
   double* out = bdata + (int64_t)b * bstride;
   for (int a = tid; a < k; a += bd) {
     int64_t o = Sb[a];
-    sx[a] = X[3 * o];
-    sy[a] = X[3 * o + 1];
-    sz[a] = X[3 * o + 2];
-    rr[a] = yobs[o] - kp.m0;
+    if (o < 0) {   // R28 padding: decoupled far-away dummy (exact, see dummy_coord)
+      sx[a] = dummy_coord(a, 0);
+      sy[a] = dummy_coord(a, 1);
+      sz[a] = dummy_coord(a, 2);
+      rr[a] = 0.0;
+    } else {
+      sx[a] = X[3 * o];
+      sy[a] = X[3 * o + 1];
+      sz[a] = X[3 * o + 2];
+      rr[a] = yobs[o] - kp.m0;
+    }
     out[LA + k + a] = sx[a];
     out[LA + 2 * k + a] = sy[a];
     out[LA + 3 * k + a] = sz[a];
@@ -441,10 +500,17 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
   double* out = bdata + (int64_t)b * bstride;
   for (int a = tid; a < k; a += bd) {
     int64_t o = Sb[a];
-    sx[a] = X[3 * o];
-    sy[a] = X[3 * o + 1];
-    sz[a] = X[3 * o + 2];
-    rr[a] = yobs[o] - kp.m0;
+    if (o < 0) {   // R28 padding: decoupled far-away dummy (exact, see dummy_coord)
+      sx[a] = dummy_coord(a, 0);
+      sy[a] = dummy_coord(a, 1);
+      sz[a] = dummy_coord(a, 2);
+      rr[a] = 0.0;
+    } else {
+      sx[a] = X[3 * o];
+      sy[a] = X[3 * o + 1];
+      sz[a] = X[3 * o + 2];
+      rr[a] = yobs[o] - kp.m0;
+    }
     out[LA + k + a] = sx[a];
     out[LA + 2 * k + a] = sy[a];
     out[LA + 3 * k + a] = sz[a];
@@ -819,6 +885,8 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   o.keep_records = 0;
   o.extreme_iters = 0;
   if (opts) o = *opts;
+  if (o.local_mode != 0 && o.local_mode != 1) return set_err(c, LCP_EINVAL, "fit: bad local_mode");
+  if (o.local_mode == 1 && !(o.beta > 0.0)) return set_err(c, LCP_EINVAL, "fit: beta must be > 0");
   if (o.precision != LCP_FP64 && o.precision != LCP_FP32) return set_err(c, LCP_EINVAL, "fit: bad precision");
   if (o.precision == LCP_FP32 && k > 128) return set_err(c, LCP_EINVAL, "fit: the FP32 posterior needs k <= 128");
   if (o.extreme_iters < 0 || o.extreme_iters > 1000) return set_err(c, LCP_EINVAL, "fit: extreme_iters not in [0, 1000]");
@@ -917,7 +985,23 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   ++c.n_launch;
   CK(cudaGetLastError());
   // a2
-  {
+  if (o.local_mode == 1) {
+    if (AM) return set_err(c, LCP_EINVAL, "fit: the box local mode is for observations (lcp_fit_local)");
+    int* cmax = c.knn_fail.as<int>();
+    CK(cudaMemsetAsync(cmax, 0, sizeof(int), c.stream));
+    k_box_sets<<<nbk, 256, 0, c.stream>>>(g, X, m, k, o.beta * kern->lengthscale[0], o.beta * kern->lengthscale[1],
+                                          o.beta * kern->lengthscale[2], c.S.as<int32_t>(), cmax);
+    ++c.n_launch;
+    CK(cudaGetLastError());
+    int hmax = 0;
+    CK(cudaMemcpyAsync(&hmax, cmax, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    c.knn_fallbacks = 0;
+    c.max_set = hmax;
+    if (hmax > k)
+      return set_err(c, LCP_EINVAL, "fit: a beta-box holds " + std::to_string(hmax) + " observations > k = " +
+                                        std::to_string(k) + " (raise k or lower beta)");
+  } else {
     int r0 = 0;
     double dens = (double)m / nbk;
     while (r0 < 64 && std::pow(2.0 * r0 + 1.0, 3) * dens < (double)k) ++r0;

@@ -50,7 +50,8 @@ class GridT(C.Structure):
 class OptsT(C.Structure):
     _fields_ = [("bucket_log2", C.c_int32), ("h_full", C.c_int32), ("precision", C.c_int32),
                 ("slab_rank", C.c_int32), ("slab_count", C.c_int32), ("slab_level", C.c_int32),
-                ("keep_records", C.c_int32), ("extreme_iters", C.c_int32), ("brick_pass", C.c_int32)]
+                ("keep_records", C.c_int32), ("extreme_iters", C.c_int32), ("brick_pass", C.c_int32),
+                ("local_mode", C.c_int32), ("pad1_", C.c_int32), ("beta", C.c_double)]
 
 
 class InfoT(C.Structure):
@@ -152,7 +153,8 @@ class Context:
     # -- a1-a4
     def fit_local(self, xyz, y, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,
                   h_full: int = 2, precision: int = FP64, slab_rank: int = 0, slab_count: int = 1,
-                  slab_level: int = 3, keep_records=False, extreme_iters: int = 0, brick_pass: int = 0):
+                  slab_level: int = 3, keep_records=False, extreme_iters: int = 0, brick_pass: int = 0,
+                  local_mode: int = 0, beta: float = 6.0):
         """xyz (m,3) / y (m,) float64, either torch CUDA tensors or numpy host arrays.
         kernel = (kind, variance, lengthscale[3], nugget, prior_mean); grid = (lo, hi, cells).
         keep_records: True = every level, int L = levels < L (parity tap)."""
@@ -164,7 +166,7 @@ class Context:
         lo, hi, cells = grid
         gt = GridT((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int32 * 3)(*cells), 0)
         ot = OptsT(bucket_log2, h_full, precision, slab_rank, slab_count, slab_level,
-                   int(keep_records), int(extreme_iters), int(brick_pass))
+                   int(keep_records), int(extreme_iters), int(brick_pass), int(local_mode), 0, float(beta))
         if isinstance(xyz, np.ndarray):
             xyz = np.ascontiguousarray(xyz, np.float64)
             y = np.ascontiguousarray(y, np.float64)
@@ -187,7 +189,7 @@ class Context:
         kt = KernelT(int(kind), 0, float(var), (C.c_double * 3)(*ls), float(nug), float(m0))
         lo, hi, cells = grid
         gt = GridT((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int32 * 3)(*cells), 0)
-        ot = OptsT(bucket_log2, h_full, FP64, 0, 1, 3, int(keep_records), int(extreme_iters), 0)
+        ot = OptsT(bucket_log2, h_full, FP64, 0, 1, 3, int(keep_records), int(extreme_iters), 0, 0, 0, 0.0)
         if isinstance(xyz_M, np.ndarray):
             xyz_M = np.ascontiguousarray(xyz_M, np.float64)
             mu_M = np.ascontiguousarray(mu_M, np.float64)

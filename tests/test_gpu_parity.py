@@ -649,3 +649,50 @@ def test_zero_noise_interpolation_gpu(dev):
     mu, var = ctx.point_marginals(torch.from_numpy(X).to(dev))
     assert np.abs(mu.cpu().numpy() - y).max() <= 1e-6
     assert np.abs(var.cpu().numpy()).max() <= 1e-8
+
+
+@pytest.mark.parametrize("name,k,beta", [("t1", 60, 0.7), ("c2", 64, 0.3), ("t2", 90, 0.5)])
+def test_beta_box_local_mode(name, k, beta, dev):
+    # NEXT-2 / R28: the paper's beta-box local sets instead of k-NN:
+    # sets bit-exact (padding -1), posteriors, node sets and LCP against the oracle
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate(name)
+    cfg = w.cfg
+    kernel, grid, _, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    ctx = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, keep_records=True,
+                               local_mode=1, beta=beta)
+    kern = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, cfg.nugget, cfg.prior_mean)
+    M = O.Model.box(kern, O.make_grid(cfg.lo, cfg.hi, cfg.cells), w.X, w.y, k, b, hf, beta)
+    S = ctx.bucket_sets().cpu().numpy()
+    bad = [bb for bb in range(M.nbuckets) if not np.array_equal(S[bb], M.bucket_set(bb))]
+    assert not bad, bad[:5]
+    cells = random_cells(name, 200, 5)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    mu_g, cov_g = mu_g.cpu().numpy(), cov_g.cpu().numpy()
+    worst = (0.0, 0.0)
+    for q, cc in enumerate(cells[:80]):
+        mu_o, cov_o = M.cell_posterior(int(cc))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, cfg.variance, 1e-5)
+        worst = (max(worst[0], em), max(worst[1], ec))
+    assert worst[0] <= 1e-5 and worst[1] <= 1e-5, worst
+    th = w.thetas[0]
+    leaves_g = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy()
+    res = compare_node_sets(ctx.node_records(), M.octree(th, cfg.alpha, cfg.max_depth)[0], cfg.alpha)
+    assert not res["unexcused"], res
+    sel = leaves_g[:: max(1, len(leaves_g) // 400)]
+    lcp_g = ctx.pmc_cells(torch.from_numpy(sel).to(dev), th, 800, 7).cpu().numpy()
+    lcp_o = M.pmc_cells(sel, th, 800, 7)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, 800)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_beta_box_too_small_k_is_einval(dev):
+    from paper_2512_12442_b200 import Context, LcpError, config_args
+    from paper_2512_12442_b200.lcp import LCP_EINVAL
+    w = generate("t1")
+    kernel, grid, k, b, hf = config_args(w.cfg)
+    with pytest.raises(LcpError) as e:
+        Context(0).fit_local(w.X, w.y, kernel, 3, grid, bucket_log2=b, h_full=hf, local_mode=1, beta=3.0)
+    assert e.value.status == LCP_EINVAL
