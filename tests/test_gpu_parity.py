@@ -696,3 +696,27 @@ def test_beta_box_too_small_k_is_einval(dev):
     with pytest.raises(LcpError) as e:
         Context(0).fit_local(w.X, w.y, kernel, 3, grid, bucket_log2=b, h_full=hf, local_mode=1, beta=3.0)
     assert e.value.status == LCP_EINVAL
+
+
+def test_full_model_leaf_posterior_two_contexts(dev):
+    # NEXT-2: the octree uses the local models, the leaves the full
+    # model.  A second context with k = m (one bucket) evaluates the leaves the
+    # first context's refine returns (device pointer, same GPU).
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate("c3")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    local = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    full = Context(0).fit_local(X, y, kernel, cfg.m, grid, bucket_log2=0, h_full=hf)
+    th = w.thetas[0]
+    leaves = local.octree_refine(th, cfg.alpha, cfg.max_depth).clone()
+    lcp = full.pmc_cells(leaves, th, 1000, cfg.mc_seed)
+    assert full.stats()["pmc_used_records"] == 0
+    M = O.Model.from_config(cfg, w.X, w.y, k=cfg.m, bucket_log2=0)
+    lv = leaves.cpu().numpy()
+    sel = np.random.default_rng(8).choice(len(lv), 150, replace=False)
+    lcp_o = M.pmc_cells(lv[sel], th, 1000, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(lcp.cpu().numpy()[sel], lcp_o, 1000)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
