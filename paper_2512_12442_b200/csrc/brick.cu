@@ -351,7 +351,7 @@ static size_t brick_smem(int k) {
 }
 
 bool fused_brick_supported(const Ctx& c) {
-  return c.k <= 128 && c.g.bs >= BK && brick_smem(c.k) <= 227 * 1024 && c.opts.precision != LCP_FP32 &&
+  return c.k <= 128 && c.g.bs >= BK && brick_smem(c.k) + 64 <= 227 * 1024 && c.opts.precision != LCP_FP32 &&
          c.g.lfull >= 2;
 }
 
@@ -575,7 +575,9 @@ bool brick_posterior_big(Ctx& c, const int64_t* cells, int64_t n, double* post, 
   if (c.k <= 128 || c.k > BIG_KMAX || c.g.bs < BK || c.g.lfull < 2 || 3 * (c.g.lfull - 2) > 30) return false;
   const int k = c.k, kp8 = (k + 7) & ~7;
   const int64_t nbr = (int64_t)1 << (3 * (c.g.lfull - 2));
-  if ((err = c.cell_bucket.ensure(sizeof(int32_t) * n)) != cudaSuccess) return false;
+  // own key buffer: the caller's per-cell bucket ids (c.cell_bucket) must survive a
+  // decline (too few cells per brick) for the per-cell fallback
+  if ((err = c.brick_key.ensure(sizeof(int32_t) * n)) != cudaSuccess) return false;
   if ((err = c.perm.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
   if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
   if ((err = c.brick_idx.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
@@ -583,7 +585,7 @@ bool brick_posterior_big(Ctx& c, const int64_t* cells, int64_t n, double* post, 
   if ((err = c.goff.ensure(sizeof(int64_t) * (nbr + 1))) != cudaSuccess) return false;
   if ((err = c.counters.ensure(sizeof(unsigned long long) * 16)) != cudaSuccess) return false;
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
-  int32_t* key = c.cell_bucket.as<int32_t>();
+  int32_t* key = c.brick_key.as<int32_t>();
   int64_t* pm = c.perm.as<int64_t>();
   const unsigned gr = (unsigned)((n + 255) / 256);
   k_brick_keys<<<gr, 256, 0, c.stream>>>(c.g, cells, n, key);
@@ -628,7 +630,7 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
   if (c.k > 128 || c.g.bs < BK) return false;
   const int k = c.k;
   size_t smem = brick_smem(k);
-  if (smem > 227 * 1024) return false;
+  if (smem + 64 > 227 * 1024) return false;
   if ((err = c.brick_flag.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
   if ((err = c.brick_idx.ensure(sizeof(int64_t) * n)) != cudaSuccess) return false;
   if ((err = c.counters.ensure(sizeof(unsigned long long) * 16)) != cudaSuccess) return false;

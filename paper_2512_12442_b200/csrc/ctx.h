@@ -116,7 +116,7 @@ struct Ctx {
   int64_t n_recs = 0;
 
   // leaf pass scratch
-  DevBuf cell_bucket, perm, cells_tmp, post, lcp_tmp, field_tmp;
+  DevBuf cell_bucket, brick_key, perm, cells_tmp, post, lcp_tmp, field_tmp;
   DevBuf brick_flag, brick_idx, brick_start;
   DevBuf vscratch;               // k_brick_big: per-CTA V scratch (L2-resident)
   // refine-time brick pass (brick.cu k_brick<true>): MC records of every cell of the

@@ -455,8 +455,26 @@ static TileArgs make_tile_args(Ctx& c) {
 }
 
 // shared-memory plan: staged bucket block (if it fits) + W per-warp buffers
+// static shared memory of the tile kernels (tile_loop's run table): the dynamic
+// cap is 227 KB minus this (a launch over the opt-in limit fails with "invalid argument")
+static size_t tile_static_smem() {
+  static const size_t v = [] {
+    size_t mx = 0;
+    const void* fs[] = {(const void*)k_marginals<0>, (const void*)k_marginals<1>,
+                        (const void*)k_cell_posterior<0>, (const void*)k_cell_posterior<1>,
+                        (const void*)k_cell_posterior_f32<0>, (const void*)k_cell_posterior_f32<1>};
+    for (const void* f : fs) {
+      cudaFuncAttributes at{};
+      if (cudaFuncGetAttributes(&at, f) == cudaSuccess) mx = std::max(mx, (size_t)at.sharedSizeBytes);
+    }
+    cudaGetLastError();
+    return mx;
+  }();
+  return v;
+}
+
 static void plan_tile(const Ctx& c, int& staged, int& warps, size_t& smem) {
-  const size_t cap = 220 * 1024;
+  const size_t cap = std::min<size_t>(220 * 1024, 227 * 1024 - tile_static_smem() - 512);
   int64_t k = c.k;
   const int64_t ks = k + ((4 - k % 16) + 16) % 16;
   size_t per_warp = sizeof(double) * (8 * ks + (k > ROWS_PER_GROUP ? 8 * ROWS_PER_GROUP : 0) + 24);

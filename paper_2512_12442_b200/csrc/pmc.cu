@@ -117,9 +117,14 @@ __global__ void k_cells_covered(Geom g, const int64_t* __restrict__ cells, int64
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool miss = false;
   if (q < n) {
-    int i, j, k;
-    cell_ijk(g, cells[q], i, j, k);
-    miss = !bdone[morton3(i >> 2, j >> 2, k >> 2)];
+    const int64_t cell = cells[q];
+    if (cell < 0 || cell >= (int64_t)g.cells[0] * g.cells[1] * g.cells[2]) {
+      miss = true;   // invalid id: take the posterior path, which reports it
+    } else {
+      int i, j, k;
+      cell_ijk(g, cell, i, j, k);
+      miss = !bdone[morton3(i >> 2, j >> 2, k >> 2)];
+    }
   }
   if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(cov, 1ull);
 }
@@ -511,6 +516,8 @@ lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* pos
   unsigned gr = (unsigned)((n + 255) / 256);
   k_cell_bucket<<<gr, 256, 0, c.stream>>>(c.g, cells, n, bkt, c.derr.as<int>());
   ++c.n_launch;
+  // reject out-of-range ids before any brick kernel indexes by them
+  if (lcp_status_t st = check_device_errors(c); st != LCP_OK) return st;
   c.last_brick_runs = 0;
   static const bool force_cell = [] {
     const char* v = std::getenv("LCP_POSTERIOR");

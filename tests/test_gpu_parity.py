@@ -720,3 +720,48 @@ def test_full_model_leaf_posterior_two_contexts(dev):
     lcp_o = M.pmc_cells(lv[sel], th, 1000, cfg.mc_seed)
     frac, mean, mx = lcp_parity(lcp.cpu().numpy()[sel], lcp_o, 1000)
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_big_k_sparse_cell_list(dev):
+    # k > 128 and too few cells per brick for k_brick_big: the declined brick path
+    # must leave the per-cell bucket ids intact for the per-cell fallback
+    w, ctx, M = _ctx("c3", dev, k=200, keep_records=False)
+    cells = random_cells("c3", 64, 21)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    mu_g, cov_g = mu_g.cpu().numpy(), cov_g.cpu().numpy()
+    assert ctx.stats()["brick_runs"] == 0
+    for q, c in enumerate(cells):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, w.cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(c), em, ec)
+    with pytest.raises(Exception):
+        ctx.cell_posterior(torch.tensor([0, int(np.prod(w.cfg.cells))], device=dev, dtype=torch.int64))
+
+
+@pytest.mark.parametrize("k", [129, 256, 409, 512, 640])
+def test_k_sweep_tile_kernels(k, dev):
+    # large k through the per-cell / marginal tile kernels (dynamic + static shared
+    # memory under the 227 KB opt-in limit at every k) and the big-k brick
+    w, ctx, M = _ctx("p1", dev, k=k, bucket_log2=1, keep_records=False)
+    cfg = w.cfg
+    cells = random_cells("p1", 24, k)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    mu_g, cov_g = mu_g.cpu().numpy(), cov_g.cpu().numpy()
+    for q, c in enumerate(cells):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(c), em, ec)
+    P = np.asarray(cfg.lo) + (np.asarray(cfg.hi) - np.asarray(cfg.lo)) * np.random.default_rng(k).random((40, 3))
+    mp, vp = ctx.point_marginals(torch.from_numpy(P).to(dev))
+    mo = np.array([M.local_marginal(M.point_bucket(p), p) for p in P])
+    em, ev = posterior_close(mp.cpu().numpy(), mo[:, 0], vp.cpu().numpy(), mo[:, 1], cfg.variance, 1e-5)
+    assert em <= 1e-5 and ev <= 1e-5, (em, ev)
+    nx, ny = cfg.cells[0], cfg.cells[1]
+    ii, jj, kk = np.meshgrid(np.arange(4), np.arange(4), np.arange(4), indexing="ij")
+    brick = (ii + nx * (jj + ny * kk)).ravel().astype(np.int64)   # one full 4^3 brick: the big-k brick path
+    mu_b, cov_b = ctx.cell_posterior(torch.from_numpy(brick).to(dev))
+    assert ctx.stats()["brick_runs"] == 1
+    for q in (0, 17, 63):
+        mu_o, cov_o = M.cell_posterior(int(brick[q]))
+        em, ec = posterior_close(mu_b[q].cpu().numpy(), mu_o, cov_b[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (q, em, ec)
