@@ -200,3 +200,146 @@ def test_fuzz_options(seed):
         off = np.ones(F.shape[1], bool)
         off[cells_u[(mask_u >> t) & 1 == 1]] = False
         assert np.all(F[t][off] == 0)
+
+
+def _draw_large(seed):
+    """Larger grids (48..130 cells per axis) with bucket sides >= 4 cells, so the
+    refine-time brick pass, the cell records and the chunked leaf pass are active."""
+    g = np.random.default_rng(30_000 + seed)
+    d = _draw(1000 + seed)
+    cells = tuple(int(c) for c in g.integers(40, 101, 3))
+    lo = np.asarray(d["lo"])
+    hi = lo + g.uniform(0.8, 2.5, 3)
+    m = int(g.integers(500, 5001))
+    X = lo + (hi - lo) * g.random((m, 3))
+    nb = 6
+    cen = lo + (hi - lo) * g.random((nb, 3))
+    amp = g.uniform(-1.0, 1.0, nb)
+    wid = g.uniform(0.1, 0.35, nb) * float(np.min(hi - lo))
+    d2 = ((X[:, None, :] - cen[None]) ** 2).sum(-1)
+    y = (amp * np.exp(-d2 / (2 * wid ** 2))).sum(-1) + 0.01 * g.standard_normal(m)
+    lfull = math.ceil(math.log2(max(cells)))
+    ls = tuple(float(v) for v in g.uniform(0.04, 0.15, 3) * (hi - lo))
+    q = np.sort(g.uniform(0.3, 0.7, 3))
+    return dict(d, cells=cells, lo=tuple(lo), hi=tuple(hi), X=X, y=y, ls=ls,
+                nug=float(10 ** g.uniform(-4, -2)), k=int(g.integers(16, 129)),
+                b=int(g.integers(2, lfull - 1)), h_full=int(g.integers(1, 4)),
+                max_depth=int(g.integers(lfull - 1, lfull + 1)), alpha=float(10 ** g.uniform(-2, -0.7)),
+                thetas=[float(v) for v in np.quantile(y, q)], N=int(g.choice([1000, 4096])))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_large(seed):
+    from paper_2512_12442_b200 import Context
+    d = _draw_large(seed)
+    dev = torch.device("cuda:0")
+    kernel = (d["kind"], d["var"], d["ls"], d["nug"], d["m0"])
+    grid = (d["lo"], d["hi"], d["cells"])
+    X, y = torch.from_numpy(d["X"]).to(dev), torch.from_numpy(d["y"]).to(dev)
+    ctx = Context(0).fit_local(X, y, kernel, d["k"], grid, bucket_log2=d["b"], h_full=d["h_full"],
+                               keep_records=True)
+    M = O.Model(O.make_kernel(d["kind"], d["var"], d["ls"], d["nug"], d["m0"]),
+                O.make_grid(d["lo"], d["hi"], d["cells"]), d["X"], d["y"], d["k"], d["b"], d["h_full"])
+    th, alpha, md, N = d["thetas"][0], d["alpha"], d["max_depth"], d["N"]
+    ncell = int(np.prod(d["cells"]))
+    lvl = ctx.set_level_field(torch.empty(ncell, dtype=torch.uint8, device=dev))
+    leaves = ctx.octree_refine(th, alpha, md).clone()
+    ctx.set_level_field(None)
+    rec_o, leaves_o = M.octree(th, alpha, md)
+    res = compare_node_sets(ctx.node_records(), rec_o, alpha)
+    assert not res["unexcused"], res["unexcused"][:10]
+    lv = leaves.cpu().numpy()
+    exact_sets = res["excused"] == 0
+    if exact_sets:
+        np.testing.assert_array_equal(np.sort(lv), leaves_o)
+    # level field: leaf cells carry max_depth; a sample of all cells against the level of
+    # the oracle's node that stopped them (pruned, or at max_depth)
+    L = lvl.cpu().numpy()
+    assert np.all(L[lv] == md) and np.all(L <= md)
+    rng = np.random.default_rng(seed)
+    if exact_sets:
+        stop = {(int(r["level"]), int(r["i"]), int(r["j"]), int(r["k"])) for r in rec_o
+                if not r["refine"] or int(r["level"]) == md}
+        nx, ny, _ = d["cells"]
+        lf = M.lfull
+        for c in rng.choice(ncell, 2000, replace=False):
+            ci, cj, ck = c % nx, (c // nx) % ny, c // (nx * ny)
+            want = next(Lv for Lv in range(md + 1)
+                        if (Lv, ci >> (lf - Lv), cj >> (lf - Lv), ck >> (lf - Lv)) in stop)
+            assert L[c] == want, (int(c), int(L[c]), want)
+    st = ctx.stats()
+    # sampled posterior and LCP of the leaves (records path when the brick pass ran)
+    sel = np.sort(rng.choice(len(lv), min(2000, len(lv)), replace=False))
+    lcp_full = ctx.pmc_cells(leaves, th, N, d["seed"])
+    assert ctx.stats()["pmc_used_records"] == st["fused"]
+    lcp_o = M.pmc_cells(lv[sel], th, N, d["seed"])
+    frac, mean, mx = lcp_parity(lcp_full.cpu().numpy()[sel], lcp_o, N)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+    mu_g, cov_g = ctx.cell_posterior(leaves[torch.from_numpy(sel[:48]).to(dev)])
+    for q, c in enumerate(lv[sel[:48]]):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, d["var"], 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(c), em, ec)
+    # z-slab decomposition on one GPU: the sum of the slab fields is the full field, bit for bit
+    f_full, _ = ctx.run_field(th, alpha, md, N, d["seed"])
+    G, sl = int(rng.integers(2, 5)), int(rng.integers(1, 4))
+    acc = torch.zeros_like(f_full)
+    for r in range(G):
+        cs = Context(0).fit_local(X, y, kernel, d["k"], grid, bucket_log2=d["b"], h_full=d["h_full"],
+                                  slab_rank=r, slab_count=G, slab_level=sl)
+        f, _ = cs.run_field(th, alpha, md, N, d["seed"])
+        acc += f
+    assert torch.equal(acc, f_full)
+    # fused three-isovalue pass, sampled
+    fields, nls, nu = ctx.run_field_multi(d["thetas"], alpha, md, N, d["seed"], 1)
+    cu, mu_ = ctx.union_cells()
+    cu, mu_ = cu.cpu().numpy(), mu_.cpu().numpy()
+    s2 = np.sort(rng.choice(len(cu), min(1500, len(cu)), replace=False))
+    lcp_m = M.pmc_cells_multi(cu[s2], d["thetas"], N, d["seed"], 1, mask=mu_[s2].astype(np.uint32))
+    F = fields.cpu().numpy()
+    for t in range(3):
+        frac, mean, mx = lcp_parity(F[t][cu[s2]], lcp_m[t], N)
+        assert frac >= 0.999 and mean <= 1e-4, (t, frac, mean, mx)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_fuzz_sgpr(seed):
+    # NEXT-2 on random draws: inducing points = the observations, (mu_M, A_M) the
+    # exact GP posterior at them under a larger noise (the oracle's literal Eq. 1)
+    from paper_2512_12442_b200 import Context
+    d = _draw(200 + seed)
+    dev = torch.device("cuda:0")
+    sn2 = max(d["nug"], 1e-4) * 10.0
+    kern_gp = O.make_kernel(d["kind"], d["var"], d["ls"], sn2, d["m0"])
+    Xm = d["X"]
+    K = np.array([[O.kernel_value(kern_gp, a, b) for b in Xm] for a in Xm])
+    Ky = K + sn2 * np.eye(len(Xm))
+    muM = d["m0"] + K @ np.linalg.solve(Ky, d["y"] - d["m0"])
+    AM = sn2 * K @ np.linalg.inv(Ky)
+    AM = 0.5 * (AM + AM.T)
+    jitter = 1e-9 * d["var"]
+    kernel = (d["kind"], d["var"], d["ls"], jitter, d["m0"])
+    grid = (d["lo"], d["hi"], d["cells"])
+    ctx = Context(0).fit_sgpr(torch.from_numpy(Xm).to(dev), torch.from_numpy(muM).to(dev),
+                              torch.from_numpy(AM).to(dev), kernel, d["k"], grid, bucket_log2=d["b"],
+                              h_full=d["h_full"], keep_records=True)
+    M = O.Model.sgpr(O.make_kernel(d["kind"], d["var"], d["ls"], jitter, d["m0"]),
+                     O.make_grid(d["lo"], d["hi"], d["cells"]), Xm, muM, AM, d["k"], d["b"], d["h_full"])
+    th, alpha, md, N = d["thetas"][0], d["alpha"], d["max_depth"], d["N"]
+    leaves = ctx.octree_refine(th, alpha, md).clone()
+    rec_o, leaves_o = M.octree(th, alpha, md)
+    res = compare_node_sets(ctx.node_records(), rec_o, alpha)
+    assert not res["unexcused"], res["unexcused"][:10]
+    lv = leaves.cpu().numpy()
+    if len(lv) == 0:
+        return
+    sel = np.random.default_rng(seed).choice(len(lv), min(48, len(lv)), replace=False)
+    mu_g, cov_g = ctx.cell_posterior(leaves[torch.from_numpy(sel).to(dev)])
+    for q, c in enumerate(lv[sel]):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, d["var"], 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(c), em, ec)
+    lcp_g = ctx.pmc_cells(leaves, th, N, d["seed"]).cpu().numpy()
+    lcp_o = M.pmc_cells(lv, th, N, d["seed"])
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, N)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
