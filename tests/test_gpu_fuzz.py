@@ -343,3 +343,49 @@ def test_fuzz_sgpr(seed):
     lcp_o = M.pmc_cells(lv, th, N, d["seed"])
     frac, mean, mx = lcp_parity(lcp_g, lcp_o, N)
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_cell_lists(seed):
+    # lcp_pmc_cells / lcp_cell_posterior on arbitrary lists: duplicates, unsorted,
+    # Morton-sorted dense blocks with repeats, host pointers; before and after a refine
+    # (after it the brick-pass records may serve the list)
+    from paper_2512_12442_b200 import Context
+    d = _draw(300 + seed)
+    dev = torch.device("cuda:0")
+    kernel = (d["kind"], d["var"], d["ls"], d["nug"], d["m0"])
+    grid = (d["lo"], d["hi"], d["cells"])
+    ctx = Context(0).fit_local(d["X"], d["y"], kernel, d["k"], grid, bucket_log2=d["b"], h_full=d["h_full"])
+    M = O.Model(O.make_kernel(d["kind"], d["var"], d["ls"], d["nug"], d["m0"]),
+                O.make_grid(d["lo"], d["hi"], d["cells"]), d["X"], d["y"], d["k"], d["b"], d["h_full"])
+    ncell = int(np.prod(d["cells"]))
+    g = np.random.default_rng(seed)
+    nx, ny, nz = d["cells"]
+    ii, jj, kk = np.meshgrid(np.arange(min(nx, 8)), np.arange(min(ny, 8)), np.arange(min(nz, 8)), indexing="ij")
+    block = (ii + nx * (jj + ny * kk)).ravel().astype(np.int64)
+    lists = {
+        "dups": g.integers(0, ncell, 700).astype(np.int64),
+        "block_rep": np.repeat(block, 2),
+        "reversed": np.arange(ncell, dtype=np.int64)[::-1].copy(),
+    }
+    th, N = d["thetas"][0], d["N"]
+    for phase in ("fit", "refined"):
+        if phase == "refined":
+            ctx.octree_refine(th, d["alpha"], d["max_depth"])
+        for name, cells in lists.items():
+            out = np.zeros(len(cells), np.float32)
+            ctx.pmc_cells(cells, th, N, d["seed"], 3, out=out)          # host in / host out
+            lo = M.pmc_cells(cells, th, N, d["seed"], 3)
+            frac, mean, mx = lcp_parity(out, lo, N)
+            assert frac >= 0.999 and mean <= 1e-4, (phase, name, frac, mean, mx)
+            # duplicates carry identical values
+            first = {}
+            for q, c in enumerate(cells.tolist()):
+                if c in first:
+                    assert out[q] == out[first[c]], (phase, name, c)
+                else:
+                    first[c] = q
+        mu, cov = ctx.cell_posterior(torch.from_numpy(lists["block_rep"]).to(dev))
+        assert torch.equal(mu[0::2], mu[1::2]) and torch.equal(cov[0::2], cov[1::2])
+    # empty list is a no-op
+    ctx.pmc_cells(np.zeros(0, np.int64), th, N, d["seed"], 0, out=np.zeros(0, np.float32))
