@@ -389,3 +389,42 @@ def test_fuzz_cell_lists(seed):
         assert torch.equal(mu[0::2], mu[1::2]) and torch.equal(cov[0::2], cov[1::2])
     # empty list is a no-op
     ctx.pmc_cells(np.zeros(0, np.int64), th, N, d["seed"], 0, out=np.zeros(0, np.float32))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fuzz_context_reuse(seed):
+    # one context refitted with a sequence of different models (grid, k, buckets,
+    # kernel, local mode): every cache (vertex cache, brick flags, cell records, leaf
+    # and union lists) must follow the current fit
+    from paper_2512_12442_b200 import Context
+    dev = torch.device("cuda:0")
+    ctx = Context(0)
+    for it in range(6):
+        d = _draw_large(40 + 10 * seed + it) if it % 3 == 1 else _draw(400 + 10 * seed + it)
+        lm = int(it % 4 == 3)
+        kernel = (d["kind"], d["var"], d["ls"], d["nug"], d["m0"])
+        grid = (d["lo"], d["hi"], d["cells"])
+        k = len(d["y"]) if lm else d["k"]
+        ctx.fit_local(torch.from_numpy(d["X"]).to(dev), torch.from_numpy(d["y"]).to(dev), kernel, k, grid,
+                      bucket_log2=d["b"], h_full=d["h_full"], keep_records=(it % 2 == 0), local_mode=lm, beta=0.8)
+        ko = O.make_kernel(d["kind"], d["var"], d["ls"], d["nug"], d["m0"])
+        go = O.make_grid(d["lo"], d["hi"], d["cells"])
+        M = (O.Model.box(ko, go, d["X"], d["y"], k, d["b"], d["h_full"], 0.8) if lm
+             else O.Model(ko, go, d["X"], d["y"], k, d["b"], d["h_full"]))
+        th, alpha, md, N = d["thetas"][0], d["alpha"], d["max_depth"], d["N"]
+        for rep in range(2):                 # the second refine reuses this fit's brick records
+            if it % 2 == 0:
+                f, nl = ctx.run_field(th, alpha, md, N, d["seed"])
+                leaves = ctx.octree_refine(th, alpha, md).clone()
+            else:
+                fields, nls, nu = ctx.run_field_multi([th, d["thetas"][1]], alpha, md, N, d["seed"], 0)
+                f = fields[0]
+                leaves = ctx.octree_refine(th, alpha, md).clone()
+            lv = leaves.cpu().numpy()
+            _, leaves_o = M.octree(th, alpha, md)
+            assert abs(len(lv) - len(leaves_o)) <= max(2, len(leaves_o) // 1000), (it, len(lv), len(leaves_o))
+            common = np.intersect1d(lv, leaves_o)
+            sel = np.sort(np.random.default_rng(it).choice(len(common), min(1500, len(common)), replace=False))
+            lcp_o = M.pmc_cells(common[sel], th, N, d["seed"])
+            frac, mean, mx = lcp_parity(f[torch.from_numpy(common[sel]).to(dev)].cpu().numpy(), lcp_o, N)
+            assert frac >= 0.999 and mean <= 1e-4, (it, rep, frac, mean, mx)
