@@ -161,8 +161,9 @@ lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold
  * brick-pass records of an earlier refine skip the posterior and factor; the
  * results are bit-identical either way.  Asynchronous on the ctx stream when
  * both pointers are device pointers (one 8-byte coverage read-back).
- * Errors: ESTATE, EINVAL (n_samples < 1, cell id out of range -> ENUMERIC-free
- * check on the host only when cells_on_device == 0), ENUMERIC, ECUDA. */
+ * Errors: ESTATE; EINVAL (n_samples < 1 or > 2^31; a cell id outside
+ * [0, nx*ny*nz): detected on the device before any kernel indexes by it and
+ * reported by this call); ENUMERIC; ECUDA. */
 lcp_status_t lcp_pmc_cells(lcp_ctx_t* ctx, const int64_t* cells, int64_t n_cells,
                            int32_t cells_on_device, double isovalue, int64_t n_samples,
                            uint64_t seed, uint32_t iso_index, float* lcp_out,
@@ -228,7 +229,9 @@ lcp_status_t lcp_set_level_field(lcp_ctx_t* ctx, uint8_t* level_dev);
  * Morton order within a level; ctx-owned device array. */
 lcp_status_t lcp_node_records(lcp_ctx_t* ctx, int64_t* n_out, const lcp_node_rec_t** recs_dev_out);
 
-/* FP64 posterior of cells: mu_dev n*8, cov_dev n*64 (row-major 8x8), device. */
+/* FP64 posterior of cells (a7, as the leaf pass computes it): mu_dev n*8,
+ * cov_dev n*64 (row-major 8x8), device.  Any list (duplicates allowed).
+ * Errors: ESTATE, EINVAL (cell id out of range), ENUMERIC, ECUDA. */
 lcp_status_t lcp_cell_posterior(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_t n,
                                 double* mu_dev, double* cov_dev);
 
@@ -237,7 +240,8 @@ lcp_status_t lcp_cell_posterior(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_
 lcp_status_t lcp_point_marginals(lcp_ctx_t* ctx, const double* xyz_dev, int64_t n,
                                  const int32_t* bucket_dev, double* mu_dev, double* var_dev);
 
-/* the k-NN set of every bucket (nbuckets x k int32, ascending), device */
+/* the local set of every bucket (nbuckets x k int32, ascending observation
+ * indices; local_mode 1 pads a set smaller than k with -1), device */
 lcp_status_t lcp_bucket_sets(lcp_ctx_t* ctx, int32_t* sets_dev);
 
 lcp_status_t lcp_get_info(lcp_ctx_t* ctx, lcp_info_t* out);
