@@ -463,6 +463,15 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
 //   X_IJ = -T_I S_J, X_II = T_I.
 // 3 + 2 barriers per block (vs 5 per column unblocked).  Same jitter retry (R15).
 constexpr int FB = 8;                  // block size
+
+// 1 / sqrt(x), x > 0: MUFU.RSQ64H seed and two Newton steps (~1 ulp); NaN for x <= 0
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  return x > 0.0 ? y : __longlong_as_double(0x7ff8000000000000ll);
+}
 __device__ __forceinline__ void dmma_f(double a, double b, double& d0, double& d1) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
@@ -520,17 +529,18 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
   for (int attempt = 0; attempt < 4 && !ok; ++attempt) {
     const double jit = attempt == 0 ? 0.0 : 1e-10 * kp.var * (attempt == 1 ? 1.0 : attempt == 2 ? 10.0 : 100.0);
     __syncthreads();
-    for (int e = tid; e < KP * KP; e += bd) {
-      const int i = e / KP, j = e - i * KP;
-      if (j > i) continue;
-      double v;
+    // lower triangle of K_y (+ identity padding rows), warp per row, lanes over columns
+    for (int i = wid; i < KP; i += nw) {
+      double* Ai = A + (int64_t)i * ST;
       if (i < k) {
-        const double r2 = kern_r2(kp, sx[i] - sx[j], sy[i] - sy[j], sz[i] - sz[j]);
-        v = kern_from_r2(kp, r2) + (i == j ? kp.nugget + jit : 0.0);
+        const double xi = sx[i], yi = sy[i], zi = sz[i];
+        for (int j = lane; j <= i; j += 32) {
+          const double r2 = kern_r2(kp, xi - sx[j], yi - sy[j], zi - sz[j]);
+          Ai[j] = kern_from_r2(kp, r2) + (i == j ? kp.nugget + jit : 0.0);
+        }
       } else {
-        v = i == j ? 1.0 : 0.0;
+        for (int j = lane; j <= i; j += 32) Ai[j] = i == j ? 1.0 : 0.0;
       }
-      A[(int64_t)i * ST + j] = v;
     }
     if (tid == 0) s_ok = 1;
     __syncthreads();
@@ -542,13 +552,16 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
 #pragma unroll
         for (int c = 0; c < FB; ++c) d[c] = (lane < FB && c <= lane) ? D[lane * ST + c] : 0.0;
         bool bad = false;
+        double rp[FB];   // 1 / pivot (every lane): the panel solve below multiplies
 #pragma unroll
         for (int j = 0; j < FB; ++j) {
           const double pj = __shfl_sync(0xffffffffu, d[j], j);
           if (!(pj > 0.0)) bad = true;
-          const double piv = sqrt(pj);
+          const double rinv = rsqrt_nr(pj);
+          rp[j] = rinv;
+          const double piv = pj * rinv;
           if (lane == j) d[j] = piv;
-          else if (lane > j && lane < FB) d[j] = d[j] / piv;
+          else if (lane > j && lane < FB) d[j] = d[j] * rinv;
 #pragma unroll
           for (int c = j + 1; c < FB; ++c) {
             const double lcj = __shfl_sync(0xffffffffu, d[j], c);
@@ -569,7 +582,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
             double sacc = (p == lane) ? 1.0 : 0.0;
 #pragma unroll
             for (int q = 0; q < p; ++q) sacc = fma(-D[p * ST + q], t[q], sacc);
-            t[p] = p < lane ? 0.0 : sacc / D[p * ST + p];
+            t[p] = p < lane ? 0.0 : sacc * rp[p];
           }
           double* T = sT + J * FB * 12;
 #pragma unroll
@@ -595,11 +608,12 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
       __syncthreads();
       // (3) trailing: A_{I1,I2} -= A_{I1,J} A_{I2,J}^T for J < I2 <= I1
       {
-        const int m = nb - J - 1;
-        int idx = 0;
-        for (int i1 = 0; i1 < m; ++i1)
-          for (int i2 = 0; i2 <= i1; ++i2, ++idx) {
-            if ((idx % nw) != wid) continue;
+        const int m = nb - J - 1, npair = m * (m + 1) / 2;
+        for (int idx = wid; idx < npair; idx += nw) {   // pair idx = i1 (i1 + 1) / 2 + i2, i2 <= i1
+            int i1 = (int)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+            while ((i1 + 1) * (i1 + 2) / 2 <= idx) ++i1;
+            while (i1 * (i1 + 1) / 2 > idx) --i1;
+            const int i2 = idx - i1 * (i1 + 1) / 2;
             const int I1 = J + 1 + i1, I2 = J + 1 + i2;
             const double* P1 = Ab(I1, J);
             const double* P2 = Ab(I2, J);
@@ -669,15 +683,14 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams k
     for (int i = j; i < k; ++i) sacc = fma(A[(int64_t)i * ST + j], vv[i], sacc);
     out[LA + j] = sacc;
   }
-  for (int64_t e = tid; e < LA; e += bd) {
-    const int64_t blk = e >> 5;
-    const int ln = (int)(e & 31);
-    int rt = (int)((sqrt(4.0 * (double)blk + 1.0) - 1.0) * 0.5);
+  // L^-1 as DMMA A-fragments: warp per 32-double block (row tile rt, column step js)
+  for (int64_t blk = wid; blk < (LA >> 5); blk += nw) {
+    int rt = (int)((sqrtf(4.0f * (float)blk + 1.0f) - 1.0f) * 0.5f);
     while ((int64_t)(rt + 1) * (rt + 2) <= blk) ++rt;
     while ((int64_t)rt * (rt + 1) > blk) --rt;
     const int js = (int)(blk - (int64_t)rt * (rt + 1));
-    const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
-    out[e] = (i < k && j <= i) ? A[(int64_t)i * ST + j] : 0.0;
+    const int i = 8 * rt + (lane >> 2), j = 4 * js + (lane & 3);
+    out[blk * 32 + lane] = (i < k && j <= i) ? A[(int64_t)i * ST + j] : 0.0;
   }
   }   // bucket loop
 }
