@@ -150,7 +150,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
                     &c.S, &c.bdata, &c.fscratch, &c.obs_key, &c.obs_sorted_key, &c.obs_sorted_idx, &c.obs_mu,
                     &c.obs_sd, &c.plo, &c.phi, &c.derr, &c.knn_fail, &c.vcache, &c.vstate, &c.front[0],
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
-                    &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.brick_key, &c.perm,
+                    &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.brick_key, &c.child_bricks, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
                     &c.brick_flag, &c.brick_idx, &c.brick_start, &c.vscratch, &c.pmc_counters, &c.crec, &c.brick_done, &c.brick_unit, &c.cellmask, &c.union_cells, &c.union_mask, &c.ext_z, &c.ext_v, &c.sgpr_A};
   for (DevBuf* b : bufs) b->release();

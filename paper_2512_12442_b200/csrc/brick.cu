@@ -156,9 +156,15 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       int i0, j0, k0;
       int64_t q0 = 0, q1 = 0;
       if (FUSED) {
+        const uint64_t key = o.bricks[r];
+        if (key == ~0ull) {   // uniform: a child slot outside the grid (early pass)
+          if (tid == 0) o.ucomp[r] = 0;
+          continue;
+        }
         int bi, bj, bk;
-        node_unkey(o.bricks[r], bi, bj, bk);
+        node_unkey(key, bi, bj, bk);
         i0 = BK * bi; j0 = BK * bj; k0 = BK * bk;
+        __syncthreads();   // every thread has read the previous brick's s_skip
         if (tid == 0) {
           uint8_t* d = o.bdone + morton3(bi, bj, bk);
           s_skip = *d;
@@ -410,6 +416,26 @@ cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double
   o.derr = c.derr.as<int>();
   unsigned grid = (unsigned)std::min<int64_t>((nb + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count);
   k_brick<true><<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), nullptr, nullptr, nb, dcnt + 13, o);
+  ++c.n_launch;
+  return cudaGetLastError();
+}
+
+// The 8 child bricks (level Lfull-2 node keys) of level-(Lfull-3) frontier nodes, in
+// node order; slots whose brick holds no grid cell get the key ~0 (skipped).
+__global__ void k_child_bricks(Geom g, const uint64_t* __restrict__ F, int64_t nF, uint64_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 8 * nF) return;
+  int i, j, k;
+  node_unkey(F[t >> 3], i, j, k);
+  const int c = (int)(t & 7);
+  const int bi = 2 * i + (c & 1), bj = 2 * j + ((c >> 1) & 1), bk = 2 * k + (c >> 2);
+  const bool in = BK * bi < g.cells[0] && BK * bj < g.cells[1] && BK * bk < g.cells[2];
+  out[t] = in ? node_key(bi, bj, bk) : ~0ull;
+}
+
+cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, uint64_t* out) {
+  if (nF <= 0) return cudaSuccess;
+  k_child_bricks<<<(unsigned)((8 * nF + 255) / 256), 256, 0, c.stream>>>(c.g, F, nF, out);
   ++c.n_launch;
   return cudaGetLastError();
 }

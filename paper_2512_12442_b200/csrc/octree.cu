@@ -396,6 +396,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
   if (c.level_field)
     CK(cudaMemsetAsync(c.level_field, 0xFF, (size_t)g.cells[0] * g.cells[1] * g.cells[2], c.stream));
+  bool early_bricks = false;
   for (int level = 0; level <= max_depth && nF > 0; ++level) {
     int h = g.lfull - level;
     CK(c.ncase.ensure(nF));
@@ -415,29 +416,47 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     CK(c.perm.ensure(sizeof(int64_t) * cap));
     CK(cudaMemsetAsync(dcnt, 0, sizeof(unsigned long long) * 16, c.stream));
     const uint64_t* F = c.front[cur].as<uint64_t>();
-    if (c.fused && h == 2) {
-      // refine-time brick pass: the frontier nodes of this level are the aligned 4^3-cell
-      // bricks; one pass computes their vertex marginals (the bound's lattice, R6, R10)
-      // and the MC records of all their cells (a7-a8), reused by every later leaf pass
+    // refine-time brick pass over level-(Lfull-2) node keys (aligned 4^3-cell bricks):
+    // one pass computes their vertex marginals (the bound's lattice, R6, R10) and the MC
+    // records of all their cells (a7-a8), reused by every later leaf pass.  Bricks done
+    // earlier in this fit are skipped inside the kernel.
+    auto brick_pass = [&](const uint64_t* keys, int64_t nk) -> cudaError_t {
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);
       cudaEventRecord(b0, c.stream);
-      const int64_t ch = std::min<int64_t>(nF, BRICK_PASS_CHUNK);
-      CK(c.post.ensure(sizeof(double) * 44 * 64 * ch));
-      for (int64_t off = 0; off < nF; off += ch) {
-        const int64_t nb = std::min(ch, nF - off);
-        CK(launch_brick_pass(c, F + off, nb, c.post.as<double>()));
-        CK(launch_chol8_rec(c, F + off, nb, c.post.as<double>()));
+      const int64_t ch = std::min<int64_t>(nk, BRICK_PASS_CHUNK);
+      cudaError_t be = c.post.ensure(sizeof(double) * 44 * 64 * ch);
+      for (int64_t off = 0; off < nk && be == cudaSuccess; off += ch) {
+        const int64_t nb = std::min(ch, nk - off);
+        be = launch_brick_pass(c, keys + off, nb, c.post.as<double>());
+        if (be == cudaSuccess) be = launch_chol8_rec(c, keys + off, nb, c.post.as<double>());
       }
       cudaEventRecord(b1, c.stream);
-      CK(cudaEventSynchronize(b1));
+      if (be == cudaSuccess) be = cudaEventSynchronize(b1);
       float bms = 0;
       cudaEventElapsedTime(&bms, b0, b1);
       c.t.brick_ms += bms;
       cudaEventDestroy(b0);
       cudaEventDestroy(b1);
+      return be;
+    };
+    // early pass at level Lfull-3 over the frontier's child bricks, when the previous
+    // level refined nearly everything (then nearly every child brick would be reached
+    // anyway): its vertex marginals serve this level's spacing-2 bound lattice, which
+    // otherwise needs a separate k_marginals pass over 1/8 of all vertices
+    static const bool early_env = [] {
+      const char* v = std::getenv("LCP_EARLY_BRICK");
+      return !(v && v[0] == '0');
+    }();
+    if (c.fused && h == 3 && early_env && level >= 1 && level > slab_level && !c.level_nodes.empty() &&
+        c.level_refined.back() * 10 >= c.level_nodes.back() * 9) {
+      CK(c.child_bricks.ensure(sizeof(uint64_t) * 8 * nF));
+      CK(launch_child_bricks(c, F, nF, c.child_bricks.as<uint64_t>()));
+      CK(brick_pass(c.child_bricks.as<uint64_t>(), 8 * nF));
+      early_bricks = true;   // covers every brick of the next frontier
     }
+    if (c.fused && h == 2 && !early_bricks) CK(brick_pass(F, nF));
     const int G = h == 0 ? 1 : (h == 1 ? 4 : (h == 2 ? 8 : 32));
     unsigned gw = (unsigned)((nF * G + 255) / 256);
 #define PRELIM(GG)                                                                                              \
