@@ -35,6 +35,11 @@ UNIT = "cells/s"
 #                           decision 3, queue store + load 14                              =  99
 OPS_PHASE1 = 120
 OPS_PHASE2 = 99
+# SURVEY.md §8(d) per-unit figure of the leaf MC ("minimal op mix", fixed before any kernel):
+# 170-210 CUDA-core issue slots + 16 MUFU per sample; the lower end, 186, is used, and each
+# further isovalue of a fused multi-isovalue pass adds the crossing-test row (21 slots).
+OPS_SURVEY = 186
+OPS_SURVEY_PER_EXTRA_ISO = 21
 SM_COUNT = 148
 LANES_PER_SM_CLK = 128
 
@@ -365,11 +370,20 @@ def run_ours(args):
     peak = SM_COUNT * LANES_PER_SM_CLK * 1965e6 / 1e12          # T lane-op/s at the max SM clock
     p2_step = float(lv[2]) / args.steps
     ops_step = samples_step * OPS_PHASE1 + p2_step * OPS_PHASE2
-    achieved = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
+    impl_mix = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
+    fused_t = len(w.thetas) if len(w.thetas) > 1 and not args.dense and not args.separate_iso else 1
+    ops_survey = samples_step * (OPS_SURVEY + OPS_SURVEY_PER_EXTRA_ISO * (fused_t - 1))
+    achieved = (ops_survey / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
     traffic = load_traffic(leaves_step / max(world, 1) / max(len(w.thetas) if args.dense or args.separate_iso else 1, 1))
     roofline = {"bound": "alu", "kernel": "k_pmc", "achieved": achieved, "peak": peak,
                 "unit": "Tlane-op/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "ops_per_sample": ops_step / samples_step if samples_step else None,
+                "ops_per_sample": ops_survey / samples_step if samples_step else None,
+                "ops_note": ("achieved = samples x SURVEY.md 8(d) minimal op mix (186 issue slots per "
+                             "sample, +21 per extra fused isovalue) / summed k_pmc time; the two-phase "
+                             "kernel executes fewer: frac_impl_mix uses its own fixed mix (120 per "
+                             "sample + 99 per phase-2 sample)"),
+                "frac_impl_mix": (impl_mix / peak) if impl_mix else None,
+                "impl_ops_per_sample": ops_step / samples_step if samples_step else None,
                 "phase2_fraction": p2_step / samples_step if samples_step else None,
                 "samples_per_s": samples_step / max(world, 1) / mc_s if mc_s > 0 else None,
                 "mc_share_of_step": mc_s / (ms_step / 1000.0),
