@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "chol8.cuh"
+#include "expfast.cuh"
 
 #include "ctx.h"
 
@@ -30,51 +31,19 @@ constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
 constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
 
-// Fast e^{-x} (x >= 0) for the brick's kernel evaluations: n = round(-x log2 e) by
-// the 1.5 2^52 magic add, f = -x - n ln2 (Cody-Waite, |f| <= ln2 / 2), e^f by its
-// degree-12 Taylor polynomial (truncation < 2e-16 relative), times 2^n built from the
-// exponent bits; 0 below 2^-1022.  The coefficients live in the constant bank, so
-// every Horner step is one DFMA with a c[] operand (the libm exp materialises each
-// 64-bit coefficient with two UMOVs per call).
-__constant__ double c_exp_taylor[13] = {
-    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
-    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
-    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
-    0x1.1eed8eff8d898p-29};
-__constant__ double c_exp_consts[4] = {1.4426950408889634074, 6755399441055744.0, 0x1.62e42fefa39efp-1,
-                                       0x1.abc9e3b39803fp-56};
-
-__device__ __forceinline__ double exp_neg_fast(double x) {
-  const double t = fma(-x, c_exp_consts[0], c_exp_consts[1]);
-  const double n = t - c_exp_consts[1];
-  double f = fma(n, -c_exp_consts[2], -x);
-  f = fma(n, -c_exp_consts[3], f);
-  double p = c_exp_taylor[12];
-#pragma unroll
-  for (int i = 11; i >= 0; --i) p = fma(p, f, c_exp_taylor[i]);
-  const int ni = __double2loint(t);
-  const double scale = __hiloint2double((ni + 1023) << 20, 0);
-  return (ni < -1022 || x > 745.0) ? 0.0 : p * scale;   // x > 745: also guards the magic-add range
-}
-
-// branch-free sqrt: MUFU.RSQ64H seed, two Newton steps on 1/sqrt, one on sqrt (~1 ulp);
-// sqrt(0) = 0 by a select (libm sqrt branches to a slow path per element)
-__device__ __forceinline__ double sqrt_fast(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  y = y * fma(-0.5 * x, y * y, 1.5);
-  y = y * fma(-0.5 * x, y * y, 1.5);
-  double r = x * y;
-  r = fma(0.5 * y, fma(-r, r, x), r);
-  return x > 0.0 ? r : 0.0;
-}
-
 // kernel value from r^2 (Matern-5/2 per BASELINE c4/c5) with exp_neg_fast
 __device__ __forceinline__ double kern_from_r2_fast(const KernParams& p, double r2) {
   if (p.kind == LCP_K_SE) return p.var * exp_neg_fast(0.5 * r2);
   const double r = sqrt_fast(r2);
   const double s5 = SQRT5 * r;
   return p.var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_fast(s5);
+}
+// the same with the table exp (k_brick: the table sits in its shared memory)
+__device__ __forceinline__ double kern_from_r2_tab(const KernParams& p, double r2, const double* __restrict__ tab) {
+  if (p.kind == LCP_K_SE) return p.var * exp_neg_tab(0.5 * r2, tab);
+  const double r = sqrt_fast(r2);
+  const double s5 = SQRT5 * r;
+  return p.var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_tab(s5, tab);
 }
 
 struct BrickArgs {
@@ -141,10 +110,12 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
   double* KV = smem + head;                     // KP x VSTR
   double* sMu = KV + (int64_t)KP * VSTR;        // NVP
   double* sT = sMu + NVP;                       // k x 16: separable squared offsets (phase 1)
+  double* sExp = sT + 16 * (int64_t)k;          // 64: 2^(j/64) for exp_neg_tab
   __shared__ int64_t s_r0;
   __shared__ int s_skip;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geom& g = a.g;
+  if (tid < 64) sExp[tid] = c_exp2_64[tid];   // read after the loop's first barrier
   int staged = -1;
   for (;;) {
     if (tid == 0) s_r0 = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
@@ -209,7 +180,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
 #pragma unroll 4
         for (int j = tid >> 7; j < KP; j += BRICK_THREADS / NVP) {
           const double* tj = sT + 16 * min(j, k - 1);
-          const double val = kern_from_r2_fast(a.kp, (tj[ta] + tj[tb]) + tj[tc]);
+          const double val = kern_from_r2_tab(a.kp, (tj[ta] + tj[tb]) + tj[tc], sExp);
           KV[(int64_t)j * VSTR + v] = (j < k && vok) ? val : 0.0;
         }
       }
@@ -353,7 +324,7 @@ static BrickArgs brick_args(const Ctx& c) {
 static size_t brick_smem(int k) {
   const int kp8 = (k + 7) & ~7;
   const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
-  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP + 16 * (int64_t)k);
+  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP + 16 * (int64_t)k + 64);
 }
 
 bool fused_brick_supported(const Ctx& c) {
