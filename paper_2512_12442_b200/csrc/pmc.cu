@@ -72,41 +72,49 @@ __global__ void k_chol8(double* __restrict__ post, int64_t n) {
 }
 
 // refine-time brick pass output (44-double slots, 64 per brick unit) -> MC records
-// indexed by the cell's Morton code in the virtual 2^Lfull cube
-__global__ void k_chol8_rec(Geom g, const uint64_t* __restrict__ bricks, int64_t nb,
-                            const uint8_t* __restrict__ ucomp, const double* __restrict__ post,
-                            CellRec* __restrict__ recs) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 64 * nb) return;
-  const int64_t u = t >> 6;
-  if (!ucomp[u]) return;   // brick done by an earlier refine: its record stands
-  const int qq = (int)(t & 63);
-  int bi, bj, bk;
-  node_unkey(bricks[u], bi, bj, bk);
-  const int xi = 4 * bi + (qq & 3), xj = 4 * bj + ((qq >> 2) & 3), xk = 4 * bk + (qq >> 4);
-  if (xi >= g.cells[0] || xj >= g.cells[1] || xk >= g.cells[2]) return;
-  const double* rec = post + 44 * t;
+// indexed by the cell's Morton code in the virtual 2^Lfull cube.  CTA per brick: the
+// brick's 64 slots are staged through shared memory (row stride 45 doubles: conflict-free)
+// so that both the 22.5 KB read and the 13 KB record write (the brick's 64 cells are 64
+// consecutive Morton codes) are coalesced.  Records of out-of-grid cells of a clipped brick
+// get written too; no leaf list ever names them.
+constexpr int REC_STR = 45;
+__global__ void __launch_bounds__(64) k_chol8_rec(Geom g, const uint64_t* __restrict__ bricks, int64_t nb,
+                                                  const uint8_t* __restrict__ ucomp, const double* __restrict__ post,
+                                                  CellRec* __restrict__ recs) {
+  __shared__ __align__(16) double sbuf[64 * REC_STR];
+  const int64_t u = blockIdx.x;
+  if (u >= nb || !ucomp[u]) return;   // brick done by an earlier refine: its records stand
+  const int q = threadIdx.x;
+  const double* src = post + 64 * 44 * u;
+  for (int e = q; e < 64 * 44; e += 64) sbuf[(e / 44) * REC_STR + e % 44] = src[e];
+  __syncthreads();
   double mu[8], sig[36];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) mu[i] = rec[i];
+  for (int i = 0; i < 8; ++i) mu[i] = sbuf[q * REC_STR + i];
 #pragma unroll
-  for (int p = 0; p < 36; ++p) sig[p] = rec[8 + p];
-  CellRec& out = recs[morton3(xi, xj, xk)];
+  for (int p = 0; p < 36; ++p) sig[p] = sbuf[q * REC_STR + 8 + p];
   double mo[8];
   float Lf[36];
   chol8_factor(mu, sig, mo, Lf);
-  double2* m2 = reinterpret_cast<double2*>(out.mu);
+  __syncthreads();   // staging buffer becomes the output buffer: 64 records by local Morton code
+  CellRec* so = reinterpret_cast<CellRec*>(sbuf);
+  CellRec& r = so[morton3(q & 3, (q >> 2) & 3, q >> 4)];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) m2[i] = make_double2(mo[2 * i], mo[2 * i + 1]);
-  float4* L4 = reinterpret_cast<float4*>(out.L);
+  for (int i = 0; i < 8; ++i) r.mu[i] = mo[i];
 #pragma unroll
-  for (int i = 0; i < 9; ++i) L4[i] = make_float4(Lf[4 * i], Lf[4 * i + 1], Lf[4 * i + 2], Lf[4 * i + 3]);
+  for (int p = 0; p < 36; ++p) r.L[p] = Lf[p];
+  __syncthreads();
+  int bi, bj, bk;
+  node_unkey(bricks[u], bi, bj, bk);
+  float4* dst = reinterpret_cast<float4*>(recs + (morton3(bi, bj, bk) << 6));
+  const float4* s4 = reinterpret_cast<const float4*>(sbuf);
+  for (int e = q; e < 64 * (int)(sizeof(CellRec) / 16); e += 64) dst[e] = s4[e];
 }
 
 cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post) {
   if (nb <= 0) return cudaSuccess;
-  k_chol8_rec<<<(unsigned)((64 * nb + 127) / 128), 128, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(),
-                                                                      post, c.crec.as<CellRec>());
+  k_chol8_rec<<<(unsigned)nb, 64, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(), post,
+                                                  c.crec.as<CellRec>());
   ++c.n_launch;
   return cudaGetLastError();
 }
