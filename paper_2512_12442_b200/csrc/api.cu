@@ -24,6 +24,11 @@ lcp_status_t check_device_errors(Ctx& c) {
   cudaError_t e = cudaMemcpyAsync(&h, c.derr.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
   if (e != cudaSuccess) return cuda_err(c, e, "device error check");
+  if (h != 0) {
+    // reported once: the flags belong to the call that raised them, not to later calls
+    e = cudaMemsetAsync(c.derr.p, 0, sizeof(int), c.stream);
+    if (e != cudaSuccess) return cuda_err(c, e, "device error reset");
+  }
   if (h & DERR_FACTOR) return set_err(c, LCP_EFACTOR, "a bucket covariance K_y is not PD after jitter");
   if (h & DERR_NUMERIC) return set_err(c, LCP_ENUMERIC, "posterior variance below -1e-8 sigma_f^2");
   if (h & DERR_OVERFLOW) return set_err(c, LCP_EINVAL, "cell id out of range");

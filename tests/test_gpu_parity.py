@@ -262,6 +262,18 @@ def test_error_codes(dev):
     with pytest.raises(LcpError) as e:
         ctx.pmc_cells(np.array([-1, 5], np.int64), 0.0, 10, 1, out=np.zeros(2, np.float32))
     assert e.value.status == LCP_EINVAL
+    # an out-of-range id in a device list is caught on the device; the error belongs to
+    # that call only (the context stays usable)
+    bad = torch.tensor([3, int(np.prod(cfg.cells)), 7], dtype=torch.int64, device=dev)
+    with pytest.raises(LcpError) as e:
+        ctx.pmc_cells(bad, 0.0, 10, 1)
+    assert e.value.status == LCP_EINVAL
+    with pytest.raises(LcpError) as e:
+        ctx.cell_posterior(bad)
+    assert e.value.status == LCP_EINVAL
+    good = ctx.pmc_cells(bad[:1].clone(), 0.0, 10, 1)
+    assert good.numel() == 1
+    ctx.octree_refine(w.thetas[0], cfg.alpha, cfg.max_depth)
     # empty list, max_depth 0 (root only), far-shifted isovalue (empty leaf set)
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
     assert ctx.pmc_cells(empty, 0.0, 10, 1).numel() == 0
