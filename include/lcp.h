@@ -170,7 +170,9 @@ lcp_status_t lcp_pmc_cells(lcp_ctx_t* ctx, const int64_t* cells, int64_t n_cells
                            int32_t out_on_device);
 
 /* a9: zero `field` (nx*ny*nz floats, device) and scatter lcp[q] into cell
- * cells[q] (every other cell is 0).  Asynchronous. */
+ * cells[q] (every other cell is 0).  Asynchronous; an id outside
+ * [0, nx*ny*nz) is skipped and reported as EINVAL by the next synchronizing call
+ * (lcp_synchronize, or any call that blocks). */
 lcp_status_t lcp_scatter_field(lcp_ctx_t* ctx, const int64_t* cells_dev, const float* lcp_dev,
                                int64_t n, float* field_dev);
 

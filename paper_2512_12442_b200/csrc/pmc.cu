@@ -502,9 +502,12 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
 }
 
 __global__ void k_scatter(const int64_t* __restrict__ cells, const float* __restrict__ lcp, int64_t n,
-                          float* __restrict__ field) {
+                          int64_t ncell, float* __restrict__ field, int* __restrict__ derr) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) field[cells[q]] = lcp[q];
+  if (q >= n) return;
+  const int64_t cell = cells[q];
+  if (cell < 0 || cell >= ncell) atomicOr(derr, DERR_OVERFLOW);   // skipped, reported by the next check
+  else field[cell] = lcp[q];
 }
 
 // posterior of n cells (device list) into post (n x 44 doubles); groups by
@@ -672,7 +675,7 @@ cudaError_t launch_scatter(Ctx& c, const int64_t* cells, const float* lcp, int64
   cudaError_t e = cudaMemsetAsync(field, 0, sizeof(float) * ncell, c.stream);
   if (e != cudaSuccess) return e;
   if (n > 0) {
-    k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cells, lcp, n, field);
+    k_scatter<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(cells, lcp, n, ncell, field, c.derr.as<int>());
     ++c.n_launch;
   }
   return cudaGetLastError();

@@ -273,6 +273,12 @@ def test_error_codes(dev):
     assert e.value.status == LCP_EINVAL
     good = ctx.pmc_cells(bad[:1].clone(), 0.0, 10, 1)
     assert good.numel() == 1
+    vals = torch.ones(3, dtype=torch.float32, device=dev)
+    f = ctx.scatter_field(bad, vals)          # asynchronous: the bad id is skipped ...
+    with pytest.raises(LcpError) as e:
+        ctx.synchronize()                     # ... and reported here
+    assert e.value.status == LCP_EINVAL
+    assert float(f.sum()) == 2.0
     ctx.octree_refine(w.thetas[0], cfg.alpha, cfg.max_depth)
     # empty list, max_depth 0 (root only), far-shifted isovalue (empty leaf set)
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
