@@ -238,7 +238,8 @@ lcp_status_t lcp_cell_posterior(lcp_ctx_t* ctx, const int64_t* cells_dev, int64_
                                 double* mu_dev, double* cov_dev);
 
 /* local marginal (mean, variance before the floor) at points xyz_dev (n x 3),
- * using bucket bucket_dev[q] or, if bucket_dev == NULL, each point's own bucket. */
+ * using bucket bucket_dev[q] or, if bucket_dev == NULL, each point's own bucket.
+ * Errors: ESTATE, EINVAL (a bucket id outside [0, nbuckets)), ENUMERIC, ECUDA. */
 lcp_status_t lcp_point_marginals(lcp_ctx_t* ctx, const double* xyz_dev, int64_t n,
                                  const int32_t* bucket_dev, double* mu_dev, double* var_dev);
 

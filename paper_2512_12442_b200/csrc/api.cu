@@ -31,7 +31,7 @@ lcp_status_t check_device_errors(Ctx& c) {
   }
   if (h & DERR_FACTOR) return set_err(c, LCP_EFACTOR, "a bucket covariance K_y is not PD after jitter");
   if (h & DERR_NUMERIC) return set_err(c, LCP_ENUMERIC, "posterior variance below -1e-8 sigma_f^2");
-  if (h & DERR_OVERFLOW) return set_err(c, LCP_EINVAL, "cell id out of range");
+  if (h & DERR_OVERFLOW) return set_err(c, LCP_EINVAL, "cell or bucket id out of range");
   return LCP_OK;
 }
 
@@ -58,6 +58,19 @@ __global__ void k_point_bucket(Geom g, const double* __restrict__ xyz, int64_t n
                      point_bucket_axis(g, 2, xyz[3 * q + 2]));
 }
 
+// caller-given bucket ids: copy, with ids outside [0, nbuckets) flagged and clamped to 0
+__global__ void k_check_buckets(const int32_t* __restrict__ in, int64_t n, int32_t nbuckets, int32_t* __restrict__ out,
+                                int* __restrict__ derr) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  int32_t b = in[q];
+  if (b < 0 || b >= nbuckets) {
+    atomicOr(derr, DERR_OVERFLOW);
+    b = 0;
+  }
+  out[q] = b;
+}
+
 __global__ void k_gather_sorted(const int32_t* __restrict__ bkt, const int64_t* __restrict__ perm, int64_t n,
                                 int32_t* __restrict__ out) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -78,8 +91,10 @@ lcp_status_t point_marginals_impl(Ctx& c, const double* xyz, int64_t n, const in
   CK(c.perm.ensure(sizeof(int64_t) * n));
   int32_t* bkt = c.cell_bucket.as<int32_t>();
   unsigned gr = (unsigned)((n + 255) / 256);
-  if (bkt_in) CK(cudaMemcpyAsync(bkt, bkt_in, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c.stream));
-  else {
+  if (bkt_in) {
+    k_check_buckets<<<gr, 256, 0, c.stream>>>(bkt_in, n, c.g.nbuckets, bkt, c.derr.as<int>());
+    ++c.n_launch;
+  } else {
     k_point_bucket<<<gr, 256, 0, c.stream>>>(c.g, xyz, n, bkt);
     ++c.n_launch;
   }

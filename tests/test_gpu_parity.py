@@ -279,6 +279,11 @@ def test_error_codes(dev):
         ctx.synchronize()                     # ... and reported here
     assert e.value.status == LCP_EINVAL
     assert float(f.sum()) == 2.0
+    P = torch.zeros((2, 3), dtype=torch.float64, device=dev)
+    with pytest.raises(LcpError) as e:
+        ctx.point_marginals(P, torch.tensor([0, 10**6], dtype=torch.int32, device=dev))
+    assert e.value.status == LCP_EINVAL
+    ctx.point_marginals(P)
     ctx.octree_refine(w.thetas[0], cfg.alpha, cfg.max_depth)
     # empty list, max_depth 0 (root only), far-shifted isovalue (empty leaf set)
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
