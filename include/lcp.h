@@ -118,7 +118,8 @@ const char* lcp_last_error(const lcp_ctx_t* ctx);
  *   synchronously), else device pointers (read before return).
  *   opts may be NULL (bucket_log2 = 0, h_full = 2, FP64, one slab, level 3, no records).
  * Errors: EINVAL (k < 1, k > m, variance <= 0, nugget < 0, lengthscale <= 0,
- * cells < 1, bucket_log2 > Lfull), EFACTOR, ENUMERIC, ENOMEM, ECUDA. */
+ * cells < 1, bucket_log2 > Lfull, a non-finite coordinate or value), EFACTOR,
+ * ENUMERIC, ENOMEM, ECUDA. */
 lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, int64_t m,
                            int32_t on_device, const lcp_kernel_t* kernel, int32_t k,
                            const lcp_grid_t* grid, const lcp_opts_t* opts);

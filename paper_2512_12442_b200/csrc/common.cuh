@@ -182,6 +182,6 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // device-side error flags (OR-ed; checked by the host at sync points)
-enum : int { DERR_NUMERIC = 1, DERR_FACTOR = 2, DERR_OVERFLOW = 4 };
+enum : int { DERR_NUMERIC = 1, DERR_FACTOR = 2, DERR_OVERFLOW = 4, DERR_INPUT = 8 };
 
 }  // namespace lcp

@@ -35,10 +35,12 @@ __device__ T block_sum(T v, T* sh) {
 }
 
 // a1: point bucket, finest cell Morton key
-__global__ void k_obs_bin(Geom g, const double* __restrict__ X, int64_t m, int32_t* __restrict__ obs_bucket,
-                          uint64_t* __restrict__ obs_key) {
+__global__ void k_obs_bin(Geom g, const double* __restrict__ X, const double* __restrict__ Y, int64_t m,
+                          int32_t* __restrict__ obs_bucket, uint64_t* __restrict__ obs_key, int* __restrict__ derr) {
   int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= m) return;
+  if (!isfinite(Y[o]) || !isfinite(X[3 * o]) || !isfinite(X[3 * o + 1]) || !isfinite(X[3 * o + 2]))
+    atomicOr(derr, DERR_INPUT);
   int bc[3], cc[3];
   for (int d = 0; d < 3; ++d) {
     double x = X[3 * o + d];
@@ -987,7 +989,8 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   const double* X = c.X.as<double>();
   unsigned gm = (unsigned)((m + 255) / 256);
   // a1
-  k_obs_bin<<<gm, 256, 0, c.stream>>>(g, X, m, c.obs_bucket.as<int32_t>(), c.obs_key.as<uint64_t>());
+  k_obs_bin<<<gm, 256, 0, c.stream>>>(g, X, c.y.as<double>(), m, c.obs_bucket.as<int32_t>(), c.obs_key.as<uint64_t>(),
+                                      c.derr.as<int>());
   ++c.n_launch;
   CK(group_by_bucket(c, c.obs_bucket.as<int32_t>(), m, c.obs_by_bucket.as<int64_t>()));
   k_bucket_ranges<<<(nbk + 255) / 256, 256, 0, c.stream>>>(c.gcount.as<int64_t>(), c.goff.as<int64_t>(), nbk,

@@ -247,6 +247,12 @@ def test_error_codes(dev):
     with pytest.raises(LcpError) as e:
         ctx.fit_local(X, y, kernel, cfg.m + 1, grid)
     assert e.value.status == LCP_EINVAL
+    for bad in ("x", "y"):
+        Xb, yb = X.clone(), y.clone()
+        (Xb[5, 1:2] if bad == "x" else yb[7:8]).fill_(float("nan"))
+        with pytest.raises(LcpError) as e:
+            ctx.fit_local(Xb, yb, kernel, k, grid, bucket_log2=b, h_full=hf)
+        assert e.value.status == LCP_EINVAL, e.value
     ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
     for bad_alpha in (0.0, 0.5, -1.0):
         with pytest.raises(LcpError) as e:
