@@ -482,8 +482,8 @@ __device__ __forceinline__ void dmma_f(double a, double b, double& d0, double& d
 
 // GMEM: K_y / X live in a per-CTA global scratch (L2-resident) instead of shared
 // memory (k > 128); CTAs loop over buckets.
-template <bool GMEM>
-__global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_blk(KernParams kp, int k, int nbk,
+template <bool GMEM, int MINB>
+__global__ void __launch_bounds__(FACT_THREADS, MINB) k_bucket_factor_blk(KernParams kp, int k, int nbk,
                                                                     const double* __restrict__ X,
                                                                     const double* __restrict__ yobs,
                                                                     const int32_t* __restrict__ S,
@@ -1072,25 +1072,36 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       const char* v = std::getenv("LCP_FACTOR_BLOCKED");
       return v && v[0] == '0';
     }();
-    if (!blk_off && bucket_factor_blk_smem(k, k > 128) <= 220 * 1024) {
-      const bool gm = k > 128;
+    // The blocked factor keeps its k x k working matrix in a per-CTA L2-resident global
+    // scratch (GMEM) with 4 CTAs (64 registers each) per SM: the factorisation is barrier-
+    // and latency-bound, and 4 concurrent buckets per SM beat 1 with the matrix in shared
+    // memory (c5 fit 23.3 -> 19.5 ms).  LCP_FACTOR_SMEM=1 selects the shared-memory variant
+    // when the matrix fits (k <= 128).
+    static const bool smem_variant = [] {
+      const char* v = std::getenv("LCP_FACTOR_SMEM");
+      return v && v[0] == '1';
+    }();
+    if (!blk_off && bucket_factor_blk_smem(k, true) <= 220 * 1024) {
+      const bool gm = !(smem_variant && bucket_factor_blk_smem(k, false) <= 220 * 1024);
       const size_t sb = bucket_factor_blk_smem(k, gm);
       const int KPf = (k + FB - 1) & ~(FB - 1);
       unsigned gridf = (unsigned)nbk;
       double* gsf = nullptr;
       if (gm) {
-        gridf = (unsigned)std::min<int64_t>(nbk, 2 * (int64_t)c.sm_count);
+        // many buckets (k <= 256): 4 CTAs of <= 64 registers per SM; otherwise 2 unconstrained
+        const bool four = KPf <= 256 && nbk >= 2 * (int64_t)c.sm_count;
+        gridf = (unsigned)std::min<int64_t>(nbk, (four ? 4 : 2) * (int64_t)c.sm_count);
         CK(c.fscratch.ensure(sizeof(double) * (size_t)gridf * KPf * (KPf + 4)));
         gsf = c.fscratch.as<double>();
-        CK(cudaFuncSetAttribute(k_bucket_factor_blk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-        k_bucket_factor_blk<true><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
-                                                                         c.S.as<int32_t>(), c.bdata.as<double>(),
-                                                                         c.bstride, gsf, c.derr.as<int>());
+        auto kf = four ? k_bucket_factor_blk<true, 4> : k_bucket_factor_blk<true, 1>;
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+        kf<<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                  c.bdata.as<double>(), c.bstride, gsf, c.derr.as<int>());
       } else {
-        CK(cudaFuncSetAttribute(k_bucket_factor_blk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-        k_bucket_factor_blk<false><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
-                                                                          c.S.as<int32_t>(), c.bdata.as<double>(),
-                                                                          c.bstride, nullptr, c.derr.as<int>());
+        CK(cudaFuncSetAttribute(k_bucket_factor_blk<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
+        k_bucket_factor_blk<false, 1><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
+                                                                             c.S.as<int32_t>(), c.bdata.as<double>(),
+                                                                             c.bstride, nullptr, c.derr.as<int>());
       }
     } else if (use_smem) {
       CK(cudaFuncSetAttribute(k_bucket_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
