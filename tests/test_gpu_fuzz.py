@@ -11,6 +11,7 @@ and the LCP values of every leaf (R20 statistics, identical Philox streams),
 and the fused two-isovalue pass.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -19,6 +20,13 @@ import oracle as O
 from parity_util import compare_node_sets, lcp_parity, posterior_close
 
 pytestmark = pytest.mark.gpu
+
+# LCP_FUZZ_SCALE=n multiplies every sweep's seed count (default 1: the committed suite)
+_SCALE = int(os.environ.get("LCP_FUZZ_SCALE", "1"))
+
+
+def _seeds(n):
+    return range(n * _SCALE)
 
 torch = pytest.importorskip("torch")
 
@@ -58,7 +66,7 @@ def _draw(seed):
                 thetas=thetas, N=N, seed=int(g.integers(0, 2**31)))
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", _seeds(40))
 def test_fuzz_whole_path(seed):
     from paper_2512_12442_b200 import Context
     d = _draw(seed)
@@ -131,7 +139,7 @@ def _opts(seed, d):
     return o, d
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", _seeds(30))
 def test_fuzz_options(seed):
     from paper_2512_12442_b200 import Context, LcpError
     d0 = _draw(100 + seed)
@@ -228,7 +236,7 @@ def _draw_large(seed):
                 thetas=[float(v) for v in np.quantile(y, q)], N=int(g.choice([1000, 4096])))
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", _seeds(6))
 def test_fuzz_large(seed):
     from paper_2512_12442_b200 import Context
     d = _draw_large(seed)
@@ -302,7 +310,7 @@ def test_fuzz_large(seed):
         assert frac >= 0.999 and mean <= 1e-4, (t, frac, mean, mx)
 
 
-@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("seed", _seeds(10))
 def test_fuzz_sgpr(seed):
     # NEXT-2 on random draws: inducing points = the observations, (mu_M, A_M) the
     # exact GP posterior at them under a larger noise (the oracle's literal Eq. 1)
@@ -345,7 +353,7 @@ def test_fuzz_sgpr(seed):
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", _seeds(8))
 def test_fuzz_cell_lists(seed):
     # lcp_pmc_cells / lcp_cell_posterior on arbitrary lists: duplicates, unsorted,
     # Morton-sorted dense blocks with repeats, host pointers; before and after a refine
@@ -391,7 +399,7 @@ def test_fuzz_cell_lists(seed):
     ctx.pmc_cells(np.zeros(0, np.int64), th, N, d["seed"], 0, out=np.zeros(0, np.float32))
 
 
-@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("seed", _seeds(3))
 def test_fuzz_context_reuse(seed):
     # one context refitted with a sequence of different models (grid, k, buckets,
     # kernel, local mode): every cache (vertex cache, brick flags, cell records, leaf
