@@ -16,6 +16,7 @@ lcp_status_t set_err(Ctx& c, lcp_status_t st, const std::string& msg) {
 
 lcp_status_t cuda_err(Ctx& c, cudaError_t e, const char* where) {
   c.err = std::string(where) + ": " + cudaGetErrorString(e);
+  cudaGetLastError();   // a failed launch's error belongs to this call, not to the next one
   return e == cudaErrorMemoryAllocation ? LCP_ENOMEM : LCP_ECUDA;
 }
 

@@ -302,8 +302,20 @@ cudaError_t launch_node_extreme(Ctx& c, int level, const uint64_t* front, int64_
   a.theta = theta;
   a.alpha = alpha;
   a.var_floor = 1e-12 * c.kp.var;
-  const int warps = 8;
-  size_t smem = sizeof(double) * warps * (8 * (size_t)a.ks + (c.k > 128 ? 1024 : 0));
+  // warp per node; as many warps per CTA (<= 8) as their K/V buffers fit in shared memory
+  static const size_t static_smem = [] {
+    cudaFuncAttributes at{};
+    if (cudaFuncGetAttributes(&at, k_node_extreme) != cudaSuccess) {
+      cudaGetLastError();
+      return (size_t)4096;
+    }
+    return (size_t)at.sharedSizeBytes;
+  }();
+  const size_t per_warp = sizeof(double) * (8 * (size_t)a.ks + (c.k > 128 ? 1024 : 0));
+  const size_t cap = 227 * 1024 - static_smem - 512;
+  const int warps = (int)std::min<size_t>(8, cap / per_warp);
+  if (warps < 1) return cudaErrorInvalidConfiguration;
+  size_t smem = per_warp * warps;
   cudaError_t e = cudaFuncSetAttribute(k_node_extreme, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   unsigned grid = (unsigned)((nF + warps - 1) / warps);

@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(512) k_cell_posterior_f32(TileArgs a, const in
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float tx = (xj - qx[c][0]) * il[0], ty = (yj - qx[c][1]) * il[1], tz = (zj - qx[c][2]) * il[2];
-          float r2 = tx * tx + ty * ty + tz * tz, kv;
+          // clamp: the far padding dummies of beta-box sets (R28) overflow FP32 squares, and
+          // Matern's inf * 0 would give NaN; at 1e30 both kernels are exactly 0 in FP32
+          float r2 = fminf(tx * tx + ty * ty + tz * tz, 1e30f), kv;
           if (a.kp.kind == LCP_K_SE) {
             kv = var_f * expf(-0.5f * r2);
           } else {
