@@ -241,7 +241,8 @@ def run_ours(args):
         if args.dense == "exact":
             k, b = cfg.m, 0
         c0, c1 = slab_cells(cfg.cells, 3, rank, world) if world > 1 else (0, ncell)
-        dense_cells = torch.arange(c0, c1, dtype=torch.int64, device=dev)
+        from workloads.gen import morton_sorted_cells
+        dense_cells = morton_sorted_cells(cfg.cells, c0, c1, device=dev)   # brick-kernel order
         dense_lcp = torch.empty(c1 - c0, dtype=torch.float32, device=dev)
     ctx = Context(local)
 

@@ -16,6 +16,7 @@ import torch  # noqa: E402
 
 from paper_2512_12442_b200 import Context, config_args  # noqa: E402
 from workloads import generate  # noqa: E402
+from workloads.gen import morton_sorted_cells  # noqa: E402
 
 
 def timed(fn, reps=3):
@@ -45,12 +46,13 @@ def run(name, alphas):
     y = torch.from_numpy(np.array(w.y)).to(dev)
     ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
     ncell = int(np.prod(cfg.cells))
-    allc = torch.arange(ncell, dtype=torch.int64, device=dev)
+    allc = morton_sorted_cells(cfg.cells, device=dev)   # Morton order: the brick posterior kernels
     lcp_all = torch.empty(ncell, dtype=torch.float32, device=dev)
+    field_all = torch.empty(ncell, dtype=torch.float32, device=dev)
 
     def dense():
         ctx.pmc_cells(allc, th, cfg.n_samples, cfg.mc_seed, 0, out=lcp_all)
-        return lcp_all
+        return ctx.scatter_field(allc, lcp_all, field_all)
 
     t_dense, f_dense = timed(dense)
     f_dense = f_dense.clone()

@@ -146,3 +146,23 @@ def random_cells(name: str, n: int, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     n = min(n, total)
     return np.sort(rng.choice(total, size=n, replace=False)).astype(np.int64)
+
+
+def morton_sorted_cells(cells, c0=0, c1=None, device=None):
+    """Linear cell ids [c0, c1) of a grid (x fastest) in Morton order of (i, j, k), as an int64
+    torch tensor: the input order under which a dense cell list takes the 4^3-brick posterior
+    kernels (a list ordering, not part of the method)."""
+    import torch
+    nx, ny, nz = cells
+    if c1 is None:
+        c1 = nx * ny * nz
+    c = torch.arange(c0, c1, dtype=torch.int64, device=device)
+
+    def spread(v):
+        out = torch.zeros_like(v)
+        for bit in range(21):
+            out |= ((v >> bit) & 1) << (3 * bit)
+        return out
+
+    key = spread(c % nx) | (spread((c // nx) % ny) << 1) | (spread(c // (nx * ny)) << 2)
+    return c[torch.argsort(key)]
