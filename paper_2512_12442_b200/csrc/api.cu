@@ -169,7 +169,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
   cudaSetDevice(c.device);
   cudaStreamSynchronize(c.stream);
   DevBuf* bufs[] = {&c.X, &c.y, &c.obs_bucket, &c.bcount, &c.bstart, &c.gcount, &c.goff, &c.obs_by_bucket,
-                    &c.S, &c.bdata, &c.fscratch, &c.obs_key, &c.obs_sorted_key, &c.obs_sorted_idx, &c.obs_mu,
+                    &c.S, &c.bdata, &c.fscratch, &c.obs_key, &c.obs_sorted_key, &c.obs_sorted_idx, &c.occ[0], &c.occ[1], &c.occ[2], &c.obs_mu,
                     &c.obs_sd, &c.plo, &c.phi, &c.derr, &c.knn_fail, &c.vcache, &c.vstate, &c.front[0],
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.brick_key, &c.child_bricks, &c.perm,

@@ -87,6 +87,8 @@ struct Ctx {
   DevBuf fscratch;           // factor scratch for large k
   DevBuf sgpr_A;             // NEXT-2: A_M (m x m) of an SGPR model
   DevBuf obs_key, obs_sorted_key, obs_sorted_idx;  // Morton keys of the finest cell
+  DevBuf occ[3];                 // occupancy bitmaps of nodes at heights 0, 1, 2 (bit per Morton code)
+  int occ_heights = 0;           // how many of occ[] are built (0 when the cube is too large)
   DevBuf obs_mu, obs_sd;     // observation marginals (Morton order after fit)
   DevBuf plo, phi;           // per-theta observation tails (Morton order)
   DevBuf derr;               // device error flags (int)

@@ -51,6 +51,19 @@ __global__ void k_obs_bin(Geom g, const double* __restrict__ X, const double* __
   obs_key[o] = morton3(cc[0], cc[1], cc[2]);
 }
 
+// occupancy bitmaps: bit (key >> 3h) of occ_h set for every observation's finest-cell key
+__global__ void k_occ_set(const uint64_t* __restrict__ key, int64_t m, int nh, uint32_t* __restrict__ o0,
+                          uint32_t* __restrict__ o1, uint32_t* __restrict__ o2) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const uint64_t kk = key[q];
+  uint32_t* o[3] = {o0, o1, o2};
+  for (int h = 0; h < nh; ++h) {
+    const uint64_t c = kk >> (3 * h);
+    atomicOr(&o[h][c >> 5], 1u << (c & 31));
+  }
+}
+
 __global__ void k_bucket_ranges(const int64_t* __restrict__ gcount, const int64_t* __restrict__ gend, int nb,
                                 int64_t* __restrict__ bcount, int64_t* __restrict__ bstart) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1000,6 +1013,20 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
                                       c.obs_sorted_idx.as<int32_t>());
   ++c.n_launch;
   CK(cudaGetLastError());
+  // occupancy bitmaps for the three finest octree levels (the preliminary test of a node
+  // without observations then skips its two binary searches); up to 2^30 cells
+  c.occ_heights = g.lfull <= 10 ? std::min(3, g.lfull + 1) : 0;
+  for (int h = 0; h < c.occ_heights; ++h) {
+    const size_t words = ((((size_t)1) << (3 * (g.lfull - h))) + 31) / 32;
+    CK(c.occ[h].ensure(sizeof(uint32_t) * words));
+    CK(cudaMemsetAsync(c.occ[h].p, 0, sizeof(uint32_t) * words, c.stream));
+  }
+  if (c.occ_heights > 0) {
+    k_occ_set<<<gm, 256, 0, c.stream>>>(c.obs_key.as<uint64_t>(), m, c.occ_heights, c.occ[0].as<uint32_t>(),
+                                        c.occ[1].as<uint32_t>(), c.occ[2].as<uint32_t>());
+    ++c.n_launch;
+    CK(cudaGetLastError());
+  }
   // a2
   if (o.local_mode == 1) {
     if (AM) return set_err(c, LCP_EINVAL, "fit: the box local mode is for observations (lcp_fit_local)");

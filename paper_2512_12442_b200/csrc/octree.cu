@@ -92,7 +92,8 @@ __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ fr
                               const double* __restrict__ phi, int64_t m, double alpha,
                               int8_t* __restrict__ ncase, int8_t* __restrict__ nref, double* __restrict__ np1,
                               double* __restrict__ np2, double* __restrict__ nU, uint32_t* __restrict__ vmask,
-                              int64_t* __restrict__ req, unsigned long long* __restrict__ nreq) {
+                              int64_t* __restrict__ req, unsigned long long* __restrict__ nreq,
+                              const uint32_t* __restrict__ occ) {
   int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int sub = threadIdx.x % G;
   const bool live = n < nF;
@@ -102,8 +103,10 @@ __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ fr
   int64_t a = 0, b = 0;
   if (live && sub == 0) {
     uint64_t mk = morton3(i, j, k);
-    a = lower_bound_u64(skey, m, mk << (3 * h));
-    b = lower_bound_u64(skey, m, (mk + 1) << (3 * h));
+    if (!occ || ((occ[mk >> 5] >> (mk & 31)) & 1u)) {   // bitmap: no observation in the node -> empty
+      a = lower_bound_u64(skey, m, mk << (3 * h));
+      b = lower_bound_u64(skey, m, (mk + 1) << (3 * h));
+    }
   }
   if (G > 1) {
     a = __shfl_sync(0xffffffffu, a, 0, G);
@@ -463,7 +466,8 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
   k_node_prelim<GG><<<gw, 256, 0, c.stream>>>(g, level, F, nF, c.obs_sorted_key.as<uint64_t>(), c.plo.as<double>(), \
                                                c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(),                \
                                                c.nref.as<int8_t>(), c.np1.as<double>(), c.np2.as<double>(),       \
-                                               c.nU.as<double>(), c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt)
+                                               c.nU.as<double>(), c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt, \
+                                               h < c.occ_heights ? c.occ[h].as<uint32_t>() : nullptr)
     if (G == 1) PRELIM(1);
     else if (G == 4) PRELIM(4);
     else if (G == 8) PRELIM(8);
