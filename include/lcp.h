@@ -66,7 +66,8 @@ typedef struct {
 
 typedef struct {
     int32_t bucket_log2;   /* bucket grid: 2^bucket_log2 buckets per axis of the virtual cube (R3) */
-    int32_t h_full;        /* candidate lattice: all vertices at node heights <= h_full (R6) */
+    int32_t h_full;        /* candidate lattice: all vertices at node heights <= h_full (R6);
+                              min(h_full, Lfull) <= 10 */
     int32_t precision;     /* lcp_prec_t of the leaf posterior (R17) */
     int32_t slab_rank;     /* z-slab decomposition: this rank ... */
     int32_t slab_count;    /* ... of slab_count (1 = whole domain) */

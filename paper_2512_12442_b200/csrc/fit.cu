@@ -924,6 +924,9 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   if (o.bucket_log2 < 0 || o.bucket_log2 > lfull || o.h_full < 0 || o.slab_rank < 0 ||
       o.slab_rank >= o.slab_count)
     return set_err(c, LCP_EINVAL, "fit: bad options (bucket_log2 / h_full / slab)");
+  // candidate lattice of a node: (2^min(h, h_full) + 1)^3 vertices, indexed in 32 bits
+  if (std::min(o.h_full, lfull) > 10)
+    return set_err(c, LCP_EINVAL, "fit: h_full > 10 (lattice of > 2^30 vertices per node)");
   if (o.slab_count > 1 && (o.slab_level < 1 || o.slab_level > lfull))
     return set_err(c, LCP_EINVAL, "fit: slab_level must be in [1, Lfull] when slab_count > 1");
 

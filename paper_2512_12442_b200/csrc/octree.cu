@@ -39,11 +39,15 @@ __device__ __forceinline__ Lattice node_lattice(const Geom& g, int h, int i, int
   return L;
 }
 
-__device__ __forceinline__ int64_t lattice_vertex(const Geom& g, const Lattice& L, int64_t q) {
-  int t0 = (int)(q % L.cnt[0]);
-  int64_t r = q / L.cnt[0];
-  int t1 = (int)(r % L.cnt[1]);
-  int t2 = (int)(r / L.cnt[1]);
+// q < cnt0 cnt1 cnt2 <= (2^h_full + 1)^3: 32-bit division (the 64-bit one is a ~70-instruction
+// routine, and the finest levels decode 8 corners for each of up to 1.3e8 nodes)
+__device__ __forceinline__ int64_t lattice_vertex(const Geom& g, const Lattice& L, int64_t q64) {
+  const unsigned q = (unsigned)q64, c0 = (unsigned)L.cnt[0], c1 = (unsigned)L.cnt[1];
+  const unsigned r = q / c0;
+  const int t0 = (int)(q - r * c0);
+  const unsigned r2 = r / c1;
+  const int t1 = (int)(r - r2 * c1);
+  const int t2 = (int)r2;
   int64_t v0 = t0 < L.cnt[0] - 1 ? L.base[0] + t0 * L.stride : L.vmax[0];
   int64_t v1 = t1 < L.cnt[1] - 1 ? L.base[1] + t1 * L.stride : L.vmax[1];
   int64_t v2 = t2 < L.cnt[2] - 1 ? L.base[2] + t2 * L.stride : L.vmax[2];
