@@ -391,22 +391,24 @@ cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double
   return cudaGetLastError();
 }
 
-// The 8 child bricks (level Lfull-2 node keys) of level-(Lfull-3) frontier nodes, in
-// node order; slots whose brick holds no grid cell get the key ~0 (skipped).
-__global__ void k_child_bricks(Geom g, const uint64_t* __restrict__ F, int64_t nF, uint64_t* __restrict__ out) {
+// The 8^gen descendant bricks (level Lfull-2 node keys) of level-(Lfull-2-gen) frontier
+// nodes, node by node; slots whose brick holds no grid cell get the key ~0 (skipped).
+__global__ void k_child_bricks(Geom g, const uint64_t* __restrict__ F, int64_t nF, int gen,
+                               uint64_t* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= 8 * nF) return;
+  if (t >= (nF << (3 * gen))) return;
   int i, j, k;
-  node_unkey(F[t >> 3], i, j, k);
-  const int c = (int)(t & 7);
-  const int bi = 2 * i + (c & 1), bj = 2 * j + ((c >> 1) & 1), bk = 2 * k + (c >> 2);
+  node_unkey(F[t >> (3 * gen)], i, j, k);
+  const int c = (int)(t & ((1 << (3 * gen)) - 1)), msk = (1 << gen) - 1;
+  const int bi = (i << gen) + (c & msk), bj = (j << gen) + ((c >> gen) & msk), bk = (k << gen) + (c >> (2 * gen));
   const bool in = BK * bi < g.cells[0] && BK * bj < g.cells[1] && BK * bk < g.cells[2];
   out[t] = in ? node_key(bi, bj, bk) : ~0ull;
 }
 
-cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, uint64_t* out) {
+cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, int gen, uint64_t* out) {
   if (nF <= 0) return cudaSuccess;
-  k_child_bricks<<<(unsigned)((8 * nF + 255) / 256), 256, 0, c.stream>>>(c.g, F, nF, out);
+  const int64_t n = nF << (3 * gen);
+  k_child_bricks<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.g, F, nF, gen, out);
   ++c.n_launch;
   return cudaGetLastError();
 }

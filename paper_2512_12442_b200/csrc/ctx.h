@@ -179,7 +179,7 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
 bool fused_brick_supported(const Ctx& c);
 bool brick_posterior_big(Ctx& c, const int64_t* cells, int64_t n, double* post, cudaError_t& err);
 cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double* post);
-cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, uint64_t* out);
+cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, int gen, uint64_t* out);
 cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post);
 lcp_status_t fused_setup(Ctx& c);
 

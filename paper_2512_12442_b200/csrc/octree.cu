@@ -448,20 +448,24 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       cudaEventDestroy(b1);
       return be;
     };
-    // early pass at level Lfull-3 over the frontier's child bricks, when the previous
-    // level refined nearly everything (then nearly every child brick would be reached
-    // anyway): its vertex marginals serve this level's spacing-2 bound lattice, which
-    // otherwise needs a separate k_marginals pass over 1/8 of all vertices
+    // early pass over the frontier's descendant bricks at level Lfull-4 (64 per node) or
+    // Lfull-3 (8 per node), when the previous level refined nearly everything (then nearly
+    // every descendant brick would be reached anyway): its vertex marginals serve the
+    // spacing-4 / spacing-2 bound lattices of those levels, which otherwise need separate
+    // k_marginals passes over 1/64 + 1/8 of all vertices
     static const bool early_env = [] {
       const char* v = std::getenv("LCP_EARLY_BRICK");
       return !(v && v[0] == '0');
     }();
-    if (c.fused && h == 3 && early_env && level >= 1 && level > slab_level && !c.level_nodes.empty() &&
-        c.level_refined.back() * 10 >= c.level_nodes.back() * 9) {
-      CK(c.child_bricks.ensure(sizeof(uint64_t) * 8 * nF));
-      CK(launch_child_bricks(c, F, nF, c.child_bricks.as<uint64_t>()));
-      CK(brick_pass(c.child_bricks.as<uint64_t>(), 8 * nF));
-      early_bricks = true;   // covers every brick of the next frontier
+    const int gen = h == 4 ? 2 : (h == 3 ? 1 : 0);
+    if (c.fused && gen > 0 && !early_bricks && early_env && level >= 1 && level > slab_level &&
+        !c.level_nodes.empty() &&
+        c.level_refined.back() * 20 >= c.level_nodes.back() * (gen == 2 ? 19 : 18)) {
+      const int64_t nk = nF << (3 * gen);
+      CK(c.child_bricks.ensure(sizeof(uint64_t) * nk));
+      CK(launch_child_bricks(c, F, nF, gen, c.child_bricks.as<uint64_t>()));
+      CK(brick_pass(c.child_bricks.as<uint64_t>(), nk));
+      early_bricks = true;   // covers every brick of the later frontiers
     }
     if (c.fused && h == 2 && !early_bricks) CK(brick_pass(F, nF));
     const int G = h == 0 ? 1 : (h == 1 ? 4 : (h == 2 ? 8 : 32));
