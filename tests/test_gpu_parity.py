@@ -794,3 +794,29 @@ def test_k_sweep_tile_kernels(k, dev):
         mu_o, cov_o = M.cell_posterior(int(brick[q]))
         em, ec = posterior_close(mu_b[q].cpu().numpy(), mu_o, cov_b[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
         assert em <= 1e-5 and ec <= 1e-5, (q, em, ec)
+
+
+def test_slab_union_equals_full_multi_iso(dev):
+    # z-slab decomposition of the fused multi-isovalue step (bench.py --gpus N on c4-type
+    # workloads): the per-slab fields of every isovalue sum to the single-domain fields
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate("c2")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    th = [-0.1, 0.1, 0.3]
+    full = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    ref, nl, nu = full.run_field_multi(th, cfg.alpha, cfg.max_depth, 1000, cfg.mc_seed, 0)
+    ref = ref.clone()
+    for G, sl in ((2, 3), (4, 2), (3, 3)):
+        acc = torch.zeros_like(ref)
+        tot = np.zeros(len(th), np.int64)
+        for r in range(G):
+            ctx = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=r,
+                                       slab_count=G, slab_level=sl)
+            f, n_r, _ = ctx.run_field_multi(th, cfg.alpha, cfg.max_depth, 1000, cfg.mc_seed, 0)
+            acc += f
+            tot += np.asarray(n_r)
+        assert torch.equal(acc, ref), (G, sl)
+        assert np.array_equal(tot, np.asarray(nl)), (G, sl, tot, nl)
