@@ -220,10 +220,25 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo (functional check of the N > 1 path on fewer GPUs than ranks:
+    # ranks share devices round-robin, collectives go through host copies; not a measurement)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def all_reduce(x, op):
+        if backend == "gloo":
+            h = x.cpu()
+            dist.all_reduce(h, op=op)
+            x.copy_(h)
+        else:
+            dist.all_reduce(x, op=op)
     w = generate(args.workload)
     cfg = w.cfg
     kernel, grid, k, b, hf = config_args(cfg)
@@ -329,8 +344,8 @@ def run_ours(args):
     t = torch.tensor([total_ms, mc_ms_tot], dtype=torch.float64, device=dev)
     lv = torch.tensor([leaves_tot, launches, p2_tot], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(lv, op=dist.ReduceOp.SUM)
+        all_reduce(t, dist.ReduceOp.MAX)
+        all_reduce(lv, dist.ReduceOp.SUM)
     total_ms = float(t[0])
     ms_step = total_ms / args.steps
     cells_per_step = ncell * len(w.thetas)
@@ -356,7 +371,7 @@ def run_ours(args):
         barrier()
         te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            all_reduce(te, dist.ReduceOp.MAX)
         e2e = {"value": cells_per_step / float(te[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes),
                "d2h_bytes_per_step": int(fh.numel() * 4 * (1 if fh.numel() > ncell or len(w.thetas) == 1

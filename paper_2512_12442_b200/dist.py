@@ -67,9 +67,11 @@ def gather_field(field, cells, slab_level: int, group=None):
     ranges = [slab_cells(cells, slab_level, r, world) for r in range(world)]
     width = max(c1 - c0 for c0, c1 in ranges)
     c0, c1 = ranges[rank]
-    send = torch.zeros(width, dtype=field.dtype, device=field.device)
+    # gloo moves host tensors only: stage CUDA slices through the host
+    dev = "cpu" if dist.get_backend(group) == "gloo" else field.device
+    send = torch.zeros(width, dtype=field.dtype, device=dev)
     send[: c1 - c0] = field[c0:c1]
-    recv = torch.empty(world * width, dtype=field.dtype, device=field.device)
+    recv = torch.empty(world * width, dtype=field.dtype, device=dev)
     dist.all_gather_into_tensor(recv, send, group=group)
     if rank == 0:
         for r, (a, b) in enumerate(ranges):
