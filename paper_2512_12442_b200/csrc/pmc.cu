@@ -227,9 +227,10 @@ __device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb) {
 // Largest |z| Box-Muller can produce: u_a >= 2^-24 gives R <= sqrt(48 ln 2) = 5.7668;
 // 5.7684 adds the lg2/sqrt approximation error.
 constexpr float ZMAX = 5.7684f;
-// one warp (one cell) per CTA, 16 CTAs per SM: a CTA's resources are released when its
-// own cell is done, so cells with more phase-2 work do not hold idle warps of their CTA
-// (8-warp CTAs: 99.9 ms per 4.19 M-cell chunk; 1-warp CTAs: 97.0 ms)
+// one warp (one cell) per CTA: a CTA's resources are released when its own cell is done,
+// so cells with more phase-2 work do not hold idle warps of their CTA (8-warp CTAs: 99.9 ms
+// per 4.19 M-cell chunk; 1-warp CTAs: 97.0 ms with a 128-register bound, 95.7 ms with the
+// looser bound below -- the same 118 registers, 17 warps per SM, a better schedule)
 #ifndef PMC_WARPS
 #define PMC_WARPS 1
 #endif
@@ -252,7 +253,7 @@ constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are 
 // sample is decided exactly as the one-pass FP32 evaluation decides it; the
 // count is the same estimator.
 #ifndef PMC_MINBLOCKS
-#define PMC_MINBLOCKS 16
+#define PMC_MINBLOCKS 8
 #endif
 #ifndef PMC_ILP
 #define PMC_ILP 2
