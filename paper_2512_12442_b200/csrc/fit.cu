@@ -898,10 +898,14 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   if (!xyz || !yv || !kern || !grid) return set_err(c, LCP_EINVAL, "fit: null argument");
   if (m < 1 || k < 1 || (int64_t)k > m) return set_err(c, LCP_EINVAL, "fit: need 1 <= k <= m");
   if (k > 1024 && (int64_t)k != m) return set_err(c, LCP_EINVAL, "fit: k > 1024 requires k == m");
-  if (!(kern->variance > 0) || !(kern->nugget >= 0) || (kern->kind != LCP_K_SE && kern->kind != LCP_K_MATERN52))
+  if (!(kern->variance > 0) || !(kern->nugget >= 0) || !std::isfinite(kern->variance) ||
+      !std::isfinite(kern->nugget) || !std::isfinite(kern->prior_mean) ||
+      (kern->kind != LCP_K_SE && kern->kind != LCP_K_MATERN52))
     return set_err(c, LCP_EINVAL, "fit: bad kernel parameters");
   for (int d = 0; d < 3; ++d)
-    if (!(kern->lengthscale[d] > 0) || grid->cells[d] < 1 || !(grid->hi[d] > grid->lo[d]) || grid->cells[d] > (1 << 20))
+    if (!(kern->lengthscale[d] > 0) || !std::isfinite(kern->lengthscale[d]) || grid->cells[d] < 1 ||
+        !(grid->hi[d] > grid->lo[d]) || !std::isfinite(grid->lo[d]) || !std::isfinite(grid->hi[d]) ||
+        grid->cells[d] > (1 << 20))
       return set_err(c, LCP_EINVAL, "fit: bad lengthscale or grid");
   lcp_opts_t o{};
   o.bucket_log2 = 0;

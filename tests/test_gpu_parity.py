@@ -247,6 +247,12 @@ def test_error_codes(dev):
     with pytest.raises(LcpError) as e:
         ctx.fit_local(X, y, kernel, cfg.m + 1, grid)
     assert e.value.status == LCP_EINVAL
+    for bad_kernel in ((kernel[0], float("inf")) + tuple(kernel[2:]),
+                       tuple(kernel[:4]) + (float("nan"),),
+                       (kernel[0], kernel[1], (float("inf"), 1.0, 1.0)) + tuple(kernel[3:])):
+        with pytest.raises(LcpError) as e:
+            ctx.fit_local(X, y, bad_kernel, k, grid, bucket_log2=b, h_full=hf)
+        assert e.value.status == LCP_EINVAL, bad_kernel
     for bad in ("x", "y"):
         Xb, yb = X.clone(), y.clone()
         (Xb[5, 1:2] if bad == "x" else yb[7:8]).fill_(float("nan"))
