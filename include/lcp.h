@@ -131,7 +131,8 @@ lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, i
  * (PAPER.md:80-100).  Each bucket keeps its k nearest inducing points and
  * evaluates Eq. 1 with the A_M term on them.  kernel->nugget
  * is the jitter added to K_SS (use ~1e-8 sigma_f^2).  Host or device pointers
- * as for lcp_fit_local.  Errors as lcp_fit_local, plus EINVAL for m > 60000. */
+ * as for lcp_fit_local.  Errors as lcp_fit_local, plus EINVAL for m > 60000 or a
+ * non-finite A_M entry. */
 lcp_status_t lcp_fit_sgpr(lcp_ctx_t* ctx, const double* xyz_M, const double* mu_M, const double* A_M,
                           int64_t m, int32_t on_device, const lcp_kernel_t* kernel, int32_t k,
                           const lcp_grid_t* grid, const lcp_opts_t* opts);

@@ -30,7 +30,7 @@ lcp_status_t check_device_errors(Ctx& c) {
     e = cudaMemsetAsync(c.derr.p, 0, sizeof(int), c.stream);
     if (e != cudaSuccess) return cuda_err(c, e, "device error reset");
   }
-  if (h & DERR_INPUT) return set_err(c, LCP_EINVAL, "non-finite observation coordinate or value");
+  if (h & DERR_INPUT) return set_err(c, LCP_EINVAL, "non-finite input (observation coordinate or value, or an A_M entry)");
   if (h & DERR_FACTOR) return set_err(c, LCP_EFACTOR, "a bucket covariance K_y is not PD after jitter");
   if (h & DERR_NUMERIC) return set_err(c, LCP_ENUMERIC, "posterior variance below -1e-8 sigma_f^2");
   if (h & DERR_OVERFLOW) return set_err(c, LCP_EINVAL, "cell or bucket id out of range");

@@ -51,6 +51,14 @@ __global__ void k_obs_bin(Geom g, const double* __restrict__ X, const double* __
   obs_key[o] = morton3(cc[0], cc[1], cc[2]);
 }
 
+// DERR_INPUT if any of n values is not finite (grid-stride)
+__global__ void k_check_finite(const double* __restrict__ v, int64_t n, int* __restrict__ derr) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(v[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(derr, DERR_INPUT);
+}
+
 // occupancy bitmaps: bit (key >> 3h) of occ_h set for every observation's finest-cell key
 __global__ void k_occ_set(const uint64_t* __restrict__ key, int64_t m, int nh, uint32_t* __restrict__ o0,
                           uint32_t* __restrict__ o1, uint32_t* __restrict__ o2) {
@@ -1083,6 +1091,9 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     CK(c.sgpr_A.ensure(sizeof(double) * (size_t)m * m));
     CK(cudaMemcpyAsync(c.sgpr_A.p, AM, sizeof(double) * (size_t)m * m,
                        on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    k_check_finite<<<std::min<int64_t>(((int64_t)m * m + 255) / 256, 4 * (int64_t)c.sm_count * 8), 256, 0,
+                     c.stream>>>(c.sgpr_A.as<double>(), (int64_t)m * m, c.derr.as<int>());
+    ++c.n_launch;
     int grid_f = std::min(nbk, c.sm_count * 2);
     CK(c.fscratch.ensure(sizeof(double) * 5 * (size_t)k * k * grid_f));
     size_t smem = sizeof(double) * 4 * (size_t)k;

@@ -826,3 +826,18 @@ def test_slab_union_equals_full_multi_iso(dev):
             tot += np.asarray(n_r)
         assert torch.equal(acc, ref), (G, sl)
         assert np.array_equal(tot, np.asarray(nl)), (G, sl, tot, nl)
+
+
+def test_sgpr_non_finite_is_einval(dev):
+    from paper_2512_12442_b200 import Context, LcpError
+    from paper_2512_12442_b200.lcp import LCP_EINVAL
+    w, cfg, muM, AM = _sgpr_inputs("t1", 20.0)
+    kernel = (cfg.kernel, cfg.variance, cfg.lengthscale, 1e-9 * cfg.variance, cfg.prior_mean)
+    grid = (cfg.lo, cfg.hi, cfg.cells)
+    AMb = AM.copy()
+    AMb[3, 5] = np.nan
+    ctx = Context(0)
+    with pytest.raises(LcpError) as e:
+        ctx.fit_sgpr(w.X, muM, AMb, kernel, cfg.k, grid, bucket_log2=cfg.bucket_log2, h_full=cfg.h_full)
+    assert e.value.status == LCP_EINVAL
+    ctx.fit_sgpr(w.X, muM, AM, kernel, cfg.k, grid, bucket_log2=cfg.bucket_log2, h_full=cfg.h_full)
