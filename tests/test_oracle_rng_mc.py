@@ -187,3 +187,47 @@ def test_mc_standard_error_scaling():
         spreads.append(np.std(est))
     ratio = spreads[0] / spreads[1]
     assert 4 / 1.6 < ratio < 4 * 1.6
+
+
+def _genz_lcp(mu, S, th, seed):
+    # LCP = 1 - P(all corners < theta) - P(all corners > theta) (R5),
+    # each orthant by scipy's Genz integration of the 8-variate normal
+    mvn = stats.multivariate_normal
+    kw = dict(cov=S, allow_singular=True, abseps=2e-5, releps=0, maxpts=400000)
+    pb = mvn.cdf(np.full(8, th), mean=mu, rng=np.random.default_rng(seed), **kw)
+    pa = mvn.cdf(np.full(8, -th), mean=-mu, rng=np.random.default_rng(seed + 1), **kw)
+    return 1.0 - pb - pa
+
+
+@pytest.mark.parametrize("name", ["c1", "t2"])
+def test_pmc_cells_composition_vs_genz(name):
+    # Pin of the composed leaf estimator orc_pmc_cells (cell posterior -> PI8 corner
+    # reorder -> clamped chol8 -> Philox/Box-Muller MC count): on real
+    # cell posteriors of the config, with LCP in (0.05, 0.95), the N = 40 000 estimate
+    # agrees with Genz orthant probabilities of the same (mu, Sigma) within 4 SE.  A wrong
+    # corner permutation, a transposed factor or a dropped Sigma term moves these cells
+    # by many SE (the posterior correlations are strong and of both signs).
+    from workloads import generate
+    w = generate(name)
+    cfg = w.cfg
+    M = O.Model.from_config(cfg, w.X, w.y)
+    th = w.thetas[0]
+    ncell = int(np.prod(cfg.cells))
+    probe = np.arange(0, ncell, max(1, ncell // 3000), dtype=np.int64)
+    coarse = M.pmc_cells(probe, th, 400, 31)
+    mid = probe[(coarse > 0.08) & (coarse < 0.92)]
+    assert len(mid) >= 12
+    cells = np.random.default_rng(5).choice(mid, 12, replace=False)
+    N = 40000
+    got = M.pmc_cells(cells, th, N, cfg.mc_seed)
+    zs = []
+    for q, c in enumerate(cells):
+        mu, S = M.cell_posterior(int(c))
+        want = _genz_lcp(mu, 0.5 * (S + S.T), th, 100 + q)
+        assert 0.03 < want < 0.97, (int(c), want)
+        se = math.sqrt(want * (1 - want) / N)
+        zs.append((got[q] - want) / se)
+    zs = np.array(zs)
+    assert np.abs(zs).max() <= 4.0, zs
+    # the 12 deviations behave like N(0, 1) draws (a biased estimator would shift them)
+    assert abs(zs.mean()) <= 4.0 / math.sqrt(len(zs)), zs
