@@ -323,6 +323,14 @@ class Context:
         raw = self._wrap_dev(p.value, n.value * NODE_DTYPE.itemsize, self._torch.uint8)
         return raw.cpu().numpy().view(NODE_DTYPE)
 
+    def node_records_device(self):
+        """The node records of the last refine as a raw uint8 CUDA tensor (a copy;
+        view it as int32 (n, 12): level, i, j, k, case, refine, then p1, p2, U as FP64)."""
+        n = C.c_int64()
+        p = C.c_void_p()
+        self._check(self._L.lcp_node_records(self._h, C.byref(n), C.byref(p)), "lcp_node_records")
+        return self._wrap_dev(p.value, n.value * NODE_DTYPE.itemsize, self._torch.uint8)
+
     def cell_posterior(self, cells):
         torch = self._torch
         n = len(cells)

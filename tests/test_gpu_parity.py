@@ -344,12 +344,7 @@ def test_full_size_c5_sampled(dev):
             bad += 1
         assert abs(o["U"] - r["U"]) < 1e-6
     assert bad == 0
-    lv = leaves.cpu().numpy()
-    sel = g.choice(len(lv), 96, replace=False)
-    lcp_g = ctx.pmc_cells(leaves, th, cfg.n_samples, cfg.mc_seed).cpu().numpy()[sel]
-    lcp_o = M.pmc_cells(lv[sel], th, cfg.n_samples, cfg.mc_seed)
-    frac, mean, mx = lcp_parity(lcp_g, lcp_o, cfg.n_samples)
-    assert frac >= 0.99 and mean <= 1e-4, (frac, mean, mx)
+    # leaf sets and LCP at full size: tests/test_gpu_headline.py
 
 
 @pytest.mark.parametrize("name", ["t2", "c2", "p1"])
@@ -531,27 +526,6 @@ def test_multi_iso_first_row_is_single_pass(dev):
             assert frac >= 0.999 and mean <= 1e-5, (t, frac, mean, mx)
 
 
-def test_multi_iso_c4_full_size_sampled(dev):
-    # BASELINE c4 (three isovalues) at full size through the fused path: sampled
-    # union cells against the oracle's one-stream multi-isovalue MC.
-    w, ctx, M = _ctx("c4", dev, keep_records=False)
-    cfg = w.cfg
-    thetas = list(w.thetas)
-    fields, nl, nu = ctx.run_field_multi(thetas, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, 0)
-    cells_g, mask_g = ctx.union_cells()
-    cells_g, mask_g = cells_g.cpu().numpy(), mask_g.cpu().numpy()
-    assert nu == len(cells_g) and nu >= max(nl)
-    for t in range(len(thetas)):
-        assert int(((mask_g >> t) & 1).sum()) == nl[t]
-    sel = np.random.default_rng(3).choice(nu, 64, replace=False)
-    lcp_o = M.pmc_cells_multi(cells_g[sel], thetas, cfg.n_samples, cfg.mc_seed, 0,
-                              mask=mask_g[sel].astype(np.uint32))
-    F = fields.cpu().numpy()
-    for t in range(len(thetas)):
-        frac, mean, mx = lcp_parity(F[t][cells_g[sel]], lcp_o[t], cfg.n_samples)
-        assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
-
-
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_brick_pass_records_equal_leaf_posterior_path(name, dev):
     # the refine-time brick pass (vertex marginals + MC records of every frontier brick)
@@ -629,12 +603,12 @@ def test_multi_iso_edges_and_errors(dev):
         ctx.pmc_cells_multi(torch.arange(10, device=dev), [0.0, float("nan")], 100, 1)
     # 16 isovalues (the largest instantiation) against the oracle on a few cells
     th16 = list(np.linspace(-0.8, 0.8, 16))
-    cells = torch.from_numpy(random_cells("t1", 64, 9)).to(dev)
+    cells = torch.from_numpy(random_cells("t1", 3000, 9)).to(dev)
     got = ctx.pmc_cells_multi(cells, th16, 700, 21, stream=4).cpu().numpy()
     want = M.pmc_cells_multi(cells.cpu().numpy(), th16, 700, 21, 4)
     for t in range(16):
         frac, mean, mx = lcp_parity(got[t], want[t], 700)
-        assert frac >= 0.98 and mean <= 2e-4, (t, frac, mean, mx)
+        assert frac >= 0.999 and mean <= 1e-4, (t, frac, mean, mx)
 
 
 def test_big_k_brick_posterior_exact_gp(dev):
