@@ -143,41 +143,99 @@ def load_traffic(cells_per_launch, kernel="k_pmc"):
         return None
 
 
-def oracle_sample(w, oracle_model=None, stride=16):
-    """The oracle as it stands on a bounded sample of the workload: the octree
-    on the level-3 subtree (0,0,0) and the leaf pass on every `stride`-th leaf
-    of it (time extrapolated to all its leaves); the model build is amortised
-    by the sample's share of the domain.  Returns (cells/s, seconds, detail)."""
+def sample_subtrees(cfg, lfull):
+    """BASELINE.md §3 sample of the oracle arm: the level-3 octree subtrees with z-index 0
+    (1/8 of the domain), visited in a fixed co-prime order so that consecutive steps
+    land in different places (corner, edge and interior subtrees).  Grids of at most
+    2^21 cells (c1-c3) are sampled whole (subtree None)."""
+    if int(np.prod(cfg.cells)) <= (1 << 21) or cfg.max_depth < 3:
+        return [None]
+    side = 1 << (lfull - 3)
+    ni, nj = [-(-cfg.cells[d] // side) for d in (0, 1)]
+    subs = [(3, i, j, 0) for j in range(nj) for i in range(ni)]
+    n = len(subs)
+    stride = next(s for s in (37, 29, 23, 19, 17, 13, 11, 7, 5, 3, 1) if np.gcd(s, n) == 1)
+    return [subs[(q * stride) % n] for q in range(n)]
+
+
+ORACLE_LEAVES_PER_STEP = 4000
+
+
+def oracle_step(w, M, sub):
+    """One step of the oracle arm on a bounded sample, timed as it runs: the oracle's octree
+    (Alg. 1) on subtree `sub` (None = the whole grid) for every isovalue, then its leaf pass
+    (posterior, chol8, MC) on at most ORACLE_LEAVES_PER_STEP evenly spaced leaves of it.
+    Returns (measured seconds, leaf cells of the sample over all isovalues, seconds of
+    the octree, seconds and cells of the leaf pass)."""
+    cfg = w.cfg
+    t_oct = t_pmc = 0.0
+    n_leaf = n_pmc = 0
+    t_start = time.perf_counter()
+    for it, th in enumerate(w.thetas):
+        t0 = time.perf_counter()
+        _, leaves = M.octree(th, cfg.alpha, cfg.max_depth, subtree=sub)
+        t_oct += time.perf_counter() - t0
+        pick = leaves[np.unique(np.linspace(0, len(leaves) - 1, min(len(leaves), ORACLE_LEAVES_PER_STEP)).astype(
+            np.int64))] if len(leaves) else leaves
+        t0 = time.perf_counter()
+        if len(pick):
+            M.pmc_cells(pick, th, cfg.n_samples, cfg.mc_seed, it)
+        t_pmc += time.perf_counter() - t0
+        n_leaf += len(leaves)
+        n_pmc += len(pick)
+    return time.perf_counter() - t_start, n_leaf, t_oct, t_pmc, n_pmc
+
+
+def oracle_rate(cfg, M, t_fit, secs_oct, secs_pmc, n_leaf, n_pmc, sub_cells):
+    """Leaf cells/s of the oracle's whole path estimated from measured parts: seconds per
+    leaf cell of the octree (sample subtree) + of the leaf pass (its sampled leaves) + the
+    model build amortised by the sample's share of the grid."""
+    total = int(np.prod(cfg.cells))
+    per_leaf = (secs_oct / max(n_leaf, 1) + secs_pmc / max(n_pmc, 1)
+                + t_fit * (sub_cells / total) / max(n_leaf, 1))
+    return 1.0 / per_leaf
+
+
+def _sub_cells(cfg, lfull, sub):
+    if sub is None:
+        return int(np.prod(cfg.cells))
+    side = 1 << (lfull - sub[0])
+    return int(np.prod([max(0, min(side, cfg.cells[d] - side * sub[1 + d])) for d in range(3)]))
+
+
+def oracle_sample(w, steps=1, warmup=0):
+    """Oracle arm: build the model once (timed), then `warmup + steps` sample steps.
+    Returns (value, measured seconds per timed step, detail dict)."""
     import oracle as O
     cfg = w.cfg
     t0 = time.perf_counter()
-    M = oracle_model or O.Model.from_config(cfg, w.X, w.y)
+    M = O.Model.from_config(cfg, w.X, w.y)
     t_fit = time.perf_counter() - t0
-    lf = M.lfull
-    sl = min(3, cfg.max_depth)
-    side = 1 << (lf - sl)
-    sample_cells = int(np.prod([min(side, c) for c in cfg.cells]))
-    total_cells = int(np.prod(cfg.cells))
-    t_oct = t_pmc = 0.0
-    n_leaf = n_done = 0
-    for it, th in enumerate(w.thetas):
-        t0 = time.perf_counter()
-        _, leaves = M.octree(th, cfg.alpha, cfg.max_depth, subtree=(sl, 0, 0, 0))
-        t_oct += time.perf_counter() - t0
-        sub = leaves[::stride]
-        t0 = time.perf_counter()
-        if len(sub):
-            M.pmc_cells(sub, th, cfg.n_samples, cfg.mc_seed, it)
-        dt = time.perf_counter() - t0
-        t_pmc += dt * (len(leaves) / max(len(sub), 1))
-        n_leaf += len(leaves)
-        n_done += len(sub)
-    secs = t_oct + t_pmc + t_fit * sample_cells / total_cells
-    detail = (f"oracle (C, FP64, OpenMP) on the level-{sl} subtree (0,0,0) = {sample_cells} cells "
-              f"({sample_cells / total_cells:.2e} of the grid): octree {t_oct:.2f} s, leaf pass on "
-              f"{n_done} of its {n_leaf} leaves x {len(w.thetas)} isovalue(s) extrapolated to {t_pmc:.2f} s, "
-              f"model build {t_fit:.2f} s amortised by the sample's share")
-    return sample_cells * len(w.thetas) / secs, secs, detail, M
+    subs = sample_subtrees(cfg, M.lfull)
+    secs = []
+    acc = [0.0, 0.0, 0, 0, 0]
+    visited = []
+    for s in range(warmup + steps):
+        sub = subs[s % len(subs)]
+        dt, n_leaf, t_oct, t_pmc, n_pmc = oracle_step(w, M, sub)
+        if s >= warmup:
+            secs.append(dt)
+            for q, v in enumerate((t_oct, t_pmc, n_leaf, n_pmc, _sub_cells(cfg, M.lfull, sub))):
+                acc[q] += v
+            visited.append(sub)
+    value = oracle_rate(cfg, M, t_fit, acc[0], acc[1], acc[2], acc[3], acc[4])
+    total_leaf_est = acc[2] * int(np.prod(cfg.cells)) / max(acc[4], 1)
+    where = ("the whole grid" if subs[0] is None else
+             f"level-3 subtrees (L, i, j, k) {visited[:6]}{' ...' if len(visited) > 6 else ''} of the z-index-0 "
+             f"layer (BASELINE.md §3; {len(subs)} subtrees = 1/8 of the domain)")
+    detail = {"sample": (f"oracle (C, FP64, OpenMP) per step: octree (Alg. 1) on {where}, every isovalue; "
+                         f"leaf pass on <= {ORACLE_LEAVES_PER_STEP} evenly spaced leaves of it; model build "
+                         f"{t_fit:.2f} s once, amortised by the sample's share of the grid"),
+              "measured_s_per_step": float(np.mean(secs)) if secs else None,
+              "octree_s": acc[0], "leaf_pass_s": acc[1], "leaf_cells_in_sample": acc[2],
+              "leaf_pass_cells": acc[3], "sample_grid_cells": acc[4], "model_build_s": t_fit,
+              "extrapolated_full_workload_s": total_leaf_est / value if value else None}
+    return value, (float(np.mean(secs)) if secs else 0.0), detail
 
 
 def run_reference(args):
@@ -189,21 +247,17 @@ def run_reference(args):
     w = generate(args.workload)
     cfg = w.cfg
     cores = O.num_threads()
-    M = None
-    vals = []
-    tot = 0.0
-    detail = ""
-    for s in range(args.warmup + args.steps):
-        v, secs, detail, M = oracle_sample(w, M)
-        if s >= args.warmup:
-            vals.append(v)
-            tot += secs
-    value = float(np.mean(vals))
+    value, s_step, detail = oracle_sample(w, args.steps, args.warmup)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / max(args.steps, 1),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * s_step,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": workload_desc(cfg, w.thetas), "sample": detail},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": detail},
+           "data": "synthetic", "config": {"workload": workload_desc(cfg, w.thetas), "sample": detail["sample"]},
+           "value_note": ("leaf cells/s of the oracle's whole path, from the measured per-leaf seconds of "
+                          "its octree and leaf pass on the sample; ms_per_step is the measured time of one "
+                          "sample step"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": detail["sample"]},
+           "oracle_detail": detail,
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -214,7 +268,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2512_12442_b200 import Context, config_args
-    from paper_2512_12442_b200.dist import gather_field
+    from paper_2512_12442_b200.dist import cell_ranges, equal_z_cuts, gather_fields, plan_z_cuts
     from workloads import generate
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -249,62 +303,68 @@ def run_ours(args):
     multi_fields = (torch.empty((len(w.thetas), ncell), dtype=torch.float32, device=dev)
                     if len(w.thetas) > 1 else None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    slab = dict(slab_rank=rank, slab_count=world, slab_level=3) if world > 1 else {}
+    slab = dict(slab_rank=rank, slab_count=world) if world > 1 else {}   # automatic slab level (lcp.h)
     if args.dense:
         # pruning-free baseline (BASELINE c3): exact GP (k = m, one bucket), every cell of the slab
-        from paper_2512_12442_b200.dist import slab_cells
         if args.dense == "exact":
             k, b = cfg.m, 0
-        c0, c1 = slab_cells(cfg.cells, 3, rank, world) if world > 1 else (0, ncell)
+        dense_cuts = equal_z_cuts(cfg.cells, world, cfg.max_depth) if world > 1 else [0, cfg.cells[2]]
+        c0, c1 = cell_ranges(cfg.cells, dense_cuts)[rank if world > 1 else 0]
         from workloads.gen import morton_sorted_cells
         dense_cells = morton_sorted_cells(cfg.cells, c0, c1, device=dev)   # brick-kernel order
         dense_lcp = torch.empty(c1 - c0, dtype=torch.float32, device=dev)
     ctx = Context(local)
+    if world > 1:
+        dist.barrier()   # every rank joins the group's first collective
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     def step(host=None):
-        """fit + run_field for every isovalue; returns (leaves, mc_ms, phase-2 samples)."""
+        """fit + run_field for every isovalue; returns (leaf cells summed over the isovalues,
+        k_pmc ms, phase-2 samples, leaf cells of the union of isovalues).  host = (X, y, field)
+        numpy arrays in pinned memory: the e2e leg, inputs and the output field through the
+        C ABI's host-pointer paths (at N > 1 the gathered field is read back on rank 0)."""
         if host is None:
             ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, extreme_iters=args.extreme, **slab)
         else:
             ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf,
                           extreme_iters=args.extreme, **slab)
+        abi_host_out = host is not None and world == 1
         leaves = 0
         mc_ms = 0.0
         p2 = 0
         if len(w.thetas) > 1 and not args.dense and not args.separate_iso:
             # NEXT-3: all isovalues in one fused leaf pass (one posterior, one sample stream)
-            fields_out = multi_fields
+            fields_out = host[2].reshape(len(w.thetas), ncell) if abi_host_out else multi_fields
             _, nl, nu = ctx.run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed,
                                             0, fields=fields_out)
             st = ctx.stats()
             if world > 1:
-                for t in range(len(w.thetas)):
-                    gather_field(fields_out[t], cfg.cells, 3)
-            if host is not None and rank == 0:
-                host[2].copy_(fields_out.reshape(-1)[: host[2].numel()], non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-            return int(nu), st["mc_ms"], st["pmc_phase2_samples"]
+                gather_fields(fields_out, cfg.cells, plan_z_cuts(st))
+            if host is not None and not abi_host_out and rank == 0:
+                host[2].reshape(len(w.thetas), ncell)[:] = fields_out.cpu().numpy()
+            return int(np.sum(nl)), st["mc_ms"], st["pmc_phase2_samples"], int(nu)
         for it, th in enumerate(w.thetas):
             if args.dense:
                 ctx.pmc_cells(dense_cells, th, cfg.n_samples, cfg.mc_seed, it, out=dense_lcp)
-                ctx.scatter_field(dense_cells, dense_lcp, field)
+                out = ctx.scatter_field(dense_cells, dense_lcp, field)
+                if abi_host_out:
+                    host[2][:] = out.cpu().numpy()
                 n = len(dense_cells)
             else:
-                _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it, field=field)
+                _, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed, it,
+                                     field=host[2] if abi_host_out else field)
             leaves += n
             st = ctx.stats()
             mc_ms += st["mc_ms"]
             p2 += st["pmc_phase2_samples"]
-            if world > 1:
-                gather_field(field, cfg.cells, 3)   # NCCL all-gather of the slab slices
-            if host is not None and rank == 0:
-                host[2].copy_(field, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-        return leaves, mc_ms, p2
+            if world > 1:   # slab slices -> rank 0
+                gather_fields(field, cfg.cells, dense_cuts if args.dense else plan_z_cuts(st))
+                if host is not None and rank == 0:
+                    host[2][:] = field.cpu().numpy()
+        return leaves, mc_ms, p2, leaves
 
     for _ in range(args.warmup):
         step()
@@ -316,6 +376,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     total_ms = 0.0
     leaves_tot = 0
+    union_tot = 0
     mc_ms_tot = 0.0
     p2_tot = 0
     st_phase = {"fit_ms": 0.0, "refine_ms": 0.0, "brick_pass_ms": 0.0, "posterior_ms": 0.0, "chol_ms": 0.0,
@@ -326,11 +387,12 @@ def run_ours(args):
         flush.fill_(1)                      # L2 flush between timed steps (256 MB > 126 MB L2)
         torch.cuda.synchronize()
         e0.record()
-        leaves, mc_ms, p2 = step()
+        leaves, mc_ms, p2, union = step()
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
         leaves_tot += leaves
+        union_tot += union
         mc_ms_tot += mc_ms
         p2_tot += p2
         s = ctx.stats()
@@ -342,41 +404,51 @@ def run_ours(args):
     clk = clocks.stop()
     launches = ctx.stats()["launches"] - launches0
     t = torch.tensor([total_ms, mc_ms_tot], dtype=torch.float64, device=dev)
-    lv = torch.tensor([leaves_tot, launches, p2_tot], dtype=torch.float64, device=dev)
+    lv = torch.tensor([leaves_tot, launches, p2_tot, union_tot], dtype=torch.float64, device=dev)
     if world > 1:
         all_reduce(t, dist.ReduceOp.MAX)
         all_reduce(lv, dist.ReduceOp.SUM)
     total_ms = float(t[0])
     ms_step = total_ms / args.steps
     cells_per_step = ncell * len(w.thetas)
-    value = cells_per_step / (ms_step / 1000.0)
-    leaves_step = float(lv[0]) / args.steps
-    samples_step = leaves_step * cfg.n_samples
+    leaves_step = float(lv[0]) / args.steps          # leaf cells x isovalues: LCP values produced
+    union_step = float(lv[3]) / args.steps           # cells through k_pmc (the fused pass tests T isovalues)
+    # BASELINE metric "PMC LCP cells/sec": leaf cells (LCP values) of the whole job per second
+    # of the end-to-end step (fit + octree + leaf pass + scatter [+ gather])
+    value = leaves_step / (ms_step / 1000.0)
+    samples_step = union_step * cfg.n_samples
 
-    # e2e: the same step through the C ABI with host (pinned) buffers
+    # e2e: the same step through the C ABI with host (pinned) buffers: X, y in through
+    # lcp_fit_local's host path, the LCP field(s) out through lcp_run_field(_multi)'s host path
     e2e = None
     if not args.no_e2e:
+        nfield = ncell * (len(w.thetas) if multi_fields is not None and not args.separate_iso and not args.dense else 1)
         Xh = torch.from_numpy(np.array(w.X)).pin_memory().numpy()
         yh = torch.from_numpy(np.array(w.y)).pin_memory().numpy()
-        fh = torch.empty(ncell * (len(w.thetas) if multi_fields is not None and not args.separate_iso else 1),
-                         dtype=torch.float32).pin_memory()
+        fh = torch.empty(nfield, dtype=torch.float32).pin_memory().numpy()
         host = (Xh, yh, fh)
         step(host)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        leaves_e = 0
         for _ in range(args.e2e_steps):
-            step(host)
+            leaves_e += step(host)[0]
         torch.cuda.synchronize()
         barrier()
-        te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64, device=dev)
+        te = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps, leaves_e / args.e2e_steps],
+                          dtype=torch.float64, device=dev)
         if world > 1:
+            tl = te.clone()
             all_reduce(te, dist.ReduceOp.MAX)
-        e2e = {"value": cells_per_step / float(te[0]), "unit": UNIT,
+            all_reduce(tl, dist.ReduceOp.SUM)
+            te[1] = tl[1]
+        e2e = {"value": float(te[1]) / float(te[0]), "unit": UNIT,
                "h2d_bytes_per_step": int(Xh.nbytes + yh.nbytes),
-               "d2h_bytes_per_step": int(fh.numel() * 4 * (1 if fh.numel() > ncell or len(w.thetas) == 1
-                                                             else len(w.thetas))),
-               "seconds_per_step": float(te[0])}
+               "d2h_bytes_per_step": int(fh.nbytes) * (1 if len(w.thetas) == 1 or fh.size > ncell else len(w.thetas)),
+               "seconds_per_step": float(te[0]),
+               "path": ("C ABI host pointers: lcp_fit_local(xy_on_device=0), lcp_run_field(_multi)(out_on_device=0)"
+                        if world == 1 else "lcp_fit_local host inputs; slab fields gathered to rank 0, then read back")}
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -414,8 +486,10 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline:
         try:
             import oracle as O
-            v, secs, detail, _ = oracle_sample(w)
-            cpu = {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle", "sample": detail}
+            v, secs, detail = oracle_sample(w, 1, 0)
+            cpu = {"value": v, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+                   "sample": detail["sample"], "measured_s": secs + detail["model_build_s"],
+                   "extrapolated_full_workload_s": detail["extrapolated_full_workload_s"]}
         except Exception as ex:  # the GPU number stands on its own
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
                    "sample": f"failed: {ex}"}
@@ -431,7 +505,8 @@ def run_ours(args):
                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                       "l2": "flushed between timed steps (256 MB write, outside the step events)"},
            "end_to_end_octree_lcp_s": ms_step / 1000.0,
-           "leaf_cells_per_step": leaves_step, "pmc_leaf_cells_per_s": leaves_step / (ms_step / 1000.0),
+           "leaf_cells_per_step": leaves_step, "grid_cells_per_s": cells_per_step / (ms_step / 1000.0),
+           "pmc_cells_per_step": union_step,
            "samples_per_step": samples_step,
            "phase_ms_per_step": {k2: v2 / args.steps for k2, v2 in st_phase.items()},
            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(float(lv[1])),

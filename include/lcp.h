@@ -69,9 +69,16 @@ typedef struct {
     int32_t h_full;        /* candidate lattice: all vertices at node heights <= h_full (R6);
                               min(h_full, Lfull) <= 10 */
     int32_t precision;     /* lcp_prec_t of the leaf posterior (R17) */
-    int32_t slab_rank;     /* z-slab decomposition: this rank ... */
-    int32_t slab_count;    /* ... of slab_count (1 = whole domain) */
-    int32_t slab_level;    /* octree level whose z-layers are split across ranks (default 3) */
+    int32_t slab_rank;     /* z-slab decomposition (SURVEY §8(e)): this rank ... */
+    int32_t slab_count;    /* ... of slab_count (1 = whole domain).  Every rank evaluates the
+                              octree levels 0..slab_level over the whole domain; the first refine
+                              after a fit then cuts the z-layers of level slab_level into
+                              slab_count contiguous ranges by prefix sums of the refined
+                              level-slab_level nodes per layer (identical on every rank, no
+                              communication) and keeps the children of layers [z0, z1) only;
+                              the cut stands until the next fit (lcp_stats_json "slab") */
+    int32_t slab_level;    /* <= 0: automatic -- the shallowest level with >= 2 slab_count
+                              z-layers, at most min(max_depth, Lfull - 3); else that level */
     int32_t keep_records;  /* parity tap: keep per-node records of levels < keep_records (0 = none) */
     int32_t extreme_iters; /* NEXT-1 (R26): iterations of the continuous extreme search at nodes
                               coarser than h_full; 0 = lattice only */
@@ -257,6 +264,27 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap);
 
 /* wait for all work queued on the ctx stream; reports deferred device errors */
 lcp_status_t lcp_synchronize(lcp_ctx_t* ctx);
+
+/* ---- z-slab decomposition across GPUs (the paper itself is
+ * single-process).  Host-only arithmetic, no device work, no ctx:
+ * the rules lcp_octree_refine applies under opts.slab_count > 1, exposed so that
+ * the caller can size and route the final gather (and test the plan on a CPU). */
+
+/* automatic slab level for `slab_count` ranks on `grid` (opts.slab_level <= 0):
+ * the shallowest level whose z-layers number >= 2 slab_count, at most
+ * min(max_depth, Lfull - 3) and at least 1.  Returns -1 on bad arguments. */
+int32_t lcp_slab_auto_level(const lcp_grid_t* grid, int32_t slab_count, int32_t max_depth);
+
+/* contiguous z-layer ranges of `slab_count` ranks: cuts_out[0..slab_count]
+ * (host, caller-owned), rank r owns layers [cuts_out[r], cuts_out[r+1]).  The cuts
+ * minimise the largest rank weight (then the sum of squared rank weights; ties to
+ * the earlier cut) over weights[0..n_layers) (host; >= 0; refine uses the expected
+ * leaf work of the refined level-slab_level nodes of each layer: 1 + 1024 x the
+ * fraction of their lattice vertices with both tails > threshold / 8); every rank
+ * gets >= 1 layer when n_layers >= slab_count; all-zero weights give equal layer
+ * counts.  LCP_EINVAL on null
+ * pointers, n_layers < 1, slab_count < 1 or a negative weight. */
+lcp_status_t lcp_slab_cuts(const int64_t* weights, int32_t n_layers, int32_t slab_count, int32_t* cuts_out);
 
 #ifdef __cplusplus
 }

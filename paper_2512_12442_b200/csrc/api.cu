@@ -428,9 +428,49 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
   arr("level_case1", c.level_case[1]);
   arr("level_case2", c.level_case[2]);
   arr("level_case3", c.level_case[3]);
+  if (c.opts.slab_count > 1) {   // the z-slab plan (identical on every rank)
+    const int64_t side = (int64_t)1 << (c.g.lfull - c.slab_L);
+    std::vector<int64_t> cuts(c.slab_cuts.begin(), c.slab_cuts.end()), ccuts;
+    for (int z : c.slab_cuts) ccuts.push_back(std::min<int64_t>((int64_t)z * side, c.g.cells[2]));
+    std::snprintf(tmp, sizeof tmp,
+                  ", \"slab\": {\"rank\": %d, \"count\": %d, \"level\": %d, \"layers\": %d, \"z0\": %d, "
+                  "\"z1\": %d, \"planned\": %d, \"records_ready\": %d, \"record_cells\": %lld",
+                  c.opts.slab_rank, c.opts.slab_count, c.slab_L, c.slab_nz, c.slab_z0, c.slab_z1,
+                  c.slab_planned ? 1 : 0, c.rec_ready ? 1 : 0, (long long)(c.rec_ready ? rec_count(c.g) : 0));
+    s += tmp;
+    arr("layer_cuts", cuts);
+    arr("cell_z_cuts", ccuts);
+    arr("weights", c.slab_w);
+    s += "}";
+  }
   s += "}";
   if (s.size() + 1 > cap) return set_err(c, LCP_EINVAL, "stats_json: buffer too small");
   std::memcpy(buf, s.c_str(), s.size() + 1);
+  return LCP_OK;
+}
+
+int32_t lcp_slab_auto_level(const lcp_grid_t* grid, int32_t slab_count, int32_t max_depth) {
+  if (!grid || slab_count < 1 || max_depth < 0) return -1;
+  lcp::Geom g{};
+  int cmax = 1;
+  for (int d = 0; d < 3; ++d) {
+    if (grid->cells[d] < 1) return -1;
+    g.cells[d] = grid->cells[d];
+    cmax = std::max(cmax, grid->cells[d]);
+  }
+  int lf = 0;
+  while ((1 << lf) < cmax) ++lf;
+  g.lfull = lf;
+  return lcp::auto_slab_level(g, slab_count, std::min(max_depth, lf));
+}
+
+lcp_status_t lcp_slab_cuts(const int64_t* weights, int32_t n_layers, int32_t slab_count, int32_t* cuts_out) {
+  if (!weights || !cuts_out || n_layers < 1 || slab_count < 1) return LCP_EINVAL;
+  std::vector<int64_t> w(weights, weights + n_layers);
+  for (int64_t v : w)
+    if (v < 0) return LCP_EINVAL;
+  std::vector<int> cut = lcp::slab_cuts(w, slab_count);
+  for (int r = 0; r <= slab_count; ++r) cuts_out[r] = cut[r];
   return LCP_OK;
 }
 

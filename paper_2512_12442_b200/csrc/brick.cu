@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         i0 = BK * bi; j0 = BK * bj; k0 = BK * bk;
         __syncthreads();   // every thread has read the previous brick's s_skip
         if (tid == 0) {
-          uint8_t* d = o.bdone + morton3(bi, bj, bk);
+          uint8_t* d = o.bdone + (rec_index(g, BK * bi, BK * bj, BK * bk) >> 6);
           s_skip = *d;
           *d = 1;
           o.ucomp[r] = s_skip ? 0 : 1;
@@ -332,33 +332,56 @@ bool fused_brick_supported(const Ctx& c) {
          c.g.lfull >= 2;
 }
 
-// Enable the refine-time brick pass for this fit when the kernel supports the model
-// and the records (208 B per cell of the virtual cube) fit in free HBM with 4 GB
-// to spare; LCP_FUSED=0 in the environment disables it (A/B measurements).
+// Enable the refine-time brick pass for this fit when the kernel supports the model;
+// LCP_FUSED=0 in the environment disables it (A/B measurements).  The record table
+// (208 B per cell) covers the rank's slab (Geom rec_*): the whole virtual cube on one
+// rank, allocated here; under a z-slab decomposition it is allocated by records_setup
+// once the first refine has placed the slab.
 lcp_status_t fused_setup(Ctx& c) {
   c.fused = false;
+  c.rec_ready = false;
+  c.g.rec_ls = 0;
+  c.g.rec_z0 = 0;
+  c.g.rec_z1 = 1;
   static const bool env_off = [] {
     const char* v = std::getenv("LCP_FUSED");
     return v && v[0] == '0';
   }();
   if (env_off || c.opts.brick_pass < 0 || !fused_brick_supported(c)) return LCP_OK;
-  const int64_t ncodes = (int64_t)1 << (3 * c.g.lfull);
-  const int64_t nbr = (int64_t)1 << (3 * (c.g.lfull - 2));
+  c.fused = true;
+  if (c.opts.slab_count > 1) return LCP_OK;   // records_setup at the slab plan
+  return records_setup(c);
+}
+
+// Allocate (grow-only) and clear the MC record table and the per-brick done flags for
+// the record range of Geom rec_*, when they fit in free HBM with 4 GB to spare;
+// otherwise the brick pass is switched off for this fit (leaves take the per-leaf path).
+lcp_status_t records_setup(Ctx& c) {
+  c.rec_ready = false;
+  if (!c.fused) return LCP_OK;
+  const int64_t ncodes = rec_count(c.g);
+  const int64_t nbr = ncodes >> 6;
   const size_t need = sizeof(CellRec) * (size_t)ncodes;
   if (c.crec.cap < need) {
     size_t fr = 0, tot = 0;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return LCP_OK;
-    if (need + ((size_t)4 << 30) > fr) return LCP_OK;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || need + ((size_t)4 << 30) > fr + c.crec.cap) {
+      cudaGetLastError();
+      c.fused = false;
+      return LCP_OK;
+    }
+    c.crec.release();
   }
   cudaError_t e;
   if ((e = c.crec.ensure(need)) != cudaSuccess) {
     cudaGetLastError();
+    c.fused = false;
     return LCP_OK;   // not enough memory after all: the per-leaf path stays
   }
-  if ((e = c.brick_done.ensure(nbr)) != cudaSuccess) return cuda_err(c, e, "brick_done");
+  if ((e = c.brick_done.ensure(std::max<int64_t>(nbr, 1))) != cudaSuccess) return cuda_err(c, e, "brick_done");
   if ((e = c.brick_unit.ensure(BRICK_PASS_CHUNK)) != cudaSuccess) return cuda_err(c, e, "brick_unit");
-  if ((e = cudaMemsetAsync(c.brick_done.p, 0, nbr, c.stream)) != cudaSuccess) return cuda_err(c, e, "brick_done");
-  c.fused = true;
+  if ((e = cudaMemsetAsync(c.brick_done.p, 0, std::max<int64_t>(nbr, 1), c.stream)) != cudaSuccess)
+    return cuda_err(c, e, "brick_done");
+  c.rec_ready = true;
   return LCP_OK;
 }
 

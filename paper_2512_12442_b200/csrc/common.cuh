@@ -35,6 +35,10 @@ struct Geom {
   int lfull;        // 2^lfull >= max cells
   int nbuckets;
   int h_full;
+  // record table of the refine-time brick pass (SURVEY §8(e) slab-local memory): the
+  // level-rec_ls nodes with z index in [rec_z0, rec_z1) (the rank's z-slab; rec_ls = 0,
+  // [0, 1) = the whole virtual cube) -- see rec_index()
+  int rec_ls, rec_z0, rec_z1;
 };
 
 __device__ __forceinline__ double kern_from_r2(const KernParams& p, double r2) {
@@ -126,6 +130,25 @@ __host__ __device__ __forceinline__ uint64_t spread3(uint64_t v) {
 }
 __host__ __device__ __forceinline__ uint64_t morton3(uint64_t x, uint64_t y, uint64_t z) {
   return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
+}
+
+// Slab-local index of cell (ci, cj, ck)'s MC record: the slab's level-rec_ls nodes in
+// (k - z0, j, i) order, each node's cells in Morton order (a node's 8^sh cells are
+// consecutive, so a 4^3 brick's 64 records stay 64 consecutive slots).  With rec_ls = 0
+// this is the cell's Morton code in the virtual 2^lfull cube.
+__host__ __device__ __forceinline__ bool rec_in_slab(const Geom& g, int ck) {
+  const int nk = ck >> (g.lfull - g.rec_ls);
+  return nk >= g.rec_z0 && nk < g.rec_z1;
+}
+__host__ __device__ __forceinline__ int64_t rec_index(const Geom& g, int ci, int cj, int ck) {
+  const int sh = g.lfull - g.rec_ls;
+  const uint64_t node = ((uint64_t)((ck >> sh) - g.rec_z0) << (2 * g.rec_ls)) |
+                        ((uint64_t)(cj >> sh) << g.rec_ls) | (uint64_t)(ci >> sh);
+  return (int64_t)((node << (3 * sh)) | (morton3(ci, cj, ck) & ((1ull << (3 * sh)) - 1)));
+}
+// records in the table: (z1 - z0) 4^rec_ls nodes x 8^(lfull - rec_ls) cells
+__host__ __forceinline__ int64_t rec_count(const Geom& g) {
+  return ((int64_t)(g.rec_z1 - g.rec_z0) << (2 * g.rec_ls)) << (3 * (g.lfull - g.rec_ls));
 }
 
 // packed node key (i | j << 21 | k << 42)

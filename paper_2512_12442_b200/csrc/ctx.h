@@ -124,8 +124,9 @@ struct Ctx {
   // refine-time brick pass (brick.cu k_brick<true>): MC records of every cell of the
   // level-(Lfull-2) frontier bricks, indexed by the cell's Morton code
   bool fused = false;            // enabled for this fit (supported and records fit in HBM)
-  DevBuf crec;                   // CellRec per Morton code of the virtual 2^Lfull cube
-  DevBuf brick_done;             // uint8 per brick (Morton code of the level-(Lfull-2) node)
+  bool rec_ready = false;        // the record table of the current slab is allocated and cleared
+  DevBuf crec;                   // CellRec per cell of the rank's slab (rec_index, common.cuh)
+  DevBuf brick_done;             // uint8 per brick of the slab (rec_index >> 6)
   DevBuf brick_unit;             // uint8 per unit of a brick-pass launch: computed by it
   DevBuf cellmask;               // NEXT-3: uint16 per cell, bit t = leaf of isovalue t
   DevBuf union_cells, union_mask; // NEXT-3: union leaf list (Morton order) and its masks
@@ -137,6 +138,13 @@ struct Ctx {
 
   // host pinned staging for counters
   int64_t* h_counters = nullptr;
+
+  // z-slab decomposition: placed by the first refine after a fit, from the
+  // refined level-slab_L nodes per z-layer (identical on every rank), kept until the next fit
+  bool slab_planned = false;
+  int slab_L = 0, slab_nz = 0, slab_z0 = 0, slab_z1 = 0;
+  std::vector<int64_t> slab_w;   // weights per z-layer of level slab_L
+  std::vector<int> slab_cuts;    // slab_count + 1 layer cuts (rank r owns [cuts[r], cuts[r+1]))
 
   // stats
   PhaseTimes t;
@@ -182,6 +190,12 @@ cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double
 cudaError_t launch_child_bricks(Ctx& c, const uint64_t* F, int64_t nF, int gen, uint64_t* out);
 cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post);
 lcp_status_t fused_setup(Ctx& c);
+lcp_status_t records_setup(Ctx& c);
+
+// z-slab plan (octree.cu; host code, also behind lcp_slab_auto_level / lcp_slab_cuts)
+int slab_layers_at(const Geom& g, int L);
+int auto_slab_level(const Geom& g, int count, int max_depth);
+std::vector<int> slab_cuts(const std::vector<int64_t>& w, int count);
 
 lcp_status_t set_err(Ctx& c, lcp_status_t st, const std::string& msg);
 lcp_status_t cuda_err(Ctx& c, cudaError_t e, const char* where);

@@ -921,7 +921,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   o.precision = LCP_FP64;
   o.slab_rank = 0;
   o.slab_count = 1;
-  o.slab_level = 3;
+  o.slab_level = 0;
   o.keep_records = 0;
   o.extreme_iters = 0;
   if (opts) o = *opts;
@@ -939,8 +939,8 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   // candidate lattice of a node: (2^min(h, h_full) + 1)^3 vertices, indexed in 32 bits
   if (std::min(o.h_full, lfull) > 10)
     return set_err(c, LCP_EINVAL, "fit: h_full > 10 (lattice of > 2^30 vertices per node)");
-  if (o.slab_count > 1 && (o.slab_level < 1 || o.slab_level > lfull))
-    return set_err(c, LCP_EINVAL, "fit: slab_level must be in [1, Lfull] when slab_count > 1");
+  if (o.slab_count > 1 && o.slab_level > lfull)
+    return set_err(c, LCP_EINVAL, "fit: slab_level must be <= Lfull (or <= 0: automatic)");
 
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -949,6 +949,7 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
 
   c.fitted = false;
   c.vcache_valid = false;
+  c.slab_planned = false;
   c.kern = *kern;
   c.grid = *grid;
   c.opts = o;

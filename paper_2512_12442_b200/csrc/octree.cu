@@ -97,7 +97,7 @@ __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ fr
                               int8_t* __restrict__ ncase, int8_t* __restrict__ nref, double* __restrict__ np1,
                               double* __restrict__ np2, double* __restrict__ nU, uint32_t* __restrict__ vmask,
                               int64_t* __restrict__ req, unsigned long long* __restrict__ nreq,
-                              const uint32_t* __restrict__ occ) {
+                              const uint32_t* __restrict__ occ, int lattice_all) {
   int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   const int sub = threadIdx.x % G;
   const bool live = n < nF;
@@ -134,7 +134,7 @@ __global__ void k_node_prelim(Geom g, int level, const uint64_t* __restrict__ fr
       nU[n] = 1.0;
     }
   }
-  if (!live || cs == 1) return;
+  if (!live || (cs == 1 && !lattice_all)) return;   // lattice_all: the slab weights read it
   Lattice L = node_lattice(g, h, i, j, k);
   int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
   for (int64_t q = sub; q < nc; q += G) {
@@ -291,10 +291,43 @@ __global__ void k_fill_level(Geom g, int level, int max_depth, const uint64_t* _
   }
 }
 
+// Slab weights (identical on every rank): per z-layer of the slab level, the expected
+// leaf work of its refined nodes -- 1 + 1024 x (fraction of the node's lattice vertices
+// whose marginal is uncertain, |z| < zs, i.e. both tails > alpha / 8) x (clipped cells /
+// full node cells).  Thin-shell fields (NEXT-4) put their leaves near few layers.
+__global__ void k_layer_weight(Geom g, int level, const uint64_t* __restrict__ front, int64_t nF,
+                               const int8_t* __restrict__ nref, const double2* __restrict__ vcache, double theta,
+                               double zs, int nz, unsigned long long* __restrict__ hist) {
+  int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= nF || !nref[n]) return;
+  int i, j, k;
+  node_unkey(front[n], i, j, k);
+  if (k >= nz) return;
+  const int h = g.lfull - level;
+  Lattice L = node_lattice(g, h, i, j, k);
+  const int64_t nc = (int64_t)L.cnt[0] * L.cnt[1] * L.cnt[2];
+  int64_t unc = 0;
+  for (int64_t q = 0; q < nc; ++q) {
+    const double2 ms = vcache[lattice_vertex(g, L, q)];
+    unc += fabs((ms.x - theta) * ms.y) < zs;
+  }
+  const uint64_t cells = (uint64_t)(L.vmax[0] - L.base[0]) * (L.vmax[1] - L.base[1]) * (L.vmax[2] - L.base[2]);
+  const uint64_t full = 1ull << (3 * h);
+  const uint64_t w = 1 + (uint64_t)((1024.0 * (double)unc / (double)nc) * ((double)cells / (double)full));
+  atomicAdd(&hist[k], (unsigned long long)w);
+}
+
+// Slab filter of a rank: the children of refined level-slab_level nodes
+// are kept iff the node's z index is in [z0, z1); leaf cells emitted at a level <=
+// slab_level are kept iff their z is in [cz0, cz1).  slab_level < 0: whole domain.
+struct Slab {
+  int level, z0, z1;
+  int64_t cz0, cz1;
+};
+
 // children / leaf counts of refined nodes
 __global__ void k_node_counts(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
-                              const int8_t* __restrict__ nref, int slab_level, int z0, int z1,
-                              int64_t* __restrict__ cnt) {
+                              const int8_t* __restrict__ nref, Slab sl, int64_t* __restrict__ cnt) {
   int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= nF) return;
   if (!nref[n]) {
@@ -305,30 +338,36 @@ __global__ void k_node_counts(Geom g, int level, int max_depth, const uint64_t* 
   node_unkey(front[n], i, j, k);
   int h = g.lfull - level;
   if (level < max_depth) {
+    if (level == sl.level && (k < sl.z0 || k >= sl.z1)) {
+      cnt[n] = 0;
+      return;
+    }
     int64_t cs = (int64_t)1 << (h - 1);
     int c = 0;
     for (int ch = 0; ch < 8; ++ch) {
       int64_t ci = 2 * (int64_t)i + (ch & 1), cj = 2 * (int64_t)j + ((ch >> 1) & 1), ck = 2 * (int64_t)k + (ch >> 2);
-      bool in = ci * cs < g.cells[0] && cj * cs < g.cells[1] && ck * cs < g.cells[2];
-      if (level + 1 == slab_level) in = in && ck >= z0 && ck < z1;
-      c += in;
+      c += ci * cs < g.cells[0] && cj * cs < g.cells[1] && ck * cs < g.cells[2];
     }
     cnt[n] = c;
   } else {
     int64_t side = (int64_t)1 << h;
-    int64_t e[3];
+    int64_t e[3], b[3];
     int a[3] = {i, j, k};
     for (int d = 0; d < 3; ++d) {
-      int64_t b = (int64_t)a[d] * side;
-      e[d] = min(b + side, (int64_t)g.cells[d]) - b;
+      b[d] = (int64_t)a[d] * side;
+      e[d] = min(b[d] + side, (int64_t)g.cells[d]);
     }
-    cnt[n] = e[0] * e[1] * e[2];
+    if (level <= sl.level) {
+      b[2] = max(b[2], sl.cz0);
+      e[2] = min(e[2], sl.cz1);
+    }
+    cnt[n] = e[2] > b[2] ? (e[0] - b[0]) * (e[1] - b[1]) * (e[2] - b[2]) : 0;
   }
 }
 
 __global__ void k_emit(Geom g, int level, int max_depth, const uint64_t* __restrict__ front, int64_t nF,
-                       const int8_t* __restrict__ nref, const int64_t* __restrict__ offs, int slab_level, int z0,
-                       int z1, uint64_t* __restrict__ next, int64_t* __restrict__ leaves) {
+                       const int8_t* __restrict__ nref, const int64_t* __restrict__ offs, Slab sl,
+                       uint64_t* __restrict__ next, int64_t* __restrict__ leaves) {
   int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= nF || !nref[n]) return;
   int i, j, k;
@@ -336,11 +375,11 @@ __global__ void k_emit(Geom g, int level, int max_depth, const uint64_t* __restr
   int h = g.lfull - level;
   int64_t o = offs[n];
   if (level < max_depth) {
+    if (level == sl.level && (k < sl.z0 || k >= sl.z1)) return;
     int64_t cs = (int64_t)1 << (h - 1);
     for (int ch = 0; ch < 8; ++ch) {
       int64_t ci = 2 * (int64_t)i + (ch & 1), cj = 2 * (int64_t)j + ((ch >> 1) & 1), ck = 2 * (int64_t)k + (ch >> 2);
       bool in = ci * cs < g.cells[0] && cj * cs < g.cells[1] && ck * cs < g.cells[2];
-      if (level + 1 == slab_level) in = in && ck >= z0 && ck < z1;
       if (in) next[o++] = node_key(ci, cj, ck);
     }
   } else {
@@ -348,10 +387,71 @@ __global__ void k_emit(Geom g, int level, int max_depth, const uint64_t* __restr
     int64_t b0 = (int64_t)i * side, b1 = (int64_t)j * side, b2 = (int64_t)k * side;
     int64_t e0 = min(b0 + side, (int64_t)g.cells[0]), e1 = min(b1 + side, (int64_t)g.cells[1]),
             e2 = min(b2 + side, (int64_t)g.cells[2]);
+    if (level <= sl.level) {
+      b2 = max(b2, sl.cz0);
+      e2 = min(e2, sl.cz1);
+    }
     for (int64_t z = b2; z < e2; ++z)
       for (int64_t y = b1; y < e1; ++y)
         for (int64_t x = b0; x < e0; ++x) leaves[o++] = x + (int64_t)g.cells[0] * (y + (int64_t)g.cells[1] * z);
   }
+}
+
+// z-layers of level L over the grid
+int slab_layers_at(const Geom& g, int L) {
+  const int64_t side = (int64_t)1 << (g.lfull - L);
+  return (int)((g.cells[2] + side - 1) / side);
+}
+
+// Automatic slab level: the shallowest level with >= 2 slab_count z-layers (weighted cuts
+// need a few layers per rank), at most Lfull - 3 (the brick pass starts below the slab
+// level) and at most max_depth.
+int auto_slab_level(const Geom& g, int count, int max_depth) {
+  const int cap = std::max(1, std::min(max_depth, g.lfull - 3));
+  for (int L = 1; L < cap; ++L)
+    if (slab_layers_at(g, L) >= 2 * count) return L;
+  return cap;
+}
+
+// Contiguous z-layer ranges of `count` ranks minimising the largest rank weight (then the
+// sum of squared rank weights; ties to the earlier cut), every rank >= 1 layer when there
+// are at least `count` layers; equal layer counts when every weight is 0.  Exact dynamic
+// programme over (ranks, layers), O(count nz^2) with nz <= 2^10; integer arithmetic only,
+// so every rank computes the same cuts.
+std::vector<int> slab_cuts(const std::vector<int64_t>& w, int count) {
+  const int nz = (int)w.size();
+  std::vector<int> cut(count + 1, 0);
+  cut[count] = nz;
+  std::vector<int64_t> P(nz + 1, 0);
+  for (int z = 0; z < nz; ++z) P[z + 1] = P[z] + w[z];
+  if (P[nz] == 0) {
+    for (int r = 1; r < count; ++r) cut[r] = (int)((int64_t)r * nz / count);
+    return cut;
+  }
+  const bool one_each = nz >= count;
+  const int64_t INF = INT64_MAX;
+  typedef std::pair<int64_t, double> Cost;   // (max rank weight, sum of squares)
+  std::vector<std::vector<Cost>> f(count + 1, std::vector<Cost>(nz + 1, Cost(INF, 0.0)));
+  std::vector<std::vector<int>> arg(count + 1, std::vector<int>(nz + 1, 0));
+  f[0][0] = Cost(0, 0.0);
+  for (int r = 1; r <= count; ++r)
+    for (int z = 0; z <= nz; ++z)
+      for (int zp = 0; zp <= z; ++zp) {
+        if (one_each && zp == z) continue;
+        if (f[r - 1][zp].first == INF) continue;
+        const int64_t load = P[z] - P[zp];
+        const Cost cst(std::max(f[r - 1][zp].first, load), f[r - 1][zp].second + (double)load * (double)load);
+        if (cst < f[r][z]) {
+          f[r][z] = cst;
+          arg[r][z] = zp;
+        }
+      }
+  for (int r = count, z = nz; r > 0; --r) {
+    cut[r] = z;
+    z = arg[r][z];
+  }
+  cut[0] = 0;
+  return cut;
 }
 
 lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
@@ -391,14 +491,29 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
   c.level_nodes.clear();
   c.level_refined.clear();
   for (int q = 0; q < 4; ++q) c.level_case[q].clear();
-  // z-slab of this rank at slab_level
-  int slab_level = -1, z0 = 0, z1 = 1 << 30;
+  // z-slab of this rank: levels 0..slab_level are evaluated over the whole
+  // domain; the cut is placed at slab_level by the first refine after the fit
+  Slab sl{-1, 0, 1 << 30, 0, INT64_MAX};
+  bool plan_now = false;
   if (c.opts.slab_count > 1) {
-    slab_level = c.opts.slab_level;
-    int64_t side = (int64_t)1 << (g.lfull - slab_level);
-    int nz = (int)((g.cells[2] + side - 1) / side);
-    z0 = (int)((int64_t)c.opts.slab_rank * nz / c.opts.slab_count);
-    z1 = (int)((int64_t)(c.opts.slab_rank + 1) * nz / c.opts.slab_count);
+    if (c.slab_planned) {
+      sl.level = c.slab_L;
+    } else {
+      const int want = c.opts.slab_level > 0 ? std::min(c.opts.slab_level, g.lfull)
+                                             : auto_slab_level(g, c.opts.slab_count, g.lfull);
+      sl.level = std::min(want, max_depth);
+      plan_now = true;
+      c.slab_L = sl.level;
+      c.slab_nz = slab_layers_at(g, sl.level);
+      if (c.fused && sl.level > g.lfull - 3) c.fused = false;   // bricks must lie below the slab level
+    }
+    if (!plan_now) {
+      sl.z0 = c.slab_z0;
+      sl.z1 = c.slab_z1;
+      const int64_t side = (int64_t)1 << (g.lfull - c.slab_L);
+      sl.cz0 = std::min<int64_t>((int64_t)sl.z0 * side, g.cells[2]);
+      sl.cz1 = std::min<int64_t>((int64_t)sl.z1 * side, g.cells[2]);
+    }
   }
   unsigned long long* dcnt = c.counters.as<unsigned long long>();
   if (c.level_field)
@@ -458,7 +573,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       return !(v && v[0] == '0');
     }();
     const int gen = h == 4 ? 2 : (h == 3 ? 1 : 0);
-    if (c.fused && gen > 0 && !early_bricks && early_env && level >= 1 && level > slab_level &&
+    if (c.fused && c.rec_ready && gen > 0 && !early_bricks && early_env && level >= 1 && level > sl.level &&
         !c.level_nodes.empty() &&
         c.level_refined.back() * 20 >= c.level_nodes.back() * (gen == 2 ? 19 : 18)) {
       const int64_t nk = nF << (3 * gen);
@@ -467,7 +582,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       CK(brick_pass(c.child_bricks.as<uint64_t>(), nk));
       early_bricks = true;   // covers every brick of the later frontiers
     }
-    if (c.fused && h == 2 && !early_bricks) CK(brick_pass(F, nF));
+    if (c.fused && c.rec_ready && h == 2 && !early_bricks) CK(brick_pass(F, nF));
     const int G = h == 0 ? 1 : (h == 1 ? 4 : (h == 2 ? 8 : 32));
     unsigned gw = (unsigned)((nF * G + 255) / 256);
 #define PRELIM(GG)                                                                                              \
@@ -475,7 +590,8 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
                                                c.phi.as<double>(), m, alpha, c.ncase.as<int8_t>(),                \
                                                c.nref.as<int8_t>(), c.np1.as<double>(), c.np2.as<double>(),       \
                                                c.nU.as<double>(), c.vstate.as<uint32_t>(), c.req.as<int64_t>(), dcnt, \
-                                               h < c.occ_heights ? c.occ[h].as<uint32_t>() : nullptr)
+                                               h < c.occ_heights ? c.occ[h].as<uint32_t>() : nullptr, \
+                                               (plan_now && level == sl.level) ? 1 : 0)
     if (G == 1) PRELIM(1);
     else if (G == 4) PRELIM(4);
     else if (G == 8) PRELIM(8);
@@ -540,8 +656,44 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
       }
       ++c.n_launch;
     }
-    k_node_counts<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), slab_level, z0, z1,
-                                            c.cnt.as<int64_t>());
+    if (plan_now && level == sl.level) {
+      // slab weights: refined nodes of this level per z-layer -> contiguous cuts (host)
+      const int nz = c.slab_nz;
+      CK(c.scan_tmp.ensure(sizeof(unsigned long long) * nz));
+      unsigned long long* hist = c.scan_tmp.as<unsigned long long>();
+      CK(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * nz, c.stream));
+      // zs: 0.5 erfc(zs) = alpha / 8 (bisection; the single-cell survival band of Eq. 4 with d = 8)
+      double za = 0.0, zb = 40.0;
+      for (int it = 0; it < 200; ++it) {
+        const double zm = 0.5 * (za + zb);
+        (0.5 * std::erfc(zm) > alpha / 8.0 ? za : zb) = zm;
+      }
+      k_layer_weight<<<gt, 256, 0, c.stream>>>(g, level, F, nF, c.nref.as<int8_t>(), c.vcache.as<double2>(), theta,
+                                               za, nz, hist);
+      ++c.n_launch;
+      c.slab_w.assign(nz, 0);
+      CK(cudaMemcpyAsync(c.slab_w.data(), hist, sizeof(int64_t) * nz, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      c.slab_cuts = slab_cuts(c.slab_w, c.opts.slab_count);
+      c.slab_z0 = c.slab_cuts[c.opts.slab_rank];
+      c.slab_z1 = c.slab_cuts[c.opts.slab_rank + 1];
+      sl.z0 = c.slab_z0;
+      sl.z1 = c.slab_z1;
+      const int64_t side = (int64_t)1 << (g.lfull - sl.level);
+      sl.cz0 = std::min<int64_t>((int64_t)sl.z0 * side, g.cells[2]);
+      sl.cz1 = std::min<int64_t>((int64_t)sl.z1 * side, g.cells[2]);
+      // a plan capped by max_depth is redone by the next refine
+      c.slab_planned = c.opts.slab_level > 0 ? sl.level == std::min(c.opts.slab_level, g.lfull)
+                                             : sl.level == auto_slab_level(g, c.opts.slab_count, g.lfull);
+      if (c.fused) {   // the slab-local record table
+        c.g.rec_ls = sl.level;
+        c.g.rec_z0 = sl.z0;
+        c.g.rec_z1 = std::max(sl.z1, sl.z0 + 1);
+        lcp_status_t rs = records_setup(c);
+        if (rs != LCP_OK) return rs;
+      }
+    }
+    k_node_counts<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), sl, c.cnt.as<int64_t>());
     ++c.n_launch;
     CK(exclusive_scan_i64(c, c.cnt.as<int64_t>(), c.offs.as<int64_t>(), nF, (int64_t*)(dcnt + 1)));
     CK(cudaMemcpyAsync(c.h_counters, dcnt, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost, c.stream));
@@ -553,15 +705,15 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     for (int q = 0; q < 4; ++q) c.level_case[q].push_back(c.h_counters[8 + q]);
     if (level < max_depth) {
       CK(c.front[cur ^ 1].ensure(sizeof(uint64_t) * std::max<int64_t>(total, 1)));
-      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
-                                       slab_level, z0, z1, c.front[cur ^ 1].as<uint64_t>(), nullptr);
+      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(), sl,
+                                       c.front[cur ^ 1].as<uint64_t>(), nullptr);
       ++c.n_launch;
       cur ^= 1;
       nF = total;
     } else {
       CK(c.leaves.ensure(sizeof(int64_t) * std::max<int64_t>(total, 1)));
-      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(),
-                                       slab_level, z0, z1, nullptr, c.leaves.as<int64_t>());
+      k_emit<<<gt, 256, 0, c.stream>>>(g, level, max_depth, F, nF, c.nref.as<int8_t>(), c.offs.as<int64_t>(), sl,
+                                       nullptr, c.leaves.as<int64_t>());
       ++c.n_launch;
       c.n_leaves = total;
       nF = 0;

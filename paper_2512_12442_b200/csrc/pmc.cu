@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(64) k_chol8_rec(Geom g, const uint64_t* __rest
   __syncthreads();
   int bi, bj, bk;
   node_unkey(bricks[u], bi, bj, bk);
-  float4* dst = reinterpret_cast<float4*>(recs + (morton3(bi, bj, bk) << 6));
+  float4* dst = reinterpret_cast<float4*>(recs + rec_index(g, 4 * bi, 4 * bj, 4 * bk));
   const float4* s4 = reinterpret_cast<const float4*>(sbuf);
   for (int e = q; e < 64 * (int)(sizeof(CellRec) / 16); e += 64) dst[e] = s4[e];
 }
@@ -131,7 +131,7 @@ __global__ void k_cells_covered(Geom g, const int64_t* __restrict__ cells, int64
     } else {
       int i, j, k;
       cell_ijk(g, cell, i, j, k);
-      miss = !bdone[morton3(i >> 2, j >> 2, k >> 2)];
+      miss = !rec_in_slab(g, k) || !bdone[rec_index(g, i, j, k) >> 6];
     }
   }
   if (__any_sync(0xffffffffu, miss) && (threadIdx.x & 31) == 0) atomicOr(cov, 1ull);
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     if (rec_by_morton) {
       int ci, cj, ck;
       cell_ijk(g, cell, ci, cj, ck);
-      ri = (int64_t)morton3(ci, cj, ck);
+      ri = rec_index(g, ci, cj, ck);
     }
     const double* rec = post + rec_stride * ri;
     float mm[8];
@@ -609,7 +609,7 @@ lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const doubl
   const int Tp = T <= 4 ? T : (T <= 6 ? 6 : (T <= 8 ? 8 : (T <= 12 ? 12 : 16)));
   // records of the refine-time brick pass cover the list? (e.g. every leaf of a refine)
   bool use_rec = false;
-  if (c.fused) {
+  if (c.fused && c.rec_ready) {
     CK(c.counters.ensure(sizeof(unsigned long long) * 16));
     unsigned long long* dcnt = c.counters.as<unsigned long long>();
     CK(cudaMemsetAsync(dcnt + 12, 0, sizeof(unsigned long long), c.stream));

@@ -1,19 +1,23 @@
 """z-slab decomposition of the octree across GPUs.
 
 Every rank fits the same bucket-local GP (observations replicated: the halo),
-refines octree levels 0 .. slab_level-1 redundantly, then keeps only the
-level-`slab_level` nodes whose z index lies in its slab (the filter is applied
-inside liblcp, k_node_counts / k_emit) and finishes refine + PMC on its own
-subtrees.  Results are bit-identical to one GPU: Philox counters are keyed by
-the global cell id and every node decision is local to the node.  The only
-collective is the final gather of the per-slab dense-field slices to rank 0.
+refines octree levels 0 .. slab_level redundantly, and the first refine after
+the fit cuts the z-layers of level `slab_level` into contiguous per-rank ranges
+by prefix sums of the refined nodes per layer -- computed identically on every
+rank, so no communication is needed (liblcp, octree.cu).  Each rank then
+finishes refine + PMC on its own subtrees.  Results are bit-identical to one GPU:
+Philox counters are keyed by the global cell id and every node decision is local
+to the node.  The only collective is the final gather of the per-slab slices of
+the dense field(s) to rank 0 (point-to-point: only rank 0 receives).
 
-This module is plumbing only (partition arithmetic and torch.distributed
-calls); all LCP arithmetic runs in liblcp.so.
+This module is plumbing only (range arithmetic and torch.distributed calls); the
+slab plan itself is liblcp's (lcp_slab_auto_level / lcp_slab_cuts, host-only).
 """
 from __future__ import annotations
 
-from typing import Tuple
+from typing import List, Sequence, Tuple
+
+from .lcp import slab_auto_level, slab_cuts
 
 
 def lfull_of(cells) -> int:
@@ -24,56 +28,77 @@ def lfull_of(cells) -> int:
     return lf
 
 
-def slab_layers(cells, slab_level: int, rank: int, world: int) -> Tuple[int, int]:
-    """z range [z0, z1) of level-`slab_level` nodes owned by `rank` (same rule
-    as liblcp's refine: equal split of the node layers that hold cells)."""
-    lf = lfull_of(cells)
-    side = 1 << (lf - slab_level)
-    nz = (cells[2] + side - 1) // side
-    return rank * nz // world, (rank + 1) * nz // world
+def layers_at(cells, level: int) -> int:
+    side = 1 << (lfull_of(cells) - level)
+    return (cells[2] + side - 1) // side
 
 
-def slab_cells(cells, slab_level: int, rank: int, world: int) -> Tuple[int, int]:
-    """[c0, c1) range of linear cell ids (x fastest) covered by the rank's slab:
-    its cells are exactly the z-planes [z0 * side, min(z1 * side, nz))."""
-    lf = lfull_of(cells)
-    side = 1 << (lf - slab_level)
-    z0, z1 = slab_layers(cells, slab_level, rank, world)
+def cell_z_cuts(cells, level: int, layer_cuts: Sequence[int]) -> List[int]:
+    """Layer cuts of `level` -> cut z-planes of cells (clipped to the grid)."""
+    side = 1 << (lfull_of(cells) - level)
+    return [min(int(z) * side, cells[2]) for z in layer_cuts]
+
+
+def cell_ranges(cells, z_cuts: Sequence[int]) -> List[Tuple[int, int]]:
+    """Per-rank [c0, c1) ranges of linear cell ids (x fastest): rank r's slab is the
+    z-planes [z_cuts[r], z_cuts[r + 1])."""
     plane = cells[0] * cells[1]
-    return min(z0 * side, cells[2]) * plane, min(z1 * side, cells[2]) * plane
+    return [(int(z_cuts[r]) * plane, int(z_cuts[r + 1]) * plane) for r in range(len(z_cuts) - 1)]
 
 
-def min_slab_level(world: int) -> int:
-    lvl = 0
-    while (1 << lvl) < world:
-        lvl += 1
-    return max(lvl, 1)
+def equal_z_cuts(cells, world: int, max_depth: int) -> List[int]:
+    """Unweighted plan (the dense baseline, which has no octree): equal layer counts at
+    the automatic slab level."""
+    lv = slab_auto_level(cells, world, max_depth)
+    return cell_z_cuts(cells, lv, slab_cuts([0] * layers_at(cells, lv), world))
 
 
-def gather_field(field, cells, slab_level: int, group=None):
-    """Assemble the dense LCP field on rank 0 from the ranks' slab slices.
+def plan_z_cuts(stats: dict) -> List[int]:
+    """The z-plane cuts of the slab plan a context reports (lcp_stats_json "slab")."""
+    return list(stats["slab"]["cell_z_cuts"])
 
-    `field` is this rank's full-size flat field (zeros outside its slab).  Each
-    rank contributes only its contiguous slab slice (padded to the largest
-    slab); rank 0 receives them with one all_gather_into_tensor and writes them
-    in place.  Returns the assembled field on rank 0 (other ranks: their input).
-    """
+
+def gather_fields(fields, cells, z_cuts: Sequence[int], group=None):
+    """Assemble the dense LCP field(s) on rank 0 from the ranks' slab slices.
+
+    `fields` is this rank's (T, nx*ny*nz) (or flat) field tensor, zero outside its
+    slab.  Every rank r > 0 sends its T contiguous slices [c0_r, c1_r) to rank 0, which
+    receives them in place (one batch of point-to-point transfers; the other ranks
+    receive nothing).  Returns `fields` (complete on rank 0)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if world == 1:
-        return field
-    ranges = [slab_cells(cells, slab_level, r, world) for r in range(world)]
-    width = max(c1 - c0 for c0, c1 in ranges)
-    c0, c1 = ranges[rank]
-    # gloo moves host tensors only: stage CUDA slices through the host
-    dev = "cpu" if dist.get_backend(group) == "gloo" else field.device
-    send = torch.zeros(width, dtype=field.dtype, device=dev)
-    send[: c1 - c0] = field[c0:c1]
-    recv = torch.empty(world * width, dtype=field.dtype, device=dev)
-    dist.all_gather_into_tensor(recv, send, group=group)
+        return fields
+    rows = fields.view(1, -1) if fields.dim() == 1 else fields
+    ranges = cell_ranges(cells, z_cuts)
+    gloo = dist.get_backend(group) == "gloo"      # gloo moves host tensors only
+    ops, staged = [], []
     if rank == 0:
-        for r, (a, b) in enumerate(ranges):
-            field[a:b] = recv[r * width: r * width + (b - a)]
-    return field
+        for r in range(1, world):
+            a, b = ranges[r]
+            if b <= a:
+                continue
+            for t in range(rows.shape[0]):
+                buf = torch.empty(b - a, dtype=rows.dtype) if gloo else rows[t, a:b]
+                ops.append(dist.P2POp(dist.irecv, buf, r, group))
+                staged.append((t, a, b, buf))
+    else:
+        a, b = ranges[rank]
+        if b > a:
+            for t in range(rows.shape[0]):
+                buf = rows[t, a:b].cpu() if gloo else rows[t, a:b]
+                ops.append(dist.P2POp(dist.isend, buf, 0, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if rank == 0 and gloo:
+        for t, a, b, buf in staged:
+            rows[t, a:b] = buf.to(rows.device)
+    return fields
+
+
+def gather_field(field, cells, z_cuts: Sequence[int], group=None):
+    """One field (flat): see gather_fields."""
+    return gather_fields(field, cells, z_cuts, group)

@@ -28,7 +28,8 @@ EXPORTS = ["lcp_create", "lcp_destroy", "lcp_last_error", "lcp_fit_local", "lcp_
            "lcp_pmc_cells", "lcp_scatter_field", "lcp_run_field", "lcp_node_records",
            "lcp_cell_posterior", "lcp_point_marginals", "lcp_bucket_sets", "lcp_get_info",
            "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field", "lcp_fit_sgpr",
-           "lcp_pmc_cells_multi", "lcp_run_field_multi", "lcp_union_cells"]
+           "lcp_pmc_cells_multi", "lcp_run_field_multi", "lcp_union_cells", "lcp_slab_auto_level",
+           "lcp_slab_cuts"]
 
 
 class LcpError(RuntimeError):
@@ -99,6 +100,8 @@ def load_library() -> C.CDLL:
     L.lcp_pmc_cells_multi.argtypes = [P, P, i64, P, i32, P, i64, u64, u32, P]
     L.lcp_run_field_multi.argtypes = [P, P, i32, dbl, i32, i64, u64, u32, P, i32, P, C.POINTER(i64)]
     L.lcp_union_cells.argtypes = [P, C.POINTER(i64), C.POINTER(P), C.POINTER(P)]
+    L.lcp_slab_auto_level.argtypes = [C.POINTER(GridT), i32, i32]
+    L.lcp_slab_cuts.argtypes = [P, i32, i32, P]
     for name in EXPORTS:
         if name not in ("lcp_destroy", "lcp_last_error"):
             getattr(L, name).restype = C.c_int
@@ -153,7 +156,7 @@ class Context:
     # -- a1-a4
     def fit_local(self, xyz, y, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,
                   h_full: int = 2, precision: int = FP64, slab_rank: int = 0, slab_count: int = 1,
-                  slab_level: int = 3, keep_records=False, extreme_iters: int = 0, brick_pass: int = 0,
+                  slab_level: int = 0, keep_records=False, extreme_iters: int = 0, brick_pass: int = 0,
                   local_mode: int = 0, beta: float = 6.0):
         """xyz (m,3) / y (m,) float64, either torch CUDA tensors or numpy host arrays.
         kernel = (kind, variance, lengthscale[3], nugget, prior_mean); grid = (lo, hi, cells).
@@ -371,6 +374,25 @@ class Context:
 
     def synchronize(self):
         self._check(self._L.lcp_synchronize(self._h), "lcp_synchronize")
+
+
+def slab_auto_level(cells, slab_count: int, max_depth: int) -> int:
+    """lcp_slab_auto_level (host-only): the slab level refine picks for slab_count ranks."""
+    gt = GridT((C.c_double * 3)(0, 0, 0), (C.c_double * 3)(1, 1, 1), (C.c_int32 * 3)(*cells), 0)
+    lv = load_library().lcp_slab_auto_level(C.byref(gt), int(slab_count), int(max_depth))
+    if lv < 0:
+        raise LcpError(LCP_EINVAL, "lcp_slab_auto_level: bad arguments")
+    return lv
+
+
+def slab_cuts(weights, slab_count: int) -> np.ndarray:
+    """lcp_slab_cuts (host-only): layer cuts (slab_count + 1) balancing the weights."""
+    w = np.ascontiguousarray(weights, np.int64)
+    out = np.zeros(slab_count + 1, np.int32)
+    st = load_library().lcp_slab_cuts(C.c_void_p(w.ctypes.data), len(w), int(slab_count), C.c_void_p(out.ctypes.data))
+    if st != LCP_OK:
+        raise LcpError(st, "lcp_slab_cuts: bad arguments")
+    return out
 
 
 def config_args(cfg, k=None, bucket_log2=None):

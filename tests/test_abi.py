@@ -16,7 +16,7 @@ def test_build_and_exports():
     from paper_2512_12442_b200 import EXPORTS, load_library
     L = load_library()
     header = open(os.path.join(ROOT, "include", "lcp.h")).read()
-    declared = set(re.findall(r"^\s*(?:lcp_status_t|void|const char\*)\s+(lcp_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:lcp_status_t|void|const char\*|int32_t)\s+(lcp_\w+)\s*\(", header, re.M))
     assert declared == set(EXPORTS), declared ^ set(EXPORTS)
     for name in declared:
         assert hasattr(L, name), name

@@ -1,0 +1,115 @@
+"""The N > 1 path of SURVEY §8(e) on the GPU: z-slab contexts with the automatic
+slab level and weighted cuts, slab-local MC record tables, and the gather to
+rank 0.  The rank-0 field equals the single-GPU field bit for bit (Philox keyed
+by the global cell id; node decisions are local to the node)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from workloads import generate
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 8), ("c4", 2), ("c4", 8)])
+def test_torchrun_gather_equals_single_gpu(name, world, tmp_path):
+    out = tmp_path / "res.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "dist_check.py"),
+           "--workload", name, "--out", str(out)]
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    p = subprocess.run(cmd, cwd=ROOT, env=env, timeout=1200, capture_output=True, text=True)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    res = json.load(open(out))
+    print(json.dumps({k: res[k] for k in ("workload", "world", "slab_level", "layers", "layer_cuts",
+                                          "leaves_per_rank", "record_cells_per_rank")}))
+    assert res["bitexact"], res["max_abs_diff"]
+    assert res["leaves_sum"] == res["leaves_n1"]
+    # no empty rank, the same plan on every rank
+    assert all(sum(lv) > 0 for lv in res["leaves_per_rank"]), res["leaves_per_rank"]
+    assert all(c == res["layer_cuts"][0] for c in res["layer_cuts"])
+    assert len(res["layer_cuts"][0]) == world + 1
+    # slab-local record tables, used by every rank's leaf pass
+    if res["records_used_n1"]:
+        assert all(res["records_used_per_rank"]), res["records_used_per_rank"]
+        assert max(res["record_cells_per_rank"]) < (1 << (3 * 8)) if name == "c4" else True
+
+
+@pytest.mark.parametrize("name,G", [("p1", 4), ("c3", 3), ("t2", 2)])
+def test_auto_slabs_union_equals_full(name, G, dev):
+    # ranks run one after another on one GPU: automatic level, weighted cuts
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate(name)
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    th = w.thetas[0]
+    full = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    ref, n_ref = full.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    ref = ref.clone()
+    acc = torch.zeros_like(ref)
+    counts, cuts = [], []
+    for r in range(G):
+        ctx = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=r, slab_count=G)
+        f, n = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+        st = ctx.stats()
+        acc += f
+        counts.append(n)
+        cuts.append(st["slab"]["layer_cuts"])
+        # a second refine of the same fit keeps the plan (records stay valid)
+        f2, n2 = ctx.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+        assert n2 == n and torch.equal(f2, f)
+    assert torch.equal(acc, ref)
+    assert sum(counts) == n_ref
+    assert all(c == cuts[0] for c in cuts)
+    if name != "t2":
+        assert min(counts) > 0, counts
+    print(name, G, "leaves per rank", counts, "max/mean", max(counts) / (sum(counts) / G))
+
+
+def test_slab_refine_shallower_than_plan(dev):
+    # a refine whose max_depth stops above the planned slab level still partitions the
+    # cells (leaf cells filtered by z), and a later full-depth refine keeps the plan
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate("c2")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    th = w.thetas[0]
+    full = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    G = 3
+    for depth in (cfg.max_depth, 1, cfg.max_depth):
+        ref = np.sort(full.octree_refine(th, cfg.alpha, depth).cpu().numpy())
+        parts = []
+        for r in range(G):
+            ctx = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=r, slab_count=G)
+            ctx.octree_refine(th, cfg.alpha, cfg.max_depth)          # places the plan
+            parts.append(ctx.octree_refine(th, cfg.alpha, depth).cpu().numpy())
+        allp = np.concatenate(parts)
+        assert len(allp) == len(np.unique(allp))
+        assert np.array_equal(np.sort(allp), ref), depth
