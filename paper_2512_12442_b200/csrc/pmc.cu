@@ -160,9 +160,23 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t
   r0 = c0; r1 = c1; r2 = c2; r3 = c3;
 }
 
+// 1.0f | (r mod 2^23) as one LOP3 (r & 0x7fffff) | one, `one` = 0x3f800000 held in a
+// register (with two immediates ptxas would emit two LOP3)
+#ifndef PMC_LOP_MERGE
+#define PMC_LOP_MERGE 1
+#endif
+__device__ __forceinline__ uint32_t mant1(uint32_t r, uint32_t one) {
+#if PMC_LOP_MERGE
+  uint32_t d;
+  asm("lop3.b32 %0, %1, 0x7fffff, %2, 0xEA;" : "=r"(d) : "r"(r), "r"(one));
+  return d;
+#else
+  return 0x3f800000u | (r & 0x7fffffu);
+#endif
+}
 // u = (r mod 2^23 + 1/2) 2^-23, exact: one LOP3 + one FADD
-__device__ __forceinline__ float u23(uint32_t r) {
-  return __uint_as_float(0x3f800000u | (r & 0x7fffffu)) - (1.0f - 0x1p-24f);
+__device__ __forceinline__ float u23(uint32_t r, uint32_t one) {
+  return __uint_as_float(mant1(r, one)) - (1.0f - 0x1p-24f);
 }
 
 __device__ __forceinline__ float sqrt_approx(float x) {
@@ -177,21 +191,10 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
-// Box-Muller (R13) with the scale folded into L': returns (z0, z1) / FOLD_SCALE =
-// (r cos 2 pi ub, r sin 2 pi ub), r = sqrt(-lg2 ua) = R / sqrt(2 ln 2).  The angle
-// is taken in (-pi, pi) as 2 pi (ub - 1/2), which flips both signs (absorbed by
-// FOLD_SCALE < 0); with F = 1 + (r mod 2^23) 2^-23 it is one FFMA:
-// 2 pi F - 2 pi (3/2 - 2^-24).
-__device__ __forceinline__ void box_muller(uint32_t ra, uint32_t rb, float& z0, float& z1) {
-  float ua = u23(ra);
-  float fb = __uint_as_float(0x3f800000u | (rb & 0x7fffffu));
-  float r = sqrt_approx(fmaxf(-lg2_approx(ua), 0.0f));
-  float s, co;
-  __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
-  z0 = r * co;
-  z1 = r * s;
-}
-
+// Box-Muller (R13) with the scale folded into L' (chol8.cuh stores FOLD_SCALE L): returns
+// (z0, z1) / FOLD_SCALE = (r cos 2 pi ub, r sin 2 pi ub), r = sqrt(-lg2 ua) = R / sqrt(2 ln 2).
+// The angle is taken in (-pi, pi) as 2 pi (ub - 1/2), which flips both signs (absorbed by
+// FOLD_SCALE < 0); with F = 1 + (r mod 2^23) 2^-23 it is one FFMA: 2 pi F - 2 pi (3/2 - 2^-24).
 // Packed FP32x2 arithmetic (sm_100a FFMA2 / FMUL2): two lanes of FP32 per
 // instruction, each rounded exactly as the scalar fmaf / multiply; a pair built
 // from one scalar twice is issued as a broadcast operand.
@@ -214,10 +217,10 @@ __device__ __forceinline__ f2_t fmul2(f2_t a, f2_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
 }
-// box_muller with the two products r cos, r sin in one FMUL2: returns pk(z0, z1)
-__device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb) {
-  float ua = u23(ra);
-  float fb = __uint_as_float(0x3f800000u | (rb & 0x7fffffu));
+// Box-Muller with the two products r cos, r sin in one FMUL2: returns pk(z0, z1)
+__device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb, uint32_t one) {
+  float ua = u23(ra, one);
+  float fb = __uint_as_float(mant1(rb, one));
   float r = sqrt_approx(fmaxf(-lg2_approx(ua), 0.0f));
   float s, co;
   __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
@@ -234,7 +237,10 @@ constexpr float ZMAX = 5.7684f;
 #ifndef PMC_WARPS
 #define PMC_WARPS 1
 #endif
-constexpr int QCAP = 96;            // pending samples per warp (< 32 + two pushes of 32)
+#ifndef PMC_ILP
+#define PMC_ILP 2
+#endif
+constexpr int QCAP = PMC_ILP >= 4 ? 160 : 96;   // pending samples per warp (< 32 + ILP pushes of 32)
 constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are branch-free
 
 // k_pmc<T>: exact two-phase evaluation of the PMC count for
@@ -255,13 +261,17 @@ constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are 
 #ifndef PMC_MINBLOCKS
 #define PMC_MINBLOCKS 8
 #endif
-#ifndef PMC_ILP
-#define PMC_ILP 2
+#ifndef PMC_QUEUE_PRED
+#define PMC_QUEUE_PRED 0
+#endif
+#ifndef PMC_UNIFORM_Q
+#define PMC_UNIFORM_Q 1
 #endif
 constexpr int MAX_ISO = 16;
 struct IsoOffsets {
   float dl[MAX_ISO];   // th_t - th_0 (padding: +inf, never crosses)
   int n_out;           // isovalues written (T is padded up to an instantiated size)
+  uint32_t one_bits;   // 0x3f800000 (the bits of 1.0f)
 };
 
 template <int T>
@@ -276,7 +286,9 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   __shared__ unsigned int s_p2;
   if (threadIdx.x == 0) s_p2 = 0;
   __syncthreads();
-  const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // one-warp CTAs: the cell index is blockIdx.x, provably warp-uniform, so ptxas keeps the
+  // Philox round keys and other per-cell scalars in uniform registers (118 -> 94 registers)
+  const int64_t q = (PMC_WARPS == 1 && PMC_UNIFORM_Q) ? (int64_t)blockIdx.x : (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const bool live = q < n;
   // m[c] = mu_c - th_0 (c < 4); mB[c] = mu_c - th_0 - B_c for the last four corners
@@ -351,6 +363,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   const float L11 = L[2], L33 = L[9];
   const f2_t M01 = pk(m[0], m[1]), M23 = pk(m[2], m[3]), MB45 = pk(mB[0], mB[1]), MB67 = pk(mB[2], mB[3]);
   const f2_t B45 = pk(B[0], B[1]), B67 = pk(B[2], B[3]), TWO = pk(2.0f, 2.0f);
+  const uint32_t ONE = D.one_bits;   // 0x3f800000 through a kernel parameter: a register, not an immediate
   // phase 1 of sample s: returns true (and the stash) if the sample is undecided.
   // y_c for c < 4 exactly; lo_c = y_c - B_c - R_c and hi_c = lo_c + 2 B_c for c >= 4.
   // Same FP32 operations in the same order as the scalar chains y = fma(L'_cd, z_d, y).
@@ -359,7 +372,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     // counter (cell lo, iso, cell hi, 2s + j) (R13): the sample word enters round 1
     // only through an XOR, so rounds 1-3 need 2 varying IMAD.WIDE instead of 4
     philox4x32_10(c1, iso, c2, 2u * s, K, r0, r1, r2, r3);
-    const f2_t zA = box_muller2(r0, r1), zB = box_muller2(r2, r3);
+    const f2_t zA = box_muller2(r0, r1, ONE), zB = box_muller2(r2, r3, ONE);
     float z[4];
     upk(zA, z[0], z[1]);
     upk(zB, z[2], z[3]);
@@ -418,12 +431,26 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; vote.sync.ballot.b32 %0, p, 0xffffffff;}"
                  : "=r"(mb) : "r"((unsigned)pb));
     const int na = __popc(ma);
+#if PMC_QUEUE_PRED
+    // predicated stores: only the ~7 % undecided samples move data
+    if (pa) {
+      const int sa = qn + __popc(ma & lt);
+      qv[sa] = a0;
+      qw[sa] = a1;
+    }
+    if (pb) {
+      const int sb = qn + na + __popc(mb & lt);
+      qv[sb] = b0;
+      qw[sb] = b1;
+    }
+#else
     const int sa = pa ? qn + __popc(ma & lt) : QCAP + lane;
     const int sb = pb ? qn + na + __popc(mb & lt) : QCAP + lane;
     qv[sa] = a0;
     qw[sa] = a1;
     qv[sb] = b0;
     qw[sb] = b1;
+#endif
     qn += na + __popc(mb);
   };
   auto push = [&](bool pend, const float4& st0, const float4& st1) {
@@ -440,8 +467,8 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
       uint32_t r4, r5, r6, r7;
       philox4x32_10(c1, iso, c2, 2u * s + 1u, K, r4, r5, r6, r7);
       float z[8];
-      upk(box_muller2(r4, r5), z[4], z[5]);
-      upk(box_muller2(r6, r7), z[6], z[7]);
+      upk(box_muller2(r4, r5, ONE), z[4], z[5]);
+      upk(box_muller2(r6, r7, ONE), z[6], z[7]);
       float mx = vb.x, mn = vb.y;
       // y_c = (lo_c + B_c) + sum_{d>=4} L'_cd z_d, pairs (4,5) and (6,7)
       f2_t Y45 = ffma2(Q45[0], pk(z[4], z[4]), pk(va.x + B[0], va.y + B[1]));
@@ -472,8 +499,21 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     }
   };
   uint32_t base = 0;
-  // two samples per lane per iteration (instruction-level parallelism)
-  for (; ILP == 2 && base + 64u <= Nl; base += 64u) {
+  // four / two samples per lane per iteration (instruction-level parallelism)
+  for (; ILP == 4 && base + 128u <= Nl; base += 128u) {
+    float4 a0, a1, b0, b1, c0, c1_, d0, d1;
+    const bool pa = phase1(base + lane, a0, a1);
+    const bool pb = phase1(base + 32u + lane, b0, b1);
+    const bool pc = phase1(base + 64u + lane, c0, c1_);
+    const bool pd = phase1(base + 96u + lane, d0, d1);
+    push2(pa, a0, a1, pb, b0, b1);
+    push2(pc, c0, c1_, pd, d0, d1);
+    drain();
+    drain();
+    drain();
+    drain();
+  }
+  for (; ILP >= 2 && base + 64u <= Nl; base += 64u) {
     float4 a0, a1, b0, b1;
     const bool pa = phase1(base + lane, a0, a1);
     const bool pb = phase1(base + 32u + lane, b0, b1);
@@ -606,6 +646,7 @@ lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const doubl
   IsoOffsets D;
   for (int t = 0; t < MAX_ISO; ++t) D.dl[t] = t < T ? (float)(thetas[t] - thetas[0]) : INFINITY;
   D.n_out = T;
+  D.one_bits = 0x3f800000u;
   const int Tp = T <= 4 ? T : (T <= 6 ? 6 : (T <= 8 ? 8 : (T <= 12 ? 12 : 16)));
   // records of the refine-time brick pass cover the list? (e.g. every leaf of a refine)
   bool use_rec = false;
