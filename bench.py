@@ -41,6 +41,10 @@ OPS_PHASE2 = 99
 OPS_SURVEY = 186
 OPS_SURVEY_PER_EXTRA_ISO = 21
 SM_COUNT = 148
+try:
+    HBM_PEAK_GBS = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    HBM_PEAK_GBS = 6532.9
 LANES_PER_SM_CLK = 128
 
 
@@ -201,6 +205,25 @@ def _sub_cells(cfg, lfull, sub):
         return int(np.prod(cfg.cells))
     side = 1 << (lfull - sub[0])
     return int(np.prod([max(0, min(side, cfg.cells[d] - side * sub[1 + d])) for d in range(3)]))
+
+
+def hbm_fractions(cells_per_launch, s_per_launch):
+    """HBM bandwidth of the hot kernels vs the measured copy peak (MEASURED_PEAKS.json):
+    k_pmc from its ncu bytes per cell x this run's cells / this run's k_pmc time; the
+    brick-pass kernels from their own ncu capture (profiles/traffic.json)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return None
+    peak = HBM_PEAK_GBS
+    out = {"peak_gbs": peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+    if s_per_launch > 0:
+        gbs = t["k_pmc"]["dram_bytes_per_cell"] * cells_per_launch / s_per_launch / 1e9
+        out["k_pmc"] = {"gbs": gbs, "frac": gbs / peak, "source": "ncu bytes/cell x live time"}
+    for kname in ("k_brick", "k_chol8_rec"):
+        if kname in t:
+            out[kname] = {"gbs": t[kname]["ncu_gbs"], "frac": t[kname]["ncu_hbm_frac"], "source": "ncu capture"}
+    return out
 
 
 def oracle_sample(w, steps=1, warmup=0):
@@ -462,7 +485,8 @@ def run_ours(args):
     fused_t = len(w.thetas) if len(w.thetas) > 1 and not args.dense and not args.separate_iso else 1
     ops_survey = samples_step * (OPS_SURVEY + OPS_SURVEY_PER_EXTRA_ISO * (fused_t - 1))
     achieved = (ops_survey / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
-    traffic = load_traffic(leaves_step / max(world, 1) / max(len(w.thetas) if args.dense or args.separate_iso else 1, 1))
+    launches_per_step = 1 if fused_t > 1 else len(w.thetas)      # k_pmc launches per step
+    traffic = load_traffic(union_step / max(world, 1) / launches_per_step)
     roofline = {"bound": "alu", "kernel": "k_pmc", "achieved": achieved, "peak": peak,
                 "unit": "Tlane-op/s", "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "ops_per_sample": ops_survey / samples_step if samples_step else None,
@@ -481,6 +505,7 @@ def run_ours(args):
                 "fp32_tflops": ((samples_step * 70 + p2_step * 34) / max(world, 1) / mc_s / 1e12
                                 if mc_s > 0 else None),
                 "fp32_peak_tflops": 74.4,
+                "hbm": hbm_fractions(union_step / max(world, 1) / launches_per_step, mc_s / launches_per_step),
                 "peak_note": "148 SMs x 128 lanes x 1.965 GHz issue slots (guide unit counts, max clock)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

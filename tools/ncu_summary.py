@@ -49,6 +49,18 @@ def run(rep):
                     'smsp__inst_executed.avg.per_cycle_active', 'sm__cycles_elapsed.avg.per_second']:
             if key in d:
                 print(f'    {key} = {d[key]}')
+        # HBM bandwidth of the launch against the measured copy peak (MEASURED_PEAKS.json)
+        units = dict(zip(h, rows[1]))
+        scale = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1e-9, 'nsecond': 1e-9, 'us': 1e-6,
+                 'usecond': 1e-6, 'ms': 1e-3, 'msecond': 1e-3}
+        try:
+            val = lambda k: float(d[k].replace(',', '')) * scale.get(units.get(k, ''), 1.0)  # noqa: E731
+            byt = val('dram__bytes_read.sum') + val('dram__bytes_write.sum')
+            dur = val('gpu__time_duration.sum')
+            gbs = byt / dur / 1e9
+            print(f'    HBM: {byt:.4g} B in {dur * 1e3:.3f} ms = {gbs:.1f} GB/s = {gbs / 6532.9:.4f} of 6532.9 GB/s')
+        except (KeyError, ValueError):
+            pass
 
 
 if __name__ == '__main__':
