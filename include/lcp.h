@@ -87,8 +87,11 @@ typedef struct {
                               records (208 B per cell) fit in free HBM, -1 = off */
     int32_t local_mode;    /* bucket local sets: 0 = the k nearest observations to the bucket
                               centre (R2, BASELINE); 1 = every observation inside the bucket box
-                              enlarged by beta * lengthscale per axis (R28),
-                              at most k of them (EINVAL otherwise), padded to k internally */
+                              enlarged by beta * lengthscale per axis (R28, PAPER.md:197-199:
+                              the paper's M' of the level-bucket_log2 node), at most k of them
+                              (EINVAL otherwise), padded to k internally; 2 = as 1, with the
+                              |M'| cap k: a bucket whose box holds more than k takes its k-NN
+                              set instead (R28b; lcp_stats_json "capped_buckets") */
     int32_t pad1_;
     double beta;           /* local_mode 1: box enlargement in lengthscales (the paper uses 6) */
 } lcp_opts_t;
@@ -135,9 +138,11 @@ lcp_status_t lcp_fit_local(lcp_ctx_t* ctx, const double* xyz, const double* y, i
 /* NEXT-2: the same as lcp_fit_local for a sparse-GP (SGPR) model: inducing
  * points xyz_M (m x 3), their posterior mean mu_M (m) and covariance A_M
  * (m x m row-major, symmetric, A_M <= K_MM) as stored after SGPR fitting
- * (PAPER.md:80-100).  Each bucket keeps its k nearest inducing points and
- * evaluates Eq. 1 with the A_M term on them.  kernel->nugget
- * is the jitter added to K_SS (use ~1e-8 sigma_f^2).  Host or device pointers
+ * (PAPER.md:80-100).  Each bucket keeps its local inducing points (opts->local_mode:
+ * its k nearest, or the beta-box set M' of PAPER.md:197-199) and evaluates Eq. 1
+ * with the A_M term on them (whitened: v^T (I - L^-1 A L^-T) v, no
+ * explicit K_SS^-1).  kernel->nugget is the jitter added to K_SS (e.g. 1e-9..1e-6
+ * sigma_f^2).  Host or device pointers
  * as for lcp_fit_local.  Errors as lcp_fit_local, plus EINVAL for m > 60000 or a
  * non-finite A_M entry. */
 lcp_status_t lcp_fit_sgpr(lcp_ctx_t* ctx, const double* xyz_M, const double* mu_M, const double* A_M,

@@ -69,7 +69,7 @@ def lib():
         L.orc_model_create.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, C.c_int64,
                                        C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]
         L.orc_model_create_box.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, C.c_int64,
-                                           C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(P)]
+                                           C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32, C.POINTER(P)]
         L.orc_model_destroy.argtypes = [P]
         L.orc_model_destroy.restype = None
         L.orc_model_nbuckets.argtypes = [P]
@@ -115,6 +115,9 @@ def lib():
         L.orc_sgpr_exact.argtypes = [C.POINTER(Kernel), dp, dp, dp, C.c_int64, dp, C.c_int64, dp, P]
         L.orc_model_create_sgpr.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, dp, C.c_int64,
                                             C.c_int32, C.c_int32, C.c_int32, C.POINTER(P)]
+        L.orc_model_create_sgpr_mode.argtypes = [C.POINTER(Kernel), C.POINTER(Grid), dp, dp, dp, C.c_int64,
+                                                 C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                                 C.POINTER(P)]
         L.orc_free.argtypes = [P]
         L.orc_free.restype = None
         L.orc_num_threads.restype = C.c_int
@@ -232,8 +235,9 @@ class Model:
         self._h = h
 
     @classmethod
-    def sgpr(cls, kern: Kernel, grid: Grid, XM, muM, AM, k, bucket_log2, h_full):
-        """NEXT-2: bucket-local SGPR model (Eq. 1 with the A_M term)."""
+    def sgpr(cls, kern: Kernel, grid: Grid, XM, muM, AM, k, bucket_log2, h_full, local_mode=0, beta=6.0):
+        """NEXT-2: bucket-local SGPR model (Eq. 1 with the A_M term); local sets k-NN (0),
+        beta-box (1) or capped beta-box (2)."""
         self = cls.__new__(cls)
         self.kern, self.grid = kern, grid
         self.X = np.ascontiguousarray(XM, np.float64)
@@ -242,14 +246,16 @@ class Model:
         self.k = int(k)
         self.cells = tuple(grid.cells)
         h = C.c_void_p()
-        _check(lib().orc_model_create_sgpr(C.byref(kern), C.byref(grid), self.X, self.y, self.A, len(self.X),
-                                           int(k), int(bucket_log2), int(h_full), C.byref(h)), "model_create_sgpr")
+        _check(lib().orc_model_create_sgpr_mode(C.byref(kern), C.byref(grid), self.X, self.y, self.A, len(self.X),
+                                                int(k), int(bucket_log2), int(h_full), int(local_mode), float(beta),
+                                                C.byref(h)), "model_create_sgpr")
         self._h = h
         return self
 
     @classmethod
-    def box(cls, kern: Kernel, grid: Grid, X, y, k, bucket_log2, h_full, beta):
-        """R28 (NEXT-2): local set = observations in the bucket box enlarged by beta l_d."""
+    def box(cls, kern: Kernel, grid: Grid, X, y, k, bucket_log2, h_full, beta, cap=False):
+        """R28 (NEXT-2): local set = observations in the bucket box enlarged by beta l_d;
+        cap (R28b): a box holding more than k observations gives the bucket its k-NN set."""
         self = cls.__new__(cls)
         self.kern, self.grid = kern, grid
         self.X = np.ascontiguousarray(X, np.float64)
@@ -258,7 +264,7 @@ class Model:
         self.cells = tuple(grid.cells)
         h = C.c_void_p()
         _check(lib().orc_model_create_box(C.byref(kern), C.byref(grid), self.X, self.y, len(self.X), int(k),
-                                          int(bucket_log2), int(h_full), float(beta), C.byref(h)),
+                                          int(bucket_log2), int(h_full), float(beta), int(bool(cap)), C.byref(h)),
                "model_create_box")
         self._h = h
         return self

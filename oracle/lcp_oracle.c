@@ -166,7 +166,9 @@ struct orc_model {
     double beta;          /* box mode: enlargement of the bucket box in units of l_d */
     double* L;            /* nbuckets x k x k, lower factor of K_y(S_B) */
     double* alpha;        /* nbuckets x k */
-    double* WAW;          /* NEXT-2 SGPR mode: nbuckets x k x k, W A_SS W with W = K_SS^-1 (NULL: GP regression) */
+    double* B;            /* NEXT-2 SGPR mode: nbuckets x k x k, B = L^-1 A_SS L^-T (stride = set size; NULL: GP
+                             regression); Eq. 1's third term K_xS W A_SS W K_Sx = v^T B v with v = L^-1 K_Sx */
+    int32_t cap;          /* box mode, R28b: a bucket whose box holds > k observations takes its k-NN set */
     double* mu_obs;       /* m: local marginal at x_i from bucket(x_i) (R10) */
     double* var_obs;      /* m (floored) */
     int32_t* obs_cell;    /* m x 3 finest cell of x_i (clamped) */
@@ -249,10 +251,10 @@ int orc_local_marginal(const orc_model_t* M, int32_t b, const double* x, double*
     forward_sub(L, k, kv, v);
     double q = orc_kernel(&M->kern, x, x);
     for (int a = 0; a < k; ++a) q -= v[a] * v[a];
-    if (M->WAW) {   /* + K_xS W A_SS W K_Sx (Eq. 1, third term) */
-        const double* C = M->WAW + (size_t)b * ks * ks;
+    if (M->B) {   /* + K_xS W A_SS W K_Sx = v^T B v (Eq. 1, third term; W = L^-T L^-1) */
+        const double* Bb = M->B + (size_t)b * ks * ks;
         for (int a = 0; a < k; ++a)
-            for (int c = 0; c < k; ++c) q += kv[a] * C[(size_t)a * k + c] * kv[c];
+            for (int c = 0; c < k; ++c) q += v[a] * Bb[(size_t)a * k + c] * v[c];
     }
     *var = q;
     free(kv); free(v);
@@ -293,24 +295,24 @@ static int box_set(const orc_model_t* M, int32_t bkt, const double* X, int64_t m
 
 static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                         const double* y, int64_t m, int32_t k, int32_t bucket_log2,
-                        int32_t h_full, double beta, orc_model_t** out);
+                        int32_t h_full, double beta, int32_t cap, orc_model_t** out);
 
 int orc_model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                      const double* y, int64_t m, int32_t k, int32_t bucket_log2,
                      int32_t h_full, orc_model_t** out) {
-    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, 0.0, out);
+    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, 0.0, 0, out);
 }
 
 int orc_model_create_box(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                          const double* y, int64_t m, int32_t k, int32_t bucket_log2,
-                         int32_t h_full, double beta, orc_model_t** out) {
+                         int32_t h_full, double beta, int32_t cap, orc_model_t** out) {
     if (!(beta > 0.0)) return ORC_EINVAL;
-    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, beta, out);
+    return model_create(kern, grid, X, y, m, k, bucket_log2, h_full, beta, cap, out);
 }
 
 static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                         const double* y, int64_t m, int32_t k, int32_t bucket_log2,
-                        int32_t h_full, double beta, orc_model_t** out) {
+                        int32_t h_full, double beta, int32_t cap, orc_model_t** out) {
     *out = NULL;
     if (m < 1 || k < 1 || k > m || bucket_log2 < 0 || h_full < 0) return ORC_EINVAL;
     if (kern->variance <= 0 || kern->nugget < 0) return ORC_EINVAL;
@@ -339,6 +341,7 @@ static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const 
     M->m = (int32_t)m;
     M->k = k;
     M->beta = beta;
+    M->cap = cap;
     if (beta > 0.0) M->kb = malloc(sizeof(int32_t) * (size_t)M->nbuckets);
     M->X = malloc(sizeof(double) * 3 * m);
     M->y = malloc(sizeof(double) * m);
@@ -356,16 +359,22 @@ static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const 
         for (int d = 0; d < 3; ++d) c[d] = grid->lo[d] + ((double)bi[d] + 0.5) * ((double)M->bs * M->h[d]);
         int32_t* S = M->S + (size_t)bkt * k;
         int kb = k;
+        int use_knn = beta <= 0.0;
         if (beta > 0.0) {
             kb = box_set(M, bkt, X, m, S, k);
-            if (kb < 0) {
+            if (kb < 0 && M->cap) {          /* R28b: the |M'| cap -- this bucket takes its k-NN set */
+                use_knn = 1;
+                kb = k;
+            } else if (kb < 0) {
 #pragma omp critical
                 status = ORC_EINVAL;
                 kb = 0;
             }
             M->kb[bkt] = kb;
-            for (int a = kb; a < k; ++a) S[a] = -1;
-        } else {
+            if (!use_knn)
+                for (int a = kb; a < k; ++a) S[a] = -1;
+        }
+        if (use_knn) {
             /* k nearest in the metric sum_d ((x_d - c_d) w_d)^2, ties -> lower index (R2) */
             knn_item* it = malloc(sizeof(knn_item) * m);
             for (int64_t i = 0; i < m; ++i) {
@@ -425,105 +434,108 @@ static int model_create(const orc_kernel_t* kern, const orc_grid_t* grid, const 
 
 void orc_model_destroy(orc_model_t* M) {
     if (!M) return;
-    free(M->X); free(M->y); free(M->S); free(M->kb); free(M->L); free(M->alpha); free(M->WAW);
+    free(M->X); free(M->y); free(M->S); free(M->kb); free(M->L); free(M->alpha); free(M->B);
     free(M->mu_obs); free(M->var_obs); free(M->obs_cell);
     free(M);
 }
 
 /* ---------------------------------------------------------------- NEXT-2 --- */
-/* W = K_MM^-1 from the Cholesky factor L of K_MM: column j solves L L^T w = e_j. */
-static void inverse_from_chol(const double* L, int n, double* W) {
-    double* e = calloc(n, sizeof(double));
+/* B = L^-1 A L^-T for the Cholesky factor L of K_MM (n x n, A row-major with row
+ * stride lda, rows/cols indexed through idx, or the identity map if idx == NULL):
+ * column c of T = L^-1 A by forward substitution, then row r of B solves L x = T[r, :]^T.
+ * With W = K_MM^-1 = L^-T L^-1, K_IM W A W K_MI = v^T B v for v = L^-1 K_MI. */
+static void whiten_A(const double* L, int n, const double* A, int64_t lda, const int32_t* idx, double* B) {
+    double* col = malloc(sizeof(double) * n);
     double* t = malloc(sizeof(double) * n);
-    double* w = malloc(sizeof(double) * n);
-    for (int j = 0; j < n; ++j) {
-        e[j] = 1.0;
-        forward_sub(L, n, e, t);
-        backward_sub(L, n, t, w);
-        for (int i = 0; i < n; ++i) W[(size_t)i * n + j] = w[i];
-        e[j] = 0.0;
+    double* T = malloc(sizeof(double) * (size_t)n * n);
+    for (int c = 0; c < n; ++c) {
+        for (int r = 0; r < n; ++r) {
+            int64_t ir = idx ? idx[r] : r, ic = idx ? idx[c] : c;
+            col[r] = A[(size_t)ir * lda + ic];
+        }
+        forward_sub(L, n, col, t);
+        for (int r = 0; r < n; ++r) T[(size_t)r * n + c] = t[r];
     }
-    free(e); free(t); free(w);
+    for (int r = 0; r < n; ++r) {
+        forward_sub(L, n, T + (size_t)r * n, t);
+        for (int c = 0; c < n; ++c) B[(size_t)r * n + c] = t[c];
+    }
+    free(col); free(t); free(T);
 }
 
-/* Eq. 1 literally, for an SGPR model (inducing points X_M,
- * their posterior mean mu_M and covariance A_M, m x m row-major):
+/* Eq. 1 for an SGPR model (inducing points X_M, their posterior mean
+ * mu_M and covariance A_M, m x m row-major):
  *   mu_I    = m0 + K_IM K_MM^-1 (mu_M - m0)
  *   Sigma_I = K_II - K_IM K_MM^-1 K_MI + K_IM K_MM^-1 A_M K_MM^-1 K_MI,
- * with K_MM + jitter I (jitter = kern->nugget). */
+ * with K_MM + jitter I (jitter = kern->nugget) = L L^T.  K_MM^-1 = L^-T L^-1 is applied
+ * by triangular solves: v = L^-1 K_MI, the second term is v^T v and the third v^T B v
+ * with B = L^-1 A_M L^-T (no explicit inverse: the product with an explicit K_MM^-1
+ * loses ~cond(K_MM) eps, 4e-7 sigma_f^2 on ill-conditioned SGPR fits, against ~1e-9
+ * here; tests/test_oracle_sgpr.py pins this against extended precision). */
 int orc_sgpr_exact(const orc_kernel_t* kern, const double* XM, const double* muM, const double* AM, int64_t m,
                    const double* Q, int64_t nq, double* mu, double* cov) {
     int n = (int)m;
     double* K = malloc(sizeof(double) * n * n);
     double* L = malloc(sizeof(double) * n * n);
-    double* W = malloc(sizeof(double) * n * n);
-    double* KQ = malloc(sizeof(double) * nq * n);
-    double* P = malloc(sizeof(double) * nq * n);   /* K_IM W */
+    double* B = malloc(sizeof(double) * n * n);
+    double* V = malloc(sizeof(double) * nq * n);   /* v_q = L^-1 K_Mq */
+    double* kq = malloc(sizeof(double) * n);
+    double* r = malloc(sizeof(double) * n);
+    double* w = malloc(sizeof(double) * n);
+    double* al = malloc(sizeof(double) * n);
     for (int a = 0; a < n; ++a)
         for (int b = 0; b < n; ++b)
             K[a * n + b] = orc_kernel(kern, XM + 3 * a, XM + 3 * b) + (a == b ? kern->nugget : 0.0);
     int st = chol_jitter(K, L, n, kern->variance);
     if (st == ORC_OK) {
-        inverse_from_chol(L, n, W);
-        for (int64_t q = 0; q < nq; ++q)
-            for (int a = 0; a < n; ++a) KQ[q * n + a] = orc_kernel(kern, Q + 3 * q, XM + 3 * a);
-        for (int64_t q = 0; q < nq; ++q)
-            for (int b = 0; b < n; ++b) {
-                double s = 0.0;
-                for (int a = 0; a < n; ++a) s += KQ[q * n + a] * W[(size_t)a * n + b];
-                P[q * n + b] = s;
-            }
+        for (int a = 0; a < n; ++a) r[a] = muM[a] - kern->prior_mean;
+        forward_sub(L, n, r, w);                  /* alpha = K_MM^-1 (mu_M - m0) */
+        backward_sub(L, n, w, al);
+        whiten_A(L, n, AM, m, NULL, B);
         for (int64_t q = 0; q < nq; ++q) {
             double s = 0.0;
-            for (int a = 0; a < n; ++a) s += P[q * n + a] * (muM[a] - kern->prior_mean);
+            for (int a = 0; a < n; ++a) {
+                kq[a] = orc_kernel(kern, Q + 3 * q, XM + 3 * a);
+                s += kq[a] * al[a];
+            }
             mu[q] = kern->prior_mean + s;
+            forward_sub(L, n, kq, V + (size_t)q * n);
         }
         if (cov)
             for (int64_t p = 0; p < nq; ++p)
                 for (int64_t q = 0; q < nq; ++q) {
+                    const double* vp = V + (size_t)p * n;
+                    const double* vq = V + (size_t)q * n;
                     double s = orc_kernel(kern, Q + 3 * p, Q + 3 * q);
-                    for (int a = 0; a < n; ++a) s -= P[p * n + a] * KQ[q * n + a];
+                    for (int a = 0; a < n; ++a) s -= vp[a] * vq[a];
                     for (int a = 0; a < n; ++a)
-                        for (int b = 0; b < n; ++b) s += P[p * n + a] * AM[(size_t)a * n + b] * P[q * n + b];
+                        for (int b = 0; b < n; ++b) s += vp[a] * B[(size_t)a * n + b] * vq[b];
                     cov[p * nq + q] = s;
                 }
     }
-    free(K); free(L); free(W); free(KQ); free(P);
+    free(K); free(L); free(B); free(V); free(kq); free(r); free(w); free(al);
     return st;
 }
 
-/* Bucket-local SGPR: each bucket keeps its k nearest inducing points S (R2) and
- * Eq. 1 restricted to S: L = chol(K_SS + jitter), alpha = W (mu_S - m0),
- * WAW = W A_SS W.  Marginals / cell posteriors add the third term of Eq. 1. */
-int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM, const double* muM,
-                          const double* AM, int64_t m, int32_t k, int32_t bucket_log2, int32_t h_full,
-                          orc_model_t** out) {
-    /* the k-NN sets, K_SS factor and alpha are the GP-regression model with nugget = jitter */
-    int st = orc_model_create(kern, grid, XM, muM, m, k, bucket_log2, h_full, out);
+/* Bucket-local SGPR: each bucket keeps its local inducing points S -- the k nearest
+ * (R2), or the beta-box set (R28; local_mode 2: capped at k by R28b) -- and Eq. 1
+ * restricted to S: L = chol(K_SS + jitter), alpha = K_SS^-1 (mu_S - m0) by solves,
+ * B = L^-1 A_SS L^-T.  Marginals / cell posteriors add the third term v^T B v. */
+int orc_model_create_sgpr_mode(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM,
+                               const double* muM, const double* AM, int64_t m, int32_t k, int32_t bucket_log2,
+                               int32_t h_full, int32_t local_mode, double beta, orc_model_t** out) {
+    /* the local sets, K_SS factor and alpha are the GP-regression model with nugget = jitter */
+    int st = local_mode == 0 ? orc_model_create(kern, grid, XM, muM, m, k, bucket_log2, h_full, out)
+                             : orc_model_create_box(kern, grid, XM, muM, m, k, bucket_log2, h_full, beta,
+                                                    local_mode == 2, out);
     if (st != ORC_OK) return st;
     orc_model_t* M = *out;
-    M->WAW = malloc(sizeof(double) * (size_t)M->nbuckets * k * k);
+    M->B = calloc((size_t)M->nbuckets * k * k, sizeof(double));
 #pragma omp parallel for schedule(dynamic)
     for (int32_t bkt = 0; bkt < M->nbuckets; ++bkt) {
-        const int32_t* S = M->S + (size_t)bkt * k;
-        const double* Lb = M->L + (size_t)bkt * k * k;
-        double* W = malloc(sizeof(double) * k * k);
-        double* T = malloc(sizeof(double) * k * k);
-        inverse_from_chol(Lb, k, W);
-        for (int a = 0; a < k; ++a)          /* T = W A_SS */
-            for (int c = 0; c < k; ++c) {
-                double s = 0.0;
-                for (int d = 0; d < k; ++d) s += W[(size_t)a * k + d] * AM[(size_t)S[d] * m + S[c]];
-                T[(size_t)a * k + c] = s;
-            }
-        double* C = M->WAW + (size_t)bkt * k * k;
-        for (int a = 0; a < k; ++a)          /* W A_SS W */
-            for (int c = 0; c < k; ++c) {
-                double s = 0.0;
-                for (int d = 0; d < k; ++d) s += T[(size_t)a * k + d] * W[(size_t)d * k + c];
-                C[(size_t)a * k + c] = s;
-            }
-        free(W); free(T);
+        const int kb = set_size(M, bkt);
+        if (kb > 0)
+            whiten_A(M->L + (size_t)bkt * k * k, kb, AM, m, M->S + (size_t)bkt * k, M->B + (size_t)bkt * k * k);
     }
     /* observation marginals now include the A term */
     for (int64_t i = 0; i < m; ++i) {
@@ -532,6 +544,12 @@ int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, cons
         if (floor_var(M, var, &M->var_obs[i]) != ORC_OK) { orc_model_destroy(M); *out = NULL; return ORC_ENUMERIC; }
     }
     return ORC_OK;
+}
+
+int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM, const double* muM,
+                          const double* AM, int64_t m, int32_t k, int32_t bucket_log2, int32_t h_full,
+                          orc_model_t** out) {
+    return orc_model_create_sgpr_mode(kern, grid, XM, muM, AM, m, k, bucket_log2, h_full, 0, 0.0, out);
 }
 
 /* ------------------------------------------------------------------ C8 --- */
@@ -558,14 +576,14 @@ int orc_cell_posterior(const orc_model_t* M, int64_t cell, double* mu, double* c
         forward_sub(L, k, Kc, V + (size_t)c * k);
     }
     int st = ORC_OK;
-    const double* Cw = M->WAW ? M->WAW + (size_t)b * ks * ks : NULL;
+    const double* Bb = M->B ? M->B + (size_t)b * ks * ks : NULL;
     for (int c = 0; c < 8; ++c)
         for (int e = 0; e < 8; ++e) {
             double s = orc_kernel(&M->kern, xc[c], xc[e]);
             for (int a = 0; a < k; ++a) s -= V[(size_t)c * k + a] * V[(size_t)e * k + a];
-            if (Cw)   /* + K_cS W A_SS W K_Se (Eq. 1, third term) */
+            if (Bb)   /* + K_cS W A_SS W K_Se = v_c^T B v_e (Eq. 1, third term) */
                 for (int a = 0; a < k; ++a)
-                    for (int d = 0; d < k; ++d) s += K[(size_t)c * k + a] * Cw[(size_t)a * k + d] * K[(size_t)e * k + d];
+                    for (int d = 0; d < k; ++d) s += V[(size_t)c * k + a] * Bb[(size_t)a * k + d] * V[(size_t)e * k + d];
             cov[c * 8 + e] = s;
         }
     for (int c = 0; c < 8; ++c)

@@ -59,10 +59,11 @@ void orc_model_destroy(orc_model_t* M);
 
 /* R28 (NEXT-2): box mode -- bucket b's local set is every observation
  * inside the bucket box enlarged by beta l_d per axis (ascending index, at most k;
- * ORC_EINVAL if a box holds more than k). */
+ * ORC_EINVAL if a box holds more than k, unless cap != 0: R28b, the |M'| cap -- such a
+ * bucket takes its k nearest observations, R2, instead). */
 int orc_model_create_box(const orc_kernel_t* kern, const orc_grid_t* grid, const double* X,
                          const double* y, int64_t m, int32_t k, int32_t bucket_log2,
-                         int32_t h_full, double beta, orc_model_t** out);
+                         int32_t h_full, double beta, int32_t cap, orc_model_t** out);
 int32_t orc_model_nbuckets(const orc_model_t* M);
 int32_t orc_model_lfull(const orc_model_t* M);
 /* S_B of bucket b (ascending observation indices), k entries */
@@ -118,6 +119,10 @@ int orc_sgpr_exact(const orc_kernel_t* kern, const double* XM, const double* muM
 int orc_model_create_sgpr(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM, const double* muM,
                           const double* AM, int64_t m, int32_t k, int32_t bucket_log2, int32_t h_full,
                           orc_model_t** out);
+/* the same with the local sets of local_mode 0 (k-NN), 1 (beta-box) or 2 (capped beta-box) */
+int orc_model_create_sgpr_mode(const orc_kernel_t* kern, const orc_grid_t* grid, const double* XM,
+                               const double* muM, const double* AM, int64_t m, int32_t k, int32_t bucket_log2,
+                               int32_t h_full, int32_t local_mode, double beta, orc_model_t** out);
 
 /* NEXT-1 (R26): continuous extreme search at nodes with h > h_full; iters = 0 disables. */
 void orc_model_set_extreme(orc_model_t* M, int32_t iters);

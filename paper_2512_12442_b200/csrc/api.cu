@@ -170,7 +170,7 @@ void lcp_destroy(lcp_ctx_t* ctx) {
   cudaStreamSynchronize(c.stream);
   DevBuf* bufs[] = {&c.X, &c.y, &c.obs_bucket, &c.bcount, &c.bstart, &c.gcount, &c.goff, &c.obs_by_bucket,
                     &c.S, &c.bdata, &c.fscratch, &c.obs_key, &c.obs_sorted_key, &c.obs_sorted_idx, &c.occ[0], &c.occ[1], &c.occ[2], &c.obs_mu,
-                    &c.obs_sd, &c.plo, &c.phi, &c.derr, &c.knn_fail, &c.vcache, &c.vstate, &c.front[0],
+                    &c.obs_sd, &c.plo, &c.phi, &c.derr, &c.knn_fail, &c.S_knn, &c.box_cnt, &c.vcache, &c.vstate, &c.front[0],
                     &c.front[1], &c.ncase, &c.nref, &c.np1, &c.np2, &c.nU, &c.cnt, &c.offs, &c.scan_tmp,
                     &c.req, &c.req_sorted, &c.counters, &c.leaves, &c.recs, &c.cell_bucket, &c.brick_key, &c.child_bricks, &c.perm,
                     &c.cells_tmp, &c.post, &c.lcp_tmp, &c.field_tmp,
@@ -405,12 +405,13 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
                 "\"scatter_ms\": %.6f, \"leaves\": %lld, \"pmc_cells\": %lld, \"pmc_samples\": %lld, "
                 "\"vertex_marginals\": %lld, \"knn_fallbacks\": %d, \"nbuckets\": %d, \"k\": %d, \"m\": %lld, "
                 "\"launches\": %lld, \"brick_runs\": %lld, \"pmc_phase2_samples\": %lld, \"brick_pass_ms\": %.6f, "
-                "\"fused\": %d, \"pmc_used_records\": %d",
+                "\"fused\": %d, \"pmc_used_records\": %d, \"capped_buckets\": %d, \"max_set\": %d",
                 c.t.fit_ms, c.t.refine_ms, c.t.posterior_ms, c.t.chol_ms, c.t.mc_ms, c.t.scatter_ms,
                 (long long)c.n_leaves, (long long)c.last_pmc_cells, (long long)c.last_pmc_samples,
                 (long long)c.last_requests, c.knn_fallbacks, c.g.nbuckets, c.k, (long long)c.m,
                 (long long)c.n_launch, (long long)c.last_brick_runs,
-                (long long)c.last_pmc_phase2, c.t.brick_ms, c.fused ? 1 : 0, c.last_pmc_records ? 1 : 0);
+                (long long)c.last_pmc_phase2, c.t.brick_ms, c.fused ? 1 : 0, c.last_pmc_records ? 1 : 0, c.n_capped,
+                c.max_set);
   s += tmp;
   auto arr = [&](const char* name, const std::vector<int64_t>& v) {
     s += ", \"";

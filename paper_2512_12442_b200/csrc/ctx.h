@@ -93,6 +93,8 @@ struct Ctx {
   DevBuf plo, phi;           // per-theta observation tails (Morton order)
   DevBuf derr;               // device error flags (int)
   DevBuf knn_fail;           // int: buckets whose ring search overflowed
+  DevBuf S_knn, box_cnt;     // local_mode 2: k-NN sets, beta-box counts per bucket
+  int n_capped = 0;          // local_mode 2: buckets whose beta-box exceeded k (took the k-NN set)
   int knn_fallbacks = 0;
   int max_set = 0;            // box mode: largest bucket set
   int64_t n_launch = 0;      // kernels this ctx has launched (cumulative)

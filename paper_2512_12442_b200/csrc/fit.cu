@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g
 // Bounds left to right without FMA, as the oracle's.  cnt_max: the largest set.
 __global__ void __launch_bounds__(256) k_box_sets(Geom g, const double* __restrict__ X, int64_t m, int k,
                                                   double bl0, double bl1, double bl2, int32_t* __restrict__ S,
-                                                  int* __restrict__ cnt_max) {
+                                                  int* __restrict__ cnt_max, int* __restrict__ cnt) {
   __shared__ int s_base;
   __shared__ int s_wcnt[8];
   const int b = blockIdx.x;
@@ -301,7 +301,19 @@ __global__ void __launch_bounds__(256) k_box_sets(Geom g, const double* __restri
   }
   const int n = s_base;
   for (int a = n + threadIdx.x; a < k; a += blockDim.x) Sb[a] = -1;
-  if (threadIdx.x == 0) atomicMax(cnt_max, n);
+  if (threadIdx.x == 0) {
+    atomicMax(cnt_max, n);
+    cnt[b] = n;
+  }
+}
+
+// R28b (local_mode 2, the |M'| cap): a bucket whose beta-box holds more than k
+// observations takes its k-NN set (R2) instead
+__global__ void k_box_cap(const int* __restrict__ cnt, int nbuckets, int k, const int32_t* __restrict__ S_knn,
+                          int32_t* __restrict__ S) {
+  const int b = blockIdx.x;
+  if (b >= nbuckets || cnt[b] <= k) return;
+  for (int a = threadIdx.x; a < k; a += blockDim.x) S[(int64_t)b * k + a] = S_knn[(int64_t)b * k + a];
 }
 
 // padded slot a of a box set: a far-away dummy observation, decoupled from everything
@@ -723,14 +735,19 @@ size_t bucket_factor_blk_smem(int k, bool gmem) {
   return sizeof(double) * (5 * (size_t)KP + 2 * (size_t)nb * FB * 12 + (gmem ? 0 : (size_t)KP * (KP + 4)));
 }
 
-// NEXT-2: SGPR bucket factor.  Eq. 1 restricted to the bucket's k nearest
-// inducing points S:  mu(x) = m0 + k_x^T W (mu_S - m0),
-//   Sigma = K - k^T C k,  C = W - W A_SS W,  W = (K_SS + jitter)^-1.
-// C is factored as C = G^T G with G LOWER triangular (Cholesky of the
-// index-reversed matrix P C P = R R^T, G = P R^T P; PSD clamp as R14), so the
-// bucket block [G as DMMA A-fragments | beta = W (mu_S - m0) | x_S] has the
-// same form as the GP-regression block (G = L^-1 there) and every downstream
-// kernel is unchanged.  Persistent CTAs with dense k x k global scratch.
+// NEXT-2: SGPR bucket factor.  Eq. 1 restricted to the bucket's local
+// inducing points S (its k nearest, or its beta-box set, R28):
+//   mu(x) = m0 + k_x^T W (mu_S - m0),  Sigma = K - k^T W k + k^T W A_SS W k,
+// W = (K_SS + jitter)^-1 = L^-T L^-1.  With v = L^-1 k and B = L^-1 A_SS L^-T the two
+// subtracted terms are v^T (I - B) v; I - B (eigenvalues in [0, 1]) is factored as
+// U U^T with U upper triangular (Cholesky of the index-reversed P (I - B) P = R R^T,
+// U = P R P; PSD clamp as R14), and G = U^T L^-1 is lower triangular with
+// Sigma = K - ||G k||^2.  So the bucket block [G as DMMA A-fragments | beta = W (mu_S -
+// m0) | x_S] has the same form as the GP-regression block (G = L^-1 there) and every
+// downstream kernel is unchanged.  No explicit W: on the ill-conditioned fuzz draws
+// (cond(K_SS) ~ 1e10-1e11) this keeps Sigma within ~1e-9 sigma_f^2 of an extended-
+// precision evaluation, where the former C = W - W A W factor lost ~1e-6.
+// Persistent CTAs with dense k x k global scratch (5 k^2 doubles each).
 __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams kp, int k, const double* __restrict__ X,
                                                                      const double* __restrict__ muM,
                                                                      const double* __restrict__ AM, int64_t m,
@@ -743,10 +760,10 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
   __shared__ double s_piv;
   const int tid = threadIdx.x, bd = blockDim.x;
   const int64_t kk = (int64_t)k * k;
-  double* M0 = scratch + (int64_t)blockIdx.x * 5 * kk;   // K -> L, later C
-  double* M1 = M0 + kk;                                  // L^-1, later T = W A
-  double* M2 = M1 + kk;                                  // W
-  double* M3 = M2 + kk;                                  // A_SS, later R
+  double* M0 = scratch + (int64_t)blockIdx.x * 5 * kk;   // K -> L, later P (I - B) P -> R
+  double* M1 = M0 + kk;                                  // L^-1
+  double* M2 = M1 + kk;                                  // T = L^-1 A_SS, later G
+  double* M3 = M2 + kk;                                  // A_SS; M3 + kk: L^-1 r
   double* sx = sm;
   double* sy = sx + k;
   double* sz = sy + k;
@@ -758,8 +775,13 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
     __syncthreads();
     for (int a = tid; a < k; a += bd) {
       int64_t o = Sb[a];
-      sx[a] = X[3 * o]; sy[a] = X[3 * o + 1]; sz[a] = X[3 * o + 2];
-      rr[a] = muM[o] - kp.m0;
+      if (o < 0) {   // R28 padding of a beta-box set: decoupled far-away dummy, no A term
+        sx[a] = dummy_coord(a, 0); sy[a] = dummy_coord(a, 1); sz[a] = dummy_coord(a, 2);
+        rr[a] = 0.0;
+      } else {
+        sx[a] = X[3 * o]; sy[a] = X[3 * o + 1]; sz[a] = X[3 * o + 2];
+        rr[a] = muM[o] - kp.m0;
+      }
       out[LA + k + a] = sx[a]; out[LA + 2 * k + a] = sy[a]; out[LA + 3 * k + a] = sz[a];
     }
     bool ok = false;
@@ -806,43 +828,48 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
         M1[(int64_t)i * k + j] = -s / M0[(int64_t)i * k + i];
       }
     }
-    // A_SS
-    for (int64_t e = tid; e < kk; e += bd) M3[e] = AM[(int64_t)Sb[e / k] * m + Sb[e % k]];
+    // A_SS (padding slots of a box set: 0 -- a decoupled dummy carries no A term)
+    for (int64_t e = tid; e < kk; e += bd) {
+      const int32_t si = Sb[e / k], sj = Sb[e % k];
+      M3[e] = (si >= 0 && sj >= 0) ? AM[(int64_t)si * m + sj] : 0.0;
+    }
+    __syncthreads();   // L^-1 and A_SS complete
+    // beta = W r = L^-T (L^-1 r) (two triangular products: no explicit W)
+    double* tv = M3 + kk;
+    for (int i = tid; i < k; i += bd) {
+      double s = 0.0;
+      for (int l = 0; l <= i; ++l) s = fma(M1[(int64_t)i * k + l], rr[l], s);
+      tv[i] = s;
+    }
     __syncthreads();
-    // W = L^-T L^-1
+    for (int i = tid; i < k; i += bd) {
+      double s = 0.0;
+      for (int l = i; l < k; ++l) s = fma(M1[(int64_t)l * k + i], tv[l], s);
+      out[LA + i] = s;
+    }
+    // T = L^-1 A_SS (into M2)
     for (int64_t e = tid; e < kk; e += bd) {
       int i = (int)(e / k), j = (int)(e % k);
       double s = 0.0;
-      for (int l = max(i, j); l < k; ++l) s = fma(M1[(int64_t)l * k + i], M1[(int64_t)l * k + j], s);
+      for (int l = 0; l <= i; ++l) s = fma(M1[(int64_t)i * k + l], M3[(int64_t)l * k + j], s);
       M2[e] = s;
     }
     __syncthreads();
-    // beta = W r -> alpha slot;  T = W A_SS (into M1)
-    for (int i = tid; i < k; i += bd) {
-      double s = 0.0;
-      for (int l = 0; l < k; ++l) s = fma(M2[(int64_t)i * k + l], rr[l], s);
-      out[LA + i] = s;
-    }
-    for (int64_t e = tid; e < kk; e += bd) {
-      int i = (int)(e / k), j = (int)(e % k);
-      double s = 0.0;
-      for (int l = 0; l < k; ++l) s = fma(M2[(int64_t)i * k + l], M3[(int64_t)l * k + j], s);
-      M1[e] = s;
-    }
-    __syncthreads();
-    // C = W - T W, stored index-reversed and symmetrised: M0[i][j] = C[k-1-i][k-1-j]
+    // I - B with B = T L^-T = L^-1 A_SS L^-T, symmetrised, stored index-reversed:
+    // M0[i][j] = (I - B)[k-1-i][k-1-j].  Eq. 1's two subtracted terms then combine as
+    // K - k^T W k + k^T W A W k = K - v^T (I - B) v with v = L^-1 k: I - B has its
+    // eigenvalues in [0, 1] and no explicit W = K_SS^-1 enters (the W - W A W form lost
+    // cond(K_SS) eps to cancellation)
     for (int64_t e = tid; e < kk; e += bd) {
       int i = (int)(e / k), j = (int)(e % k);
       double s1 = 0.0, s2 = 0.0;
-      for (int l = 0; l < k; ++l) {
-        s1 = fma(M1[(int64_t)i * k + l], M2[(int64_t)l * k + j], s1);
-        s2 = fma(M1[(int64_t)j * k + l], M2[(int64_t)l * k + i], s2);
-      }
-      double c = M2[e] - 0.5 * (s1 + s2);
-      M0[(int64_t)(k - 1 - i) * k + (k - 1 - j)] = c;
+      for (int l = 0; l <= j; ++l) s1 = fma(M2[(int64_t)i * k + l], M1[(int64_t)j * k + l], s1);
+      for (int l = 0; l <= i; ++l) s2 = fma(M2[(int64_t)j * k + l], M1[(int64_t)i * k + l], s2);
+      M0[(int64_t)(k - 1 - i) * k + (k - 1 - j)] = (i == j ? 1.0 : 0.0) - 0.5 * (s1 + s2);
     }
     __syncthreads();
-    // clamped Cholesky of P C P (in place, lower), tol = 1e-12 max diag
+    // clamped Cholesky of P (I - B) P = R R^T (in place, lower), tol = 1e-12 max diag;
+    // I - B = U U^T with U = P R P upper triangular
     if (tid == 0) {
       double md = 0.0;
       for (int i = 0; i < k; ++i) md = fmax(md, M0[(int64_t)i * k + i]);
@@ -868,7 +895,16 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
       }
     }
     __syncthreads();
-    // G = P R^T P (lower): G[i][j] = R[k-1-j][k-1-i], written as DMMA A-fragments
+    // G = U^T L^-1 (lower): G[i][j] = sum_{p=j..i} U[p][i] L^-1[p][j], U[p][i] = R[k-1-p][k-1-i];
+    // Sigma = K - ||G k||^2, the GP-regression form of the block (G = L^-1 there)
+    for (int64_t e = tid; e < kk; e += bd) {
+      int i = (int)(e / k), j = (int)(e % k);
+      double s = 0.0;
+      for (int pp = j; pp <= i; ++pp) s = fma(M0[(int64_t)(k - 1 - pp) * k + (k - 1 - i)], M1[(int64_t)pp * k + j], s);
+      M2[e] = j <= i ? s : 0.0;
+    }
+    __syncthreads();
+    // G written as DMMA A-fragments
     for (int64_t e = tid; e < LA; e += bd) {
       const int64_t blk = e >> 5;
       const int ln = (int)(e & 31);
@@ -877,7 +913,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
       while ((int64_t)rt * (rt + 1) > blk) --rt;
       const int js = (int)(blk - (int64_t)rt * (rt + 1));
       const int i = 8 * rt + (ln >> 2), j = 4 * js + (ln & 3);
-      out[e] = (i < k && j <= i) ? M0[(int64_t)(k - 1 - j) * k + (k - 1 - i)] : 0.0;
+      out[e] = (i < k && j <= i) ? M2[(int64_t)i * k + j] : 0.0;
     }
   }
 }
@@ -925,8 +961,8 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   o.keep_records = 0;
   o.extreme_iters = 0;
   if (opts) o = *opts;
-  if (o.local_mode != 0 && o.local_mode != 1) return set_err(c, LCP_EINVAL, "fit: bad local_mode");
-  if (o.local_mode == 1 && !(o.beta > 0.0)) return set_err(c, LCP_EINVAL, "fit: beta must be > 0");
+  if (o.local_mode < 0 || o.local_mode > 2) return set_err(c, LCP_EINVAL, "fit: bad local_mode");
+  if (o.local_mode >= 1 && !(o.beta > 0.0 && std::isfinite(o.beta))) return set_err(c, LCP_EINVAL, "fit: beta must be > 0");
   if (o.precision != LCP_FP64 && o.precision != LCP_FP32) return set_err(c, LCP_EINVAL, "fit: bad precision");
   if (o.precision == LCP_FP32 && k > 128) return set_err(c, LCP_EINVAL, "fit: the FP32 posterior needs k <= 128");
   if (o.extreme_iters < 0 || o.extreme_iters > 1000) return set_err(c, LCP_EINVAL, "fit: extreme_iters not in [0, 1000]");
@@ -1044,47 +1080,72 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     CK(cudaGetLastError());
   }
   // a2
-  if (o.local_mode == 1) {
-    if (AM) return set_err(c, LCP_EINVAL, "fit: the box local mode is for observations (lcp_fit_local)");
-    int* cmax = c.knn_fail.as<int>();
-    CK(cudaMemsetAsync(cmax, 0, sizeof(int), c.stream));
-    k_box_sets<<<nbk, 256, 0, c.stream>>>(g, X, m, k, o.beta * kern->lengthscale[0], o.beta * kern->lengthscale[1],
-                                          o.beta * kern->lengthscale[2], c.S.as<int32_t>(), cmax);
-    ++c.n_launch;
-    CK(cudaGetLastError());
-    int hmax = 0;
-    CK(cudaMemcpyAsync(&hmax, cmax, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
-    c.knn_fallbacks = 0;
-    c.max_set = hmax;
-    if (hmax > k)
-      return set_err(c, LCP_EINVAL, "fit: a beta-box holds " + std::to_string(hmax) + " observations > k = " +
-                                        std::to_string(k) + " (raise k or lower beta)");
-  } else {
+  auto knn_sets = [&](int32_t* Sout) -> cudaError_t {
     int r0 = 0;
     double dens = (double)m / nbk;
     while (r0 < 64 && std::pow(2.0 * r0 + 1.0, 3) * dens < (double)k) ++r0;
     size_t smem = sizeof(double) * KNN_CMAX + sizeof(int32_t) * KNN_CMAX + sizeof(int32_t) * (k + 2) +
                   sizeof(double) * (k + 1);
-    CK(cudaFuncSetAttribute(k_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k_knn_brute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaError_t ee;
+    if ((ee = cudaFuncSetAttribute(k_knn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return ee;
+    if ((ee = cudaFuncSetAttribute(k_knn_brute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return ee;
     int* nfail_dev = c.knn_fail.as<int>();
     int* list_dev = nfail_dev + 1;
-    CK(cudaMemsetAsync(nfail_dev, 0, sizeof(int), c.stream));
+    if ((ee = cudaMemsetAsync(nfail_dev, 0, sizeof(int), c.stream)) != cudaSuccess) return ee;
     k_knn<<<nbk, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, c.bstart.as<int64_t>(), c.bcount.as<int64_t>(),
-                                              c.obs_by_bucket.as<int64_t>(), c.S.as<int32_t>(), list_dev,
-                                              nfail_dev, r0);
+                                              c.obs_by_bucket.as<int64_t>(), Sout, list_dev, nfail_dev, r0);
     ++c.n_launch;
-    CK(cudaGetLastError());
+    if ((ee = cudaGetLastError()) != cudaSuccess) return ee;
     int nfail = 0;
-    CK(cudaMemcpyAsync(&nfail, nfail_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    CK(cudaStreamSynchronize(c.stream));
+    if ((ee = cudaMemcpyAsync(&nfail, nfail_dev, sizeof(int), cudaMemcpyDeviceToHost, c.stream)) != cudaSuccess)
+      return ee;
+    if ((ee = cudaStreamSynchronize(c.stream)) != cudaSuccess) return ee;
     c.knn_fallbacks = nfail;
     if (nfail > 0) {
-      k_knn_brute<<<nfail, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, list_dev, c.S.as<int32_t>());
+      k_knn_brute<<<nfail, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, list_dev, Sout);
+      ++c.n_launch;
+      if ((ee = cudaGetLastError()) != cudaSuccess) return ee;
+    }
+    return cudaSuccess;
+  };
+  c.n_capped = 0;
+  if (o.local_mode >= 1) {
+    int32_t* S_knn = nullptr;
+    if (o.local_mode == 2) {   // the |M'| cap: k-NN sets for the buckets whose box overflows
+      CK(c.S_knn.ensure(sizeof(int32_t) * (size_t)nbk * k));
+      S_knn = c.S_knn.as<int32_t>();
+      CK(knn_sets(S_knn));
+    }
+    CK(c.box_cnt.ensure(sizeof(int) * (size_t)nbk));
+    int* cmax = c.knn_fail.as<int>();
+    CK(cudaMemsetAsync(cmax, 0, sizeof(int), c.stream));
+    k_box_sets<<<nbk, 256, 0, c.stream>>>(g, X, m, k, o.beta * kern->lengthscale[0], o.beta * kern->lengthscale[1],
+                                          o.beta * kern->lengthscale[2], c.S.as<int32_t>(), cmax,
+                                          c.box_cnt.as<int>());
+    ++c.n_launch;
+    CK(cudaGetLastError());
+    int hmax = 0;
+    CK(cudaMemcpyAsync(&hmax, cmax, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    if (o.local_mode == 1) c.knn_fallbacks = 0;
+    c.max_set = std::min(hmax, k);
+    if (hmax > k && o.local_mode == 1)
+      return set_err(c, LCP_EINVAL, "fit: a beta-box holds " + std::to_string(hmax) + " observations > k = " +
+                                        std::to_string(k) + " (raise k, lower beta, or use local_mode 2)");
+    if (hmax > k) {
+      k_box_cap<<<nbk, 128, 0, c.stream>>>(c.box_cnt.as<int>(), nbk, k, S_knn, c.S.as<int32_t>());
       ++c.n_launch;
       CK(cudaGetLastError());
+      std::vector<int> hc(nbk);
+      CK(cudaMemcpyAsync(hc.data(), c.box_cnt.p, sizeof(int) * (size_t)nbk, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      for (int v : hc) c.n_capped += v > k;
     }
+  } else {
+    CK(knn_sets(c.S.as<int32_t>()));
   }
   // a3
   if (AM) {

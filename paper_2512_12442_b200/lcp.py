@@ -183,8 +183,10 @@ class Context:
         return self
 
     def fit_sgpr(self, xyz_M, mu_M, A_M, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,
-                 h_full: int = 2, keep_records=False, extreme_iters: int = 0):
-        """NEXT-2: bucket-local Eq. 1 of an SGPR model (inducing points, mean, covariance A_M)."""
+                 h_full: int = 2, keep_records=False, extreme_iters: int = 0, local_mode: int = 0,
+                 beta: float = 6.0):
+        """NEXT-2: bucket-local Eq. 1 of an SGPR model (inducing points, mean, covariance A_M);
+        local sets k-NN (local_mode 0), beta-box (1) or beta-box capped at k (2)."""
         if keep_records is True:
             keep_records = 64
         kind, var, ls, nug, m0 = kernel
@@ -192,7 +194,8 @@ class Context:
         kt = KernelT(int(kind), 0, float(var), (C.c_double * 3)(*ls), float(nug), float(m0))
         lo, hi, cells = grid
         gt = GridT((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int32 * 3)(*cells), 0)
-        ot = OptsT(bucket_log2, h_full, FP64, 0, 1, 3, int(keep_records), int(extreme_iters), 0, 0, 0, 0.0)
+        ot = OptsT(bucket_log2, h_full, FP64, 0, 1, 0, int(keep_records), int(extreme_iters), 0, int(local_mode), 0,
+                   float(beta))
         if isinstance(xyz_M, np.ndarray):
             xyz_M = np.ascontiguousarray(xyz_M, np.float64)
             mu_M = np.ascontiguousarray(mu_M, np.float64)

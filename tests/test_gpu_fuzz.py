@@ -329,17 +329,22 @@ def test_fuzz_sgpr(seed):
     muM = d["m0"] + K @ np.linalg.solve(Ky, d["y"] - d["m0"])
     AM = sn2 * K @ np.linalg.inv(Ky)
     AM = 0.5 * (AM + AM.T)
-    # jitter 1e-6 sigma_f^2 (the usual SGPR value): with 1e-9 the random draws' K_SS reach
-    # cond ~1e12, and C = W - W A_SS W (R1, NEXT-2) then cancels to ~1e-7 sigma_f^2 -- within
-    # the posterior tolerance, but the near-singular 8x8 Sigma makes the MC count diverge
-    jitter = 1e-6 * d["var"]
+    # jitter 1e-9 sigma_f^2: the random draws' K_SS reach cond ~1e10-1e11; both sides evaluate
+    # Eq. 1 whitened (no explicit K_SS^-1), accurate to ~1e-9 sigma_f^2 (test_oracle_sgpr.py)
+    jitter = 1e-9 * d["var"]
     kernel = (d["kind"], d["var"], d["ls"], jitter, d["m0"])
     grid = (d["lo"], d["hi"], d["cells"])
+    # every third draw: the paper's local model -- beta-box sets M' capped at k (R28, R28b)
+    lm, beta = (2, float(np.random.default_rng(seed).uniform(0.3, 3.0))) if seed % 3 == 2 else (0, 6.0)
     ctx = Context(0).fit_sgpr(torch.from_numpy(Xm).to(dev), torch.from_numpy(muM).to(dev),
                               torch.from_numpy(AM).to(dev), kernel, d["k"], grid, bucket_log2=d["b"],
-                              h_full=d["h_full"], keep_records=True)
+                              h_full=d["h_full"], keep_records=True, local_mode=lm, beta=beta)
     M = O.Model.sgpr(O.make_kernel(d["kind"], d["var"], d["ls"], jitter, d["m0"]),
-                     O.make_grid(d["lo"], d["hi"], d["cells"]), Xm, muM, AM, d["k"], d["b"], d["h_full"])
+                     O.make_grid(d["lo"], d["hi"], d["cells"]), Xm, muM, AM, d["k"], d["b"], d["h_full"],
+                     local_mode=lm, beta=beta)
+    if lm:
+        S = ctx.bucket_sets().cpu().numpy()
+        assert all(np.array_equal(S[bb], M.bucket_set(bb)) for bb in range(M.nbuckets))
     th, alpha, md, N = d["thetas"][0], d["alpha"], d["max_depth"], d["N"]
     leaves = ctx.octree_refine(th, alpha, md).clone()
     rec_o, leaves_o = M.octree(th, alpha, md)

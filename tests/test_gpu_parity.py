@@ -815,3 +815,97 @@ def test_sgpr_non_finite_is_einval(dev):
         ctx.fit_sgpr(w.X, muM, AMb, kernel, cfg.k, grid, bucket_log2=cfg.bucket_log2, h_full=cfg.h_full)
     assert e.value.status == LCP_EINVAL
     ctx.fit_sgpr(w.X, muM, AM, kernel, cfg.k, grid, bucket_log2=cfg.bucket_log2, h_full=cfg.h_full)
+
+
+@pytest.mark.parametrize("name,k,beta", [("c2", 24, 1.2), ("t2", 30, 0.9)])
+def test_capped_beta_box_local_mode(name, k, beta, dev):
+    # R28b: beta-box sets with the |M'| cap k (local_mode 2) -- buckets whose box holds more
+    # than k observations take their k-NN set; sets bit-exact, posteriors, node sets, LCP
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate(name)
+    cfg = w.cfg
+    kernel, grid, _, b, hf = config_args(cfg)
+    ctx = Context(0).fit_local(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(np.array(w.y)).to(dev),
+                               kernel, k, grid, bucket_log2=b, h_full=hf, keep_records=True, local_mode=2, beta=beta)
+    kern = O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, cfg.nugget, cfg.prior_mean)
+    M = O.Model.box(kern, O.make_grid(cfg.lo, cfg.hi, cfg.cells), w.X, w.y, k, b, hf, beta, cap=True)
+    st = ctx.stats()
+    assert 0 < st["capped_buckets"] < M.nbuckets, st["capped_buckets"]
+    S = ctx.bucket_sets().cpu().numpy()
+    bad = [bb for bb in range(M.nbuckets) if not np.array_equal(S[bb], M.bucket_set(bb))]
+    assert not bad, bad[:5]
+    cells = random_cells(name, 120, 6)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    for q, cc in enumerate(cells[:60]):
+        mu_o, cov_o = M.cell_posterior(int(cc))
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(cc), em, ec)
+    th = w.thetas[0]
+    leaves_g = ctx.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy()
+    rec_o, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+    res = compare_node_sets(ctx.node_records(), rec_o, cfg.alpha)
+    assert not res["unexcused"], res["unexcused"][:10]
+    sel = leaves_g[:: max(1, len(leaves_g) // 2000)]
+    lcp_g = ctx.pmc_cells(torch.from_numpy(sel).to(dev), th, 800, 7).cpu().numpy()
+    lcp_o = M.pmc_cells(sel, th, 800, 7)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, 800)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+def test_paper_beta6_at_c4_scale(dev):
+    # the paper's beta = 6 at BASELINE c4 scale (m = 2000, k = 64): every
+    # bucket's 6-lengthscale box holds far more than k observations, so the |M'| cap (R28b)
+    # gives every bucket its k-NN set -- the field is the default k-NN field bit for bit
+    from paper_2512_12442_b200 import Context, config_args
+    w = generate("c4")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    X = torch.from_numpy(np.array(w.X)).to(dev)
+    y = torch.from_numpy(np.array(w.y)).to(dev)
+    th = w.thetas[1]
+    ref = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    f_ref, n_ref = ref.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    f_ref = f_ref.clone()
+    box = Context(0).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, local_mode=2, beta=6.0)
+    st = box.stats()
+    assert st["capped_buckets"] == box.info()["nbuckets"]
+    f_box, n_box = box.run_field(th, cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)
+    assert n_box == n_ref and torch.equal(f_box, f_ref)
+
+
+@pytest.mark.parametrize("name,mode,beta,k", [("t2", 1, 0.7, 90), ("c2", 2, 1.2, 24)])
+def test_sgpr_beta_box(name, mode, beta, k, dev):
+    # NEXT-2, the paper's exact model variant: SGPR input (Eq. 1 with A_M) on the beta-box
+    # local sets M' (mode 2: capped at k), jitter 1e-9 sigma_f^2
+    from paper_2512_12442_b200 import Context
+    w, cfg, muM, AM = _sgpr_inputs(name, 20.0)
+    jitter = 1e-9 * cfg.variance
+    kernel = (cfg.kernel, cfg.variance, cfg.lengthscale, jitter, cfg.prior_mean)
+    grid = (cfg.lo, cfg.hi, cfg.cells)
+    ctx = Context(0).fit_sgpr(torch.from_numpy(np.array(w.X)).to(dev), torch.from_numpy(muM).to(dev),
+                              torch.from_numpy(AM).to(dev), kernel, k, grid, bucket_log2=cfg.bucket_log2,
+                              h_full=cfg.h_full, keep_records=True, local_mode=mode, beta=beta)
+    M = O.Model.sgpr(O.make_kernel(cfg.kernel, cfg.variance, cfg.lengthscale, jitter, cfg.prior_mean),
+                     O.make_grid(cfg.lo, cfg.hi, cfg.cells), w.X, muM, AM, k, cfg.bucket_log2, cfg.h_full,
+                     local_mode=mode, beta=beta)
+    S = ctx.bucket_sets().cpu().numpy()
+    assert all(np.array_equal(S[bb], M.bucket_set(bb)) for bb in range(M.nbuckets))
+    if mode == 1:
+        assert (S < 0).any()          # padded (decoupled dummy) slots are exercised
+    cells = random_cells(name, 150, 5)
+    mu_g, cov_g = ctx.cell_posterior(torch.from_numpy(cells).to(dev))
+    for q, c in enumerate(cells):
+        mu_o, cov_o = M.cell_posterior(int(c))
+        em, ec = posterior_close(mu_g[q].cpu().numpy(), mu_o, cov_g[q].cpu().numpy(), cov_o, cfg.variance, 1e-5)
+        assert em <= 1e-5 and ec <= 1e-5, (int(c), em, ec)
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    rec_o, leaves_o = M.octree(th, cfg.alpha, cfg.max_depth)
+    res = compare_node_sets(ctx.node_records(), rec_o, cfg.alpha)
+    assert not res["unexcused"], (res["unexcused"][:10], res)
+    lv = leaves.cpu().numpy()
+    sel = lv[:: max(1, len(lv) // 1500)]
+    lcp_g = ctx.pmc_cells(torch.from_numpy(sel).to(dev), th, 1000, cfg.mc_seed).cpu().numpy()
+    lcp_o = M.pmc_cells(sel, th, 1000, cfg.mc_seed)
+    frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1000)
+    assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)

@@ -89,3 +89,63 @@ def test_local_sgpr_octree_and_pmc_run():
     assert len(leaves) > 0
     lcp = M.pmc_cells(leaves[::50], w.thetas[0], 400, 3)
     assert np.all((lcp >= 0) & (lcp <= 1))
+
+
+def _ld_chol(A):
+    n = len(A)
+    L = np.zeros_like(A)
+    for j in range(n):
+        L[j, j] = np.sqrt(A[j, j] - L[j, :j] @ L[j, :j])
+        L[j + 1:, j] = (A[j + 1:, j] - L[j + 1:, :j] @ L[j, :j]) / L[j, j]
+    return L
+
+
+def _ld_fwd(L, B):
+    X = np.zeros_like(B)
+    for i in range(len(L)):
+        X[i] = (B[i] - L[i, :i] @ X[:i]) / L[i, i]
+    return X
+
+
+def test_sgpr_eq1_accuracy_ill_conditioned():
+    # Eq. 1 on an ill-conditioned SGPR fit (jitter 1e-9 sigma_f^2, cond(K_MM) ~ 1e10-1e11, the
+    # random configuration of the GPU SGPR sweep that broke parity in round 1) against the same
+    # formula in 80-bit extended precision, evaluated two ways (literal K W A W K with the
+    # explicit inverse, and whitened v^T B v) that must agree with each other first.  The
+    # oracle's FP64 posterior is within 2e-8 sigma_f^2 (an explicit-inverse FP64 evaluation
+    # is off by ~4e-7 here).
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    g = np.random.default_rng(10_000 + 281)        # the draw of tests/test_gpu_fuzz.py seed 81
+    lo = g.uniform(-2.0, 1.0, 3)
+    hi = lo + g.uniform(0.4, 3.0, 3)
+    m = 150
+    X = lo + (hi - lo) * g.random((m, 3))
+    y = np.sin(X @ np.array([1.3, -0.7, 0.4])) + 0.01 * g.standard_normal(m)
+    var = 1.4
+    ls = tuple(0.5 * (hi - lo))
+    sn2 = 1e-3
+    jit = 1e-9 * var
+    kern_gp = O.make_kernel(SE, var, ls, sn2, 0.0)
+    muM, AM = _gp_to_sgpr(kern_gp, X, y, sn2)
+    kern = O.make_kernel(SE, var, ls, jit, 0.0)
+    K = np.array([[O.kernel_value(kern, a, b) for b in X] for a in X]) + jit * np.eye(m)
+    assert np.linalg.cond(K) > 1e10
+    Q = lo + (hi - lo) * g.random((6, 3))
+    mu_o, cov_o = O.sgpr_exact(kern, X, muM, AM, Q)
+    LD = np.longdouble
+    KQ = np.array([[O.kernel_value(kern, a, q) for q in Q] for a in X]).astype(LD)
+    KQQ = np.array([[O.kernel_value(kern, a, b) for b in Q] for a in Q]).astype(LD)
+    L = _ld_chol(K.astype(LD))
+    V = _ld_fwd(L, KQ)                                      # L^-1 K_MQ
+    B = _ld_fwd(L, _ld_fwd(L, AM.astype(LD)).T).T           # L^-1 A L^-T
+    ref_w = KQQ - V.T @ V + V.T @ B @ V
+    Linv = _ld_fwd(L, np.eye(m, dtype=LD))
+    W = Linv.T @ Linv
+    P = KQ.T @ W
+    ref_l = KQQ - P @ KQ + P @ AM.astype(LD) @ P.T
+    mu_ref = KQ.T @ (W @ muM.astype(LD))
+    assert float(np.abs(ref_w - ref_l).max()) < 5e-9 * var
+    assert float(np.abs(cov_o - ref_w.astype(float)).max()) < 2e-8 * var
+    assert float(np.abs(mu_o - mu_ref.astype(float)).max()) < 1e-8 * max(1.0, float(np.abs(mu_ref).max()))
