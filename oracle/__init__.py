@@ -319,10 +319,10 @@ class Model:
         f = lib().orc_local_f_grad(self._h, b, np.ascontiguousarray(x, np.float64), theta, g)
         return f, g
 
-    def node_extremes(self, theta, level, i, j, k):
-        out = np.zeros(6)
+    def node_extremes(self, theta, level, i, j, k, starts=False):
+        out = np.zeros(12)
         lib().orc_node_extremes(self._h, theta, level, i, j, k, out)
-        return out
+        return (out[:6], out[6:9], out[9:12]) if starts else out[:6]
 
     def cell_posterior(self, cell):
         mu = np.zeros(8)

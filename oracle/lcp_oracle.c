@@ -837,13 +837,23 @@ static double local_f_grad(const orc_model_t* M, int32_t b, const double* x, dou
 }
 
 /* R26: deterministic bounded search for the extreme of f over the node box,
- * maximising sgn * f from the lattice extreme `av`.  Local model: the node's
- * bucket when the node lies inside one bucket (level >= bucket_log2, the paper's
- * per-node local model), else the start vertex's bucket with the
- * box clipped to that bucket.  Iteration (extreme_iters times): normalised
- * projected-gradient step of length `step` (start: a quarter of the shortest box
- * side); accept if sgn*f increases (step doubles, capped at the longest side),
- * else halve the step; stop when the projected gradient vanishes. */
+ * maximising F = sgn * f from the lattice extreme `av` -- a projected limited-memory
+ * quasi-Newton iteration in the spirit of the paper's L-BFGS-B (R26b):
+ *   local model: the node's bucket when the node lies inside one bucket (level >=
+ *   bucket_log2, the paper's per-node local model), else the start
+ *   vertex's bucket with the box clipped to that bucket;
+ *   direction: the free gradient g~ (components at an active bound that point out of
+ *   the box are 0) times the L-BFGS inverse-Hessian estimate of -F (two-loop recursion
+ *   over the last EXT_MEM pairs s = x+ - x, y = g - g+, kept when s.y > 1e-12 |s| |y|;
+ *   H0 = (s.y / y.y) I), restricted to the free components; a non-ascent direction
+ *   resets the memory and takes g~;
+ *   step: x(t) = clip(x + t d), first t = step0 / |d| without memory (step0 = a quarter
+ *   of the shortest box side), t = 1 with memory, t |d| <= the longest side;
+ *   accept iff F(x(t)) > F and F(x(t)) >= F + 1e-4 g.(x(t) - x) (Armijo), else t /= 2;
+ *   a step below 1e-12 of the longest side resets the memory, or ends the search
+ *   without memory; so does a vanishing free gradient.
+ * extreme_iters counts evaluations of f and grad f (one per trial point). */
+#define EXT_MEM 4
 static double extreme_search(const orc_model_t* M, double theta, int32_t level, const int64_t* base,
                              const int64_t* vmax, const int32_t* av, int sgn, double* f_start) {
     int64_t lo_v[3], hi_v[3];
@@ -870,27 +880,89 @@ static double extreme_search(const orc_model_t* M, double theta, int32_t level, 
         if (w < mn) mn = w;
         if (w > mx) mx = w;
     }
-    double step = 0.25 * mn;
+    const double step0 = 0.25 * mn;
     double F = sgn * local_f_grad(M, b, x, theta, g);
     if (f_start) *f_start = sgn * F;
     for (int d = 0; d < 3; ++d) g[d] *= sgn;
-    for (int it = 0; it < M->extreme_iters; ++it) {
-        for (int d = 0; d < 3; ++d)
-            if ((x[d] <= blo[d] && g[d] < 0.0) || (x[d] >= bhi[d] && g[d] > 0.0)) g[d] = 0.0;
-        double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-        if (!(gn > 0.0)) break;
-        double xn[3], gt[3];
-        for (int d = 0; d < 3; ++d) {
-            double t = x[d] + step * (g[d] / gn);
-            xn[d] = t < blo[d] ? blo[d] : (t > bhi[d] ? bhi[d] : t);
+    double S[EXT_MEM][3], Y[EXT_MEM][3], RHO[EXT_MEM];
+    int nmem = 0;
+    int need_dir = 1, done = 0;
+    double dir[3] = {0, 0, 0}, t = 0.0, dn = 0.0;
+    for (int it = 0; it < M->extreme_iters && !done; ++it) {
+        double xt[3];
+        for (;;) {                     /* find a trial point (no evaluation) */
+            if (need_dir) {
+                double gf[3];
+                for (int d = 0; d < 3; ++d)
+                    gf[d] = ((x[d] <= blo[d] && g[d] < 0.0) || (x[d] >= bhi[d] && g[d] > 0.0)) ? 0.0 : g[d];
+                double gn = sqrt(gf[0] * gf[0] + gf[1] * gf[1] + gf[2] * gf[2]);
+                if (!(gn > 0.0)) { done = 1; break; }
+                /* two-loop recursion on the free gradient (newest pair last) */
+                double q[3] = {gf[0], gf[1], gf[2]}, al[EXT_MEM];
+                for (int i = nmem - 1; i >= 0; --i) {
+                    al[i] = RHO[i] * (S[i][0] * q[0] + S[i][1] * q[1] + S[i][2] * q[2]);
+                    for (int d = 0; d < 3; ++d) q[d] -= al[i] * Y[i][d];
+                }
+                if (nmem > 0) {
+                    const int l = nmem - 1;
+                    double sy = S[l][0] * Y[l][0] + S[l][1] * Y[l][1] + S[l][2] * Y[l][2];
+                    double yy = Y[l][0] * Y[l][0] + Y[l][1] * Y[l][1] + Y[l][2] * Y[l][2];
+                    for (int d = 0; d < 3; ++d) q[d] *= sy / yy;
+                }
+                for (int i = 0; i < nmem; ++i) {
+                    double be = RHO[i] * (Y[i][0] * q[0] + Y[i][1] * q[1] + Y[i][2] * q[2]);
+                    for (int d = 0; d < 3; ++d) q[d] += S[i][d] * (al[i] - be);
+                }
+                for (int d = 0; d < 3; ++d) dir[d] = gf[d] == 0.0 ? 0.0 : q[d];
+                double slope = g[0] * dir[0] + g[1] * dir[1] + g[2] * dir[2];
+                if (!(slope > 0.0)) {      /* not an ascent direction: reset to the gradient */
+                    nmem = 0;
+                    for (int d = 0; d < 3; ++d) dir[d] = gf[d];
+                }
+                dn = sqrt(dir[0] * dir[0] + dir[1] * dir[1] + dir[2] * dir[2]);
+                t = nmem == 0 ? step0 / dn : 1.0;
+                if (t * dn > mx) t = mx / dn;
+                need_dir = 0;
+            }
+            if (t * dn < 1e-12 * mx) {     /* step collapsed */
+                if (nmem > 0) { nmem = 0; need_dir = 1; continue; }
+                done = 1;
+                break;
+            }
+            for (int d = 0; d < 3; ++d) {
+                double v = x[d] + t * dir[d];
+                xt[d] = v < blo[d] ? blo[d] : (v > bhi[d] ? bhi[d] : v);
+            }
+            break;
         }
-        double Fn = sgn * local_f_grad(M, b, xn, theta, gt);
-        if (Fn > F) {
-            F = Fn;
-            for (int d = 0; d < 3; ++d) { x[d] = xn[d]; g[d] = sgn * gt[d]; }
-            step = step * 2.0 < mx ? step * 2.0 : mx;
+        if (done) break;
+        double gt[3];
+        double Ft = sgn * local_f_grad(M, b, xt, theta, gt);
+        for (int d = 0; d < 3; ++d) gt[d] *= sgn;
+        double gdx = g[0] * (xt[0] - x[0]) + g[1] * (xt[1] - x[1]) + g[2] * (xt[2] - x[2]);
+        if (Ft > F && Ft >= F + 1e-4 * gdx) {
+            double sv[3], yv[3];
+            for (int d = 0; d < 3; ++d) { sv[d] = xt[d] - x[d]; yv[d] = g[d] - gt[d]; }
+            double sy = sv[0] * yv[0] + sv[1] * yv[1] + sv[2] * yv[2];
+            double ss = sqrt(sv[0] * sv[0] + sv[1] * sv[1] + sv[2] * sv[2]);
+            double ys = sqrt(yv[0] * yv[0] + yv[1] * yv[1] + yv[2] * yv[2]);
+            if (sy > 1e-12 * ss * ys) {
+                if (nmem == EXT_MEM) {
+                    for (int i = 1; i < EXT_MEM; ++i) {
+                        for (int d = 0; d < 3; ++d) { S[i - 1][d] = S[i][d]; Y[i - 1][d] = Y[i][d]; }
+                        RHO[i - 1] = RHO[i];
+                    }
+                    --nmem;
+                }
+                for (int d = 0; d < 3; ++d) { S[nmem][d] = sv[d]; Y[nmem][d] = yv[d]; }
+                RHO[nmem] = 1.0 / sy;
+                ++nmem;
+            }
+            F = Ft;
+            for (int d = 0; d < 3; ++d) { x[d] = xt[d]; g[d] = gt[d]; }
+            need_dir = 1;
         } else {
-            step *= 0.5;
+            t *= 0.5;
         }
     }
     return sgn * F;
@@ -898,7 +970,8 @@ static double extreme_search(const orc_model_t* M, double theta, int32_t level, 
 
 void orc_model_set_extreme(orc_model_t* M, int32_t iters) { M->extreme_iters = iters > 0 ? iters : 0; }
 
-/* test tap: out = {lattice zmax, lattice zmin, searched zmax, searched zmin, f at the two starts} */
+/* test tap: out = {lattice zmax, lattice zmin, searched zmax, searched zmin, f at the two starts,
+ * start of the max search (3), start of the min search (3)} */
 void orc_node_extremes(const orc_model_t* M, double theta, int32_t level, int32_t i, int32_t j, int32_t k,
                        double* out) {
     int32_t h = M->lfull - level;
@@ -932,6 +1005,8 @@ void orc_node_extremes(const orc_model_t* M, double theta, int32_t level, int32_
     out[1] = zmin;
     out[2] = extreme_search(M, theta, level, base, vmax, amax, +1, &out[4]);
     out[3] = extreme_search(M, theta, level, base, vmax, amin, -1, &out[5]);
+    vertex_pos(M, amax[0], amax[1], amax[2], out + 6);   /* the two search starts */
+    vertex_pos(M, amin[0], amin[1], amin[2], out + 9);
 }
 
 double orc_local_f_grad(const orc_model_t* M, int32_t b, const double* x, double theta, double* grad) {

@@ -5,9 +5,9 @@
 // For nodes coarser than h_full (whose candidate lattice is strided) that need a
 // bound, one warp per node climbs f(x) = (mu(x) - theta) / (sigma(x) sqrt 2) from
 // the lattice argmax (for Q_lo) and descends from the lattice argmin (for Q_hi)
-// over the node box with a deterministic projected-gradient iteration (the
-// iteration DESIGN.md R26 specifies; the CPU oracle implements it
-// independently).  Each evaluation of f and
+// over the node box with a deterministic projected limited-memory quasi-Newton
+// iteration (L-BFGS two-loop direction on the free variables, projected Armijo
+// backtracking; R26/R26b; the CPU oracle implements it independently).  Each evaluation of f and
 // grad f at a point uses the bucket's local GP:
 //   K columns [k_x, d k_x / dx_0, d/dx_1, d/dx_2] for both search points (8 columns),
 //   mu and grad mu = the columns dotted with alpha,
@@ -23,6 +23,8 @@ __device__ __forceinline__ void dmma_x(double a, double b, double& d0, double& d
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+
+constexpr int EXT_MEM = 4;   // L-BFGS memory (pairs s, y) per search
 
 struct ExtArgs {
   KernParams kp;
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(256) k_node_extreme(ExtArgs a, int level, cons
       mn = fmin(mn, w);
       mx = fmax(mx, w);
     }
-    step[s] = 0.25 * mn;
+    step[s] = 0.25 * mn;   // the first step length (no curvature memory yet)
     smax[s] = mx;
   }
   const double sg[2] = {1.0, -1.0};
@@ -213,30 +215,72 @@ __global__ void __launch_bounds__(256) k_node_extreme(ExtArgs a, int level, cons
     f[1] = f1[0];
     for (int d = 0; d < 3; ++d) gf[1][d] = gf1[0][d];
   }
-  bool done[2];
+  // R26b: projected limited-memory quasi-Newton ascent of F = sg f per side (the CPU
+  // oracle implements the same iteration independently)
+  double Sm[2][EXT_MEM][3], Ym[2][EXT_MEM][3], RHO[2][EXT_MEM], dir[2][3], t[2], dn[2];
+  int nmem[2] = {0, 0};
+  bool done[2], need_dir[2] = {true, true};
   for (int s = 0; s < 2; ++s) {
     F[s] = sg[s] * f[s];
     for (int d = 0; d < 3; ++d) gr[s][d] = sg[s] * gf[s][d];
     done[s] = false;
+    t[s] = dn[s] = 0.0;
   }
   for (int it = 0; it < a.iters && !(done[0] && done[1]); ++it) {
     double xn[2][3];
     for (int s = 0; s < 2; ++s) {
-      if (done[s]) {
-        for (int d = 0; d < 3; ++d) xn[s][d] = x[s][d];
-        continue;
-      }
-      for (int d = 0; d < 3; ++d)
-        if ((x[s][d] <= blo[s][d] && gr[s][d] < 0.0) || (x[s][d] >= bhi[s][d] && gr[s][d] > 0.0)) gr[s][d] = 0.0;
-      double gn = sqrt(gr[s][0] * gr[s][0] + gr[s][1] * gr[s][1] + gr[s][2] * gr[s][2]);
-      if (!(gn > 0.0)) {
-        done[s] = true;
-        for (int d = 0; d < 3; ++d) xn[s][d] = x[s][d];
-        continue;
-      }
-      for (int d = 0; d < 3; ++d) {
-        double t = x[s][d] + step[s] * (gr[s][d] / gn);
-        xn[s][d] = t < blo[s][d] ? blo[s][d] : (t > bhi[s][d] ? bhi[s][d] : t);
+      for (int d = 0; d < 3; ++d) xn[s][d] = x[s][d];
+      while (!done[s]) {                 // find a trial point (no evaluation)
+        if (need_dir[s]) {
+          double gfr[3];
+          for (int d = 0; d < 3; ++d)
+            gfr[d] = ((x[s][d] <= blo[s][d] && gr[s][d] < 0.0) || (x[s][d] >= bhi[s][d] && gr[s][d] > 0.0))
+                         ? 0.0 : gr[s][d];
+          const double gn = sqrt(gfr[0] * gfr[0] + gfr[1] * gfr[1] + gfr[2] * gfr[2]);
+          if (!(gn > 0.0)) {
+            done[s] = true;
+            break;
+          }
+          double q[3] = {gfr[0], gfr[1], gfr[2]}, al[EXT_MEM];
+          for (int i = nmem[s] - 1; i >= 0; --i) {
+            al[i] = RHO[s][i] * (Sm[s][i][0] * q[0] + Sm[s][i][1] * q[1] + Sm[s][i][2] * q[2]);
+            for (int d = 0; d < 3; ++d) q[d] -= al[i] * Ym[s][i][d];
+          }
+          if (nmem[s] > 0) {
+            const int l = nmem[s] - 1;
+            const double sy = Sm[s][l][0] * Ym[s][l][0] + Sm[s][l][1] * Ym[s][l][1] + Sm[s][l][2] * Ym[s][l][2];
+            const double yy = Ym[s][l][0] * Ym[s][l][0] + Ym[s][l][1] * Ym[s][l][1] + Ym[s][l][2] * Ym[s][l][2];
+            for (int d = 0; d < 3; ++d) q[d] *= sy / yy;
+          }
+          for (int i = 0; i < nmem[s]; ++i) {
+            const double be = RHO[s][i] * (Ym[s][i][0] * q[0] + Ym[s][i][1] * q[1] + Ym[s][i][2] * q[2]);
+            for (int d = 0; d < 3; ++d) q[d] += Sm[s][i][d] * (al[i] - be);
+          }
+          for (int d = 0; d < 3; ++d) dir[s][d] = gfr[d] == 0.0 ? 0.0 : q[d];
+          const double slope = gr[s][0] * dir[s][0] + gr[s][1] * dir[s][1] + gr[s][2] * dir[s][2];
+          if (!(slope > 0.0)) {          // not an ascent direction: reset to the gradient
+            nmem[s] = 0;
+            for (int d = 0; d < 3; ++d) dir[s][d] = gfr[d];
+          }
+          dn[s] = sqrt(dir[s][0] * dir[s][0] + dir[s][1] * dir[s][1] + dir[s][2] * dir[s][2]);
+          t[s] = nmem[s] == 0 ? step[s] / dn[s] : 1.0;
+          if (t[s] * dn[s] > smax[s]) t[s] = smax[s] / dn[s];
+          need_dir[s] = false;
+        }
+        if (t[s] * dn[s] < 1e-12 * smax[s]) {   // step collapsed
+          if (nmem[s] > 0) {
+            nmem[s] = 0;
+            need_dir[s] = true;
+            continue;
+          }
+          done[s] = true;
+          break;
+        }
+        for (int d = 0; d < 3; ++d) {
+          const double v = x[s][d] + t[s] * dir[s][d];
+          xn[s][d] = v < blo[s][d] ? blo[s][d] : (v > bhi[s][d] ? bhi[s][d] : v);
+        }
+        break;
       }
     }
     if (done[0] && done[1]) break;
@@ -253,16 +297,46 @@ __global__ void __launch_bounds__(256) k_node_extreme(ExtArgs a, int level, cons
     }
     for (int s = 0; s < 2; ++s) {
       if (done[s]) continue;
-      const double Fn = sg[s] * f[s];
-      if (Fn > F[s]) {
-        F[s] = Fn;
+      const double Ft = sg[s] * f[s];
+      double gt[3];
+      for (int d = 0; d < 3; ++d) gt[d] = sg[s] * gf[s][d];
+      const double gdx =
+          gr[s][0] * (xn[s][0] - x[s][0]) + gr[s][1] * (xn[s][1] - x[s][1]) + gr[s][2] * (xn[s][2] - x[s][2]);
+      if (Ft > F[s] && Ft >= F[s] + 1e-4 * gdx) {
+        double sv[3], yv[3];
+        for (int d = 0; d < 3; ++d) {
+          sv[d] = xn[s][d] - x[s][d];
+          yv[d] = gr[s][d] - gt[d];
+        }
+        const double sy = sv[0] * yv[0] + sv[1] * yv[1] + sv[2] * yv[2];
+        const double ss = sqrt(sv[0] * sv[0] + sv[1] * sv[1] + sv[2] * sv[2]);
+        const double ys = sqrt(yv[0] * yv[0] + yv[1] * yv[1] + yv[2] * yv[2]);
+        if (sy > 1e-12 * ss * ys) {
+          if (nmem[s] == EXT_MEM) {
+            for (int i = 1; i < EXT_MEM; ++i) {
+              for (int d = 0; d < 3; ++d) {
+                Sm[s][i - 1][d] = Sm[s][i][d];
+                Ym[s][i - 1][d] = Ym[s][i][d];
+              }
+              RHO[s][i - 1] = RHO[s][i];
+            }
+            --nmem[s];
+          }
+          for (int d = 0; d < 3; ++d) {
+            Sm[s][nmem[s]][d] = sv[d];
+            Ym[s][nmem[s]][d] = yv[d];
+          }
+          RHO[s][nmem[s]] = 1.0 / sy;
+          ++nmem[s];
+        }
+        F[s] = Ft;
         for (int d = 0; d < 3; ++d) {
           x[s][d] = xn[s][d];
-          gr[s][d] = sg[s] * gf[s][d];
+          gr[s][d] = gt[d];
         }
-        step[s] = step[s] * 2.0 < smax[s] ? step[s] * 2.0 : smax[s];
+        need_dir[s] = true;
       } else {
-        step[s] *= 0.5;
+        t[s] *= 0.5;
       }
     }
   }
