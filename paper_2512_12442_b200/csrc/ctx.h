@@ -3,8 +3,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include "common.cuh"
 #include "lcp.h"
@@ -49,6 +52,20 @@ struct DevBuf {
   }
   template <typename T>
   T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// host-side trace range (NVTX) around a phase of a call: visible in Nsight Systems / ncu
+// --nvtx timelines; a no-op unless a profiler is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int v) {
+    char b[64];
+    std::snprintf(b, sizeof b, fmt, v);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 constexpr int64_t BRICK_PASS_CHUNK = (int64_t)1 << 17;   // bricks per brick-pass launch (8.4 M cells)

@@ -939,6 +939,7 @@ static double host_kern(const KernParams& p, const double* a, const double* b) {
 lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, int on_device,
                       const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts,
                       const double* AM) {
+  NvtxRange nvtx_("lcp_fit");
   if (!xyz || !yv || !kern || !grid) return set_err(c, LCP_EINVAL, "fit: null argument");
   if (m < 1 || k < 1 || (int64_t)k > m) return set_err(c, LCP_EINVAL, "fit: need 1 <= k <= m");
   if (k > 1024 && (int64_t)k != m) return set_err(c, LCP_EINVAL, "fit: k > 1024 requires k == m");

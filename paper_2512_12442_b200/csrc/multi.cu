@@ -104,6 +104,7 @@ cudaError_t launch_scatter(Ctx& c, const int64_t* cells, const float* lcp, int64
 lcp_status_t run_field_multi_impl(Ctx& c, const double* thetas, int T, double alpha, int max_depth, int64_t N,
                                   uint64_t seed, uint32_t stream, float* fields, int64_t* n_leaf_out,
                                   int64_t* n_union_out) {
+  NvtxRange nvtx_("lcp_run_field_multi (T = %d)", T);
   if (!c.fitted) return set_err(c, LCP_ESTATE, "run_field_multi before fit");
   if (T < 1 || T > 16) return set_err(c, LCP_EINVAL, "run_field_multi: need 1 <= n_iso <= 16");
   cudaError_t e;

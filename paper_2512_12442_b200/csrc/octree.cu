@@ -455,6 +455,7 @@ std::vector<int> slab_cuts(const std::vector<int64_t>& w, int count) {
 }
 
 lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
+  NvtxRange nvtx_("lcp_octree_refine");
   if (!c.fitted) return set_err(c, LCP_ESTATE, "refine before fit");
   if (!(alpha > 0.0 && alpha < 0.5)) return set_err(c, LCP_EINVAL, "refine: threshold must be in (0, 0.5)");
   if (max_depth < 0 || max_depth > c.g.lfull) return set_err(c, LCP_EINVAL, "refine: max_depth not in [0, Lfull]");
@@ -520,6 +521,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     CK(cudaMemsetAsync(c.level_field, 0xFF, (size_t)g.cells[0] * g.cells[1] * g.cells[2], c.stream));
   bool early_bricks = false;
   for (int level = 0; level <= max_depth && nF > 0; ++level) {
+    NvtxRange nvtx_l("octree level %d", level);
     int h = g.lfull - level;
     CK(c.ncase.ensure(nF));
     CK(c.nref.ensure(nF));
@@ -543,6 +545,7 @@ lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth) {
     // records of all their cells (a7-a8), reused by every later leaf pass.  Bricks done
     // earlier in this fit are skipped inside the kernel.
     auto brick_pass = [&](const uint64_t* keys, int64_t nk) -> cudaError_t {
+      NvtxRange nvtx_b("brick pass");
       cudaEvent_t b0, b1;
       cudaEventCreate(&b0);
       cudaEventCreate(&b1);

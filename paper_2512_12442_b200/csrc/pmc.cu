@@ -557,6 +557,7 @@ __global__ void k_scatter(const int64_t* __restrict__ cells, const float* __rest
 // posterior of n cells (device list) into post (n x 44 doubles); groups by
 // bucket unless the list already comes in long same-bucket runs.
 lcp_status_t posterior_impl(Ctx& c, const int64_t* cells, int64_t n, double* post) {
+  NvtxRange nvtx_("leaf posterior");
   cudaError_t e;
 #define CK(x)                                        \
   do {                                               \
@@ -618,6 +619,7 @@ static void launch_pmc(Ctx& c, unsigned grid, const int64_t* cells, const double
 lcp_status_t pmc_multi_impl(Ctx& c, const int64_t* cells, int64_t n, const double* thetas, int T,
                             const uint32_t* mask, int64_t N, uint64_t seed, uint32_t iso, float* out,
                             int64_t stride) {
+  NvtxRange nvtx_("lcp_pmc (T isovalues = %d)", T);
   if (!c.fitted) return set_err(c, LCP_ESTATE, "pmc before fit");
   if (N < 1 || N > ((int64_t)1 << 31)) return set_err(c, LCP_EINVAL, "pmc: need 1 <= n_samples <= 2^31");
   if (n < 0) return set_err(c, LCP_EINVAL, "pmc: negative cell count");
