@@ -18,6 +18,10 @@
 
 namespace lcp {
 
+#ifndef PMC_ABS_LG2
+#define PMC_ABS_LG2 1
+#endif
+
 // The constant -sqrt(2 ln 2) of Box-Muller's R = sqrt(-2 ln 2 lg2(u_a)) (and its sign)
 // is carried by L' (chol8.cuh stores FOLD_SCALE L), so k_pmc draws z / FOLD_SCALE.
 constexpr int64_t PMC_CHUNK = (int64_t)1 << 23;   // cells per posterior/MC chunk (2.9 GB of records)
@@ -221,7 +225,13 @@ __device__ __forceinline__ f2_t fmul2(f2_t a, f2_t b) {
 __device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb, uint32_t one) {
   float ua = u23(ra, one);
   float fb = __uint_as_float(mant1(rb, one));
+#if PMC_ABS_LG2
+  // |lg2 u| (u < 1, so -lg2 u except where the approximation strays above 0 by ~2^-22):
+  // the absolute value is a free MUFU operand modifier, where max(-lg2 u, 0) costs an FMNMX
+  float r = sqrt_approx(fabsf(lg2_approx(ua)));
+#else
   float r = sqrt_approx(fmaxf(-lg2_approx(ua), 0.0f));
+#endif
   float s, co;
   __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
   return fmul2(pk(co, s), pk(r, r));
