@@ -29,12 +29,12 @@ sys.path.insert(0, ROOT)
 METRIC = "PMC LCP cells/sec"
 UNIT = "cells/s"
 # minimal op mix of the two-phase k_pmc, in issue slots (lane-ops):
-#   phase 1, every sample : Philox4x32-10 40, 2 Box-Muller pairs 22 (8 MUFU),
-#                           partial L z 26 FFMA, bounds 8, min/max 12, decision 5, queue 3  = 116
-#   phase 2, queued sample: Philox 40, 2 Box-Muller pairs 22, 10 FFMA, min/max 6,
-#                           decision 3, queue store + load 14                              =  95
-OPS_PHASE1 = 116
-OPS_PHASE2 = 95
+#   phase 1, every sample : Philox4x32-10 40, 2 Box-Muller pairs 20 (8 MUFU),
+#                           partial L z 26 FFMA, bounds 8, min/max 12, decision 5, queue 3  = 114
+#   phase 2, queued sample: Philox 40, 2 Box-Muller pairs 20, 10 FFMA, min/max 6,
+#                           decision 3, queue store + load 14                              =  93
+OPS_PHASE1 = 114
+OPS_PHASE2 = 93
 # SURVEY.md §8(d) per-unit figure of the leaf MC ("minimal op mix", fixed before any kernel):
 # 170-210 CUDA-core issue slots + 16 MUFU per sample; the lower end, 186, is used, and each
 # further isovalue of a fused multi-isovalue pass adds the crossing-test row (21 slots).
@@ -492,8 +492,8 @@ def run_ours(args):
                 "ops_per_sample": ops_survey / samples_step if samples_step else None,
                 "ops_note": ("achieved = samples x SURVEY.md 8(d) minimal op mix (186 issue slots per "
                              "sample, +21 per extra fused isovalue) / summed k_pmc time; the two-phase "
-                             "kernel executes fewer: frac_impl_mix uses its own fixed mix (116 per "
-                             "sample + 95 per phase-2 sample)"),
+                             "kernel executes fewer: frac_impl_mix uses its own fixed mix (114 per "
+                             "sample + 93 per phase-2 sample)"),
                 "frac_impl_mix": (impl_mix / peak) if impl_mix else None,
                 "impl_ops_per_sample": ops_step / samples_step if samples_step else None,
                 "phase2_fraction": p2_step / samples_step if samples_step else None,
