@@ -34,7 +34,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 8), ("c4", 2), ("c4", 8)])
+@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 8), ("c4", 2), ("c4", 8), ("c5", 8)])
 def test_torchrun_gather_equals_single_gpu(name, world, tmp_path):
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
@@ -55,7 +55,8 @@ def test_torchrun_gather_equals_single_gpu(name, world, tmp_path):
     # slab-local record tables, used by every rank's leaf pass
     if res["records_used_n1"]:
         assert all(res["records_used_per_rank"]), res["records_used_per_rank"]
-        assert max(res["record_cells_per_rank"]) < (1 << (3 * 8)) if name == "c4" else True
+        lf = {"c2": 6, "c4": 8, "c5": 9}[name]
+        assert max(res["record_cells_per_rank"]) < (1 << (3 * lf))   # slab-local: below the whole cube
 
 
 @pytest.mark.parametrize("name,G", [("p1", 4), ("c3", 3), ("t2", 2)])

@@ -58,6 +58,22 @@ def main():
     y = torch.from_numpy(np.array(w.y)).to(dev)
     ncell = int(np.prod(cfg.cells))
     T = len(w.thetas)
+    # the single-GPU reference first (rank 0), kept on the host, its context freed before the
+    # slab contexts are built: all ranks may share one device
+    ref, nl_ref, full_records = None, None, None
+    if rank == 0:
+        ref_ctx = Context(local).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
+        if T > 1:
+            r_, nl_r, _ = ref_ctx.run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, N, cfg.mc_seed, 0)
+            nl_ref = [int(v) for v in nl_r]
+        else:
+            r_, n_r = ref_ctx.run_field(w.thetas[0], cfg.alpha, cfg.max_depth, N, cfg.mc_seed)
+            r_, nl_ref = r_.view(1, -1), [int(n_r)]
+        ref = r_.cpu()
+        full_records = ref_ctx.stats()["pmc_used_records"]
+        del r_, ref_ctx
+        torch.cuda.empty_cache()
+    dist.barrier()
     ctx = Context(local).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=rank,
                                    slab_count=world)
     if T > 1:
@@ -76,17 +92,10 @@ def main():
     gathered = [None] * world if rank == 0 else None
     dist.gather_object(info, gathered, dst=0)
     if rank == 0:
-        ref_ctx = Context(local).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf)
-        if T > 1:
-            ref, nl_ref, _ = ref_ctx.run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, N, cfg.mc_seed, 0)
-            nl_ref = [int(v) for v in nl_ref]
-        else:
-            r, n = ref_ctx.run_field(w.thetas[0], cfg.alpha, cfg.max_depth, N, cfg.mc_seed)
-            ref, nl_ref = r.view(1, -1), [int(n)]
-        full_records = ref_ctx.stats()
+        got = fields.cpu()
         res = {"workload": args.workload, "world": world, "backend": backend, "gpus": ngpu,
-               "bitexact": bool(torch.equal(fields, ref)),
-               "max_abs_diff": float((fields - ref).abs().max()),
+               "bitexact": bool(torch.equal(got, ref)),
+               "max_abs_diff": float((got - ref).abs().max()),
                "leaves_n1": nl_ref, "leaves_per_rank": [g["leaves"] for g in gathered],
                "leaves_sum": [int(sum(g["leaves"][t] for g in gathered)) for t in range(T)],
                "layer_cuts": [g["slab"]["layer_cuts"] for g in gathered],
@@ -94,7 +103,7 @@ def main():
                "weights": gathered[0]["slab"]["weights"],
                "record_cells_per_rank": [g["slab"]["record_cells"] for g in gathered],
                "records_used_per_rank": [g["pmc_used_records"] for g in gathered],
-               "records_used_n1": full_records["pmc_used_records"], "ncell": ncell}
+               "records_used_n1": full_records, "ncell": ncell}
         json.dump(res, open(args.out, "w"))
         print(json.dumps(res))
     dist.barrier()
