@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-fit-shard", action="store_true",
+                    help="N > 1: every rank fits every bucket (default: factors sharded and all-gathered)")
     ap.add_argument("--extreme", type=int, default=0,
                     help="NEXT-1: continuous extreme-search iterations at coarse octree nodes (0 = lattice)")
     ap.add_argument("--separate-iso", action="store_true",
@@ -291,7 +293,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2512_12442_b200 import Context, config_args
-    from paper_2512_12442_b200.dist import cell_ranges, equal_z_cuts, gather_fields, plan_z_cuts
+    from paper_2512_12442_b200.dist import cell_ranges, equal_z_cuts, fit_sharded, gather_fields, plan_z_cuts
     from workloads import generate
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -349,11 +351,13 @@ def run_ours(args):
         k_pmc ms, phase-2 samples, leaf cells of the union of isovalues).  host = (X, y, field)
         numpy arrays in pinned memory: the e2e leg, inputs and the output field through the
         C ABI's host-pointer paths (at N > 1 the gathered field is read back on rank 0)."""
-        if host is None:
-            ctx.fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, extreme_iters=args.extreme, **slab)
+        xin, yin = (X, y) if host is None else (host[0], host[1])
+        if world > 1 and not args.no_fit_shard:
+            # the bucket factors split across the ranks and all-gathered in place (NCCL)
+            fit_sharded(ctx, xin, yin, kernel, k, grid, rank, world, bucket_log2=b, h_full=hf,
+                        extreme_iters=args.extreme)
         else:
-            ctx.fit_local(host[0], host[1], kernel, k, grid, bucket_log2=b, h_full=hf,
-                          extreme_iters=args.extreme, **slab)
+            ctx.fit_local(xin, yin, kernel, k, grid, bucket_log2=b, h_full=hf, extreme_iters=args.extreme, **slab)
         abi_host_out = host is not None and world == 1
         leaves = 0
         mc_ms = 0.0

@@ -92,8 +92,11 @@ typedef struct {
                               (EINVAL otherwise), padded to k internally; 2 = as 1, with the
                               |M'| cap k: a bucket whose box holds more than k takes its k-NN
                               set instead (R28b; lcp_stats_json "capped_buckets") */
-    int32_t pad1_;
-    double beta;           /* local_mode 1: box enlargement in lengthscales (the paper uses 6) */
+    int32_t fit_shard;     /* with slab_count > 1: 1 = this rank computes the local sets and
+                              factors of its 1/slab_count share of the buckets only; the caller
+                              all-gathers the blocks (lcp_fit_shard_buffers) and calls
+                              lcp_fit_finish; 0 = every rank fits every bucket */
+    double beta;           /* local_mode 1, 2: box enlargement in lengthscales (the paper uses 6) */
 } lcp_opts_t;
 
 /* per evaluated octree node (Alg. 1) */
@@ -269,6 +272,19 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap);
 
 /* wait for all work queued on the ctx stream; reports deferred device errors */
 lcp_status_t lcp_synchronize(lcp_ctx_t* ctx);
+
+/* Sharded fit (opts->fit_shard = 1, slab_count > 1): after lcp_fit_local /
+ * lcp_fit_sgpr returned, the ctx holds the bucket blocks and local sets of its share
+ * only.  Buckets are split by index: rank r owns [r per, (r+1) per) of the range padded
+ * to slab_count x per.  bdata_dev / sets_dev (ctx-owned device arrays of slab_count x
+ * chunk bytes; rank r's chunk at r x chunk) are to be all-gathered in place by the
+ * caller (e.g. NCCL allgather with sendbuff = recvbuff + rank x chunk); then
+ * lcp_fit_finish computes the observation marginals (a4) and completes the fit.
+ * Every other call returns ESTATE in between.  The fitted model is the one an
+ * unsharded fit builds, bit for bit (per-bucket arithmetic does not depend on the split). */
+lcp_status_t lcp_fit_shard_buffers(lcp_ctx_t* ctx, void** bdata_dev, int64_t* bdata_chunk_bytes,
+                                   void** sets_dev, int64_t* sets_chunk_bytes);
+lcp_status_t lcp_fit_finish(lcp_ctx_t* ctx);
 
 /* ---- z-slab decomposition across GPUs (the paper itself is
  * single-process).  Host-only arithmetic, no device work, no ctx:

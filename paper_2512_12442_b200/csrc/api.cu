@@ -450,6 +450,24 @@ lcp_status_t lcp_stats_json(lcp_ctx_t* ctx, char* buf, size_t cap) {
   return LCP_OK;
 }
 
+lcp_status_t lcp_fit_shard_buffers(lcp_ctx_t* ctx, void** bdata_dev, int64_t* bdata_chunk_bytes, void** sets_dev,
+                                   int64_t* sets_chunk_bytes) {
+  CTX_GUARD(ctx);
+  if (!bdata_dev || !bdata_chunk_bytes || !sets_dev || !sets_chunk_bytes) return LCP_EINVAL;
+  if (!c.fit_pending) return set_err(c, LCP_ESTATE, "fit_shard_buffers: no sharded fit pending");
+  *bdata_dev = c.bdata.p;
+  *bdata_chunk_bytes = (int64_t)sizeof(double) * c.bstride * c.shard_per;
+  *sets_dev = c.S.p;
+  *sets_chunk_bytes = (int64_t)sizeof(int32_t) * c.k * c.shard_per;
+  return LCP_OK;
+}
+
+lcp_status_t lcp_fit_finish(lcp_ctx_t* ctx) {
+  CTX_GUARD(ctx);
+  if (!c.fit_pending) return set_err(c, LCP_ESTATE, "fit_finish: no sharded fit pending");
+  return fit_finish_impl(c);
+}
+
 int32_t lcp_slab_auto_level(const lcp_grid_t* grid, int32_t slab_count, int32_t max_depth) {
   if (!grid || slab_count < 1 || max_depth < 0) return -1;
   lcp::Geom g{};

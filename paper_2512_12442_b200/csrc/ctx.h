@@ -84,6 +84,8 @@ struct Ctx {
 
   // model (after fit)
   bool fitted = false;
+  bool fit_pending = false;  // sharded fit: bucket blocks of the other ranks not exchanged yet
+  int shard_per = 0;         // sharded fit: buckets per rank (the last rank's range padded)
   KernParams kp{};
   Geom g{};
   lcp_kernel_t kern{};
@@ -181,6 +183,7 @@ cudaError_t group_by_key(Ctx& c, const int32_t* key_of_item, int64_t n, int64_t 
 lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* y, int64_t m, int on_device,
                       const lcp_kernel_t* kern, int k, const lcp_grid_t* grid, const lcp_opts_t* opts,
                       const double* AM = nullptr);
+lcp_status_t fit_finish_impl(Ctx& c);
 lcp_status_t refine_impl(Ctx& c, double theta, double alpha, int max_depth);
 lcp_status_t pmc_impl(Ctx& c, const int64_t* cells_dev, int64_t n, double theta, int64_t N,
                       uint64_t seed, uint32_t iso, float* out_dev);

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn(KernParams kp, Geom g, cons
                                                      const int64_t* __restrict__ bcount,
                                                      const int64_t* __restrict__ obs_by_bucket,
                                                      int32_t* __restrict__ S, int* __restrict__ fail_list,
-                                                     int* __restrict__ n_fail, int r0) {
+                                                     int* __restrict__ n_fail, int r0, int b0) {
   extern __shared__ unsigned char sm_raw[];
   double* cd2 = reinterpret_cast<double*>(sm_raw);
   int32_t* cidx = reinterpret_cast<int32_t*>(cd2 + KNN_CMAX);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn(KernParams kp, Geom g, cons
   __shared__ long long s_red[32];
   __shared__ int s_n;
   __shared__ double s_d2k;
-  const int b = blockIdx.x;
+  const int b = b0 + blockIdx.x;
   int32_t* Sb = S + (int64_t)b * k;
   if ((int64_t)k >= m) {
     for (int a = threadIdx.x; a < k; a += blockDim.x) Sb[a] = a;
@@ -263,10 +263,10 @@ __global__ void __launch_bounds__(KNN_THREADS) k_knn_brute(KernParams kp, Geom g
 // Bounds left to right without FMA, as the oracle's.  cnt_max: the largest set.
 __global__ void __launch_bounds__(256) k_box_sets(Geom g, const double* __restrict__ X, int64_t m, int k,
                                                   double bl0, double bl1, double bl2, int32_t* __restrict__ S,
-                                                  int* __restrict__ cnt_max, int* __restrict__ cnt) {
+                                                  int* __restrict__ cnt_max, int* __restrict__ cnt, int b0) {
   __shared__ int s_base;
   __shared__ int s_wcnt[8];
-  const int b = blockIdx.x;
+  const int b = b0 + blockIdx.x;
   const int bi[3] = {b % g.nb[0], (b / g.nb[0]) % g.nb[1], b / (g.nb[0] * g.nb[1])};
   const double bw[3] = {bl0, bl1, bl2};
   double lo[3], hi[3];
@@ -310,8 +310,8 @@ __global__ void __launch_bounds__(256) k_box_sets(Geom g, const double* __restri
 // R28b (local_mode 2, the |M'| cap): a bucket whose beta-box holds more than k
 // observations takes its k-NN set (R2) instead
 __global__ void k_box_cap(const int* __restrict__ cnt, int nbuckets, int k, const int32_t* __restrict__ S_knn,
-                          int32_t* __restrict__ S) {
-  const int b = blockIdx.x;
+                          int32_t* __restrict__ S, int b0) {
+  const int b = b0 + blockIdx.x;
   if (b >= nbuckets || cnt[b] <= k) return;
   for (int a = threadIdx.x; a < k; a += blockDim.x) S[(int64_t)b * k + a] = S_knn[(int64_t)b * k + a];
 }
@@ -331,11 +331,11 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor(KernParams kp, i
                                                                 const int32_t* __restrict__ S,
                                                                 double* __restrict__ bdata, int64_t bstride,
                                                                 double* __restrict__ gscratch,
-                                                                int* __restrict__ derr) {
+                                                                int* __restrict__ derr, int b0) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
   __shared__ double s_piv;
-  const int b = blockIdx.x;
+  const int b = b0 + blockIdx.x;
   const int tid = threadIdx.x, bd = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = bd >> 5;
   const int64_t tri = tri_size(k);
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(FACT_THREADS, MINB) k_bucket_factor_blk(KernPa
                                                                     const int32_t* __restrict__ S,
                                                                     double* __restrict__ bdata, int64_t bstride,
                                                                     double* __restrict__ gscratch,
-                                                                    int* __restrict__ derr) {
+                                                                    int* __restrict__ derr, int b0) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(FACT_THREADS, MINB) k_bucket_factor_blk(KernPa
   double* Srow = sT + nb * FB * 12;      // nb blocks of 8 x 12: S_J of the inverse's block row
   double* A = GMEM ? gscratch + (int64_t)blockIdx.x * KP * ST : Srow + nb * FB * 12;   // KP x ST
   const int lr = lane >> 2, lc = lane & 3;
-  for (int b = blockIdx.x; b < nbk; b += gridDim.x) {
+  for (int b = b0 + blockIdx.x; b < nbk; b += gridDim.x) {   // buckets [b0, nbk)
   __syncthreads();
   const int32_t* Sb = S + (int64_t)b * k;
   double* out = bdata + (int64_t)b * bstride;
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
                                                                      const int32_t* __restrict__ S,
                                                                      double* __restrict__ bdata, int64_t bstride,
                                                                      double* __restrict__ scratch, int nbuckets,
-                                                                     int* __restrict__ derr) {
+                                                                     int* __restrict__ derr, int b0) {
   extern __shared__ double sm[];
   __shared__ int s_ok;
   __shared__ double s_piv;
@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(FACT_THREADS) k_bucket_factor_sgpr(KernParams 
   double* sz = sy + k;
   double* rr = sz + k;
   const int64_t LA = la_size(k);
-  for (int b = blockIdx.x; b < nbuckets; b += gridDim.x) {
+  for (int b = b0 + blockIdx.x; b < nbuckets; b += gridDim.x) {   // buckets [b0, nbuckets)
     const int32_t* Sb = S + (int64_t)b * k;
     double* out = bdata + (int64_t)b * bstride;
     __syncthreads();
@@ -1037,8 +1037,19 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   CK(c.obs_by_bucket.ensure(sizeof(int64_t) * m));
   CK(c.bcount.ensure(sizeof(int64_t) * nbk));
   CK(c.bstart.ensure(sizeof(int64_t) * nbk));
-  CK(c.S.ensure(sizeof(int32_t) * (size_t)nbk * k));
-  CK(c.bdata.ensure(sizeof(double) * (size_t)nbk * c.bstride));
+  // sharded fit (opts.fit_shard with slab_count > 1): this rank computes the k-NN sets and
+  // factors of buckets [b0, b1) only -- an equal split of the bucket index range padded to
+  // nbp = slab_count x per buckets -- and the caller all-gathers the blocks in place
+  // (lcp_fit_shard_buffers) before lcp_fit_finish
+  const bool shard = o.fit_shard != 0 && o.slab_count > 1;
+  const int per = shard ? (nbk + o.slab_count - 1) / o.slab_count : nbk;
+  const int nbp = shard ? per * o.slab_count : nbk;
+  const int b0 = shard ? std::min(nbk, o.slab_rank * per) : 0;
+  const int b1 = shard ? std::min(nbk, b0 + per) : nbk;
+  c.shard_per = per;
+  c.fit_pending = false;
+  CK(c.S.ensure(sizeof(int32_t) * (size_t)nbp * k));
+  CK(c.bdata.ensure(sizeof(double) * (size_t)nbp * c.bstride));
   CK(c.obs_mu.ensure(sizeof(double) * m));
   CK(c.obs_sd.ensure(sizeof(double) * m));
   CK(c.derr.ensure(sizeof(int) * 4));
@@ -1096,8 +1107,9 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     int* nfail_dev = c.knn_fail.as<int>();
     int* list_dev = nfail_dev + 1;
     if ((ee = cudaMemsetAsync(nfail_dev, 0, sizeof(int), c.stream)) != cudaSuccess) return ee;
-    k_knn<<<nbk, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, c.bstart.as<int64_t>(), c.bcount.as<int64_t>(),
-                                              c.obs_by_bucket.as<int64_t>(), Sout, list_dev, nfail_dev, r0);
+    if (b1 <= b0) return cudaSuccess;
+    k_knn<<<b1 - b0, KNN_THREADS, smem, c.stream>>>(kp, g, X, m, k, c.bstart.as<int64_t>(), c.bcount.as<int64_t>(),
+                                                  c.obs_by_bucket.as<int64_t>(), Sout, list_dev, nfail_dev, r0, b0);
     ++c.n_launch;
     if ((ee = cudaGetLastError()) != cudaSuccess) return ee;
     int nfail = 0;
@@ -1123,10 +1135,12 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     CK(c.box_cnt.ensure(sizeof(int) * (size_t)nbk));
     int* cmax = c.knn_fail.as<int>();
     CK(cudaMemsetAsync(cmax, 0, sizeof(int), c.stream));
-    k_box_sets<<<nbk, 256, 0, c.stream>>>(g, X, m, k, o.beta * kern->lengthscale[0], o.beta * kern->lengthscale[1],
-                                          o.beta * kern->lengthscale[2], c.S.as<int32_t>(), cmax,
-                                          c.box_cnt.as<int>());
-    ++c.n_launch;
+    if (b1 > b0) {
+      k_box_sets<<<b1 - b0, 256, 0, c.stream>>>(g, X, m, k, o.beta * kern->lengthscale[0],
+                                                o.beta * kern->lengthscale[1], o.beta * kern->lengthscale[2],
+                                                c.S.as<int32_t>(), cmax, c.box_cnt.as<int>(), b0);
+      ++c.n_launch;
+    }
     CK(cudaGetLastError());
     int hmax = 0;
     CK(cudaMemcpyAsync(&hmax, cmax, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -1136,12 +1150,13 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     if (hmax > k && o.local_mode == 1)
       return set_err(c, LCP_EINVAL, "fit: a beta-box holds " + std::to_string(hmax) + " observations > k = " +
                                         std::to_string(k) + " (raise k, lower beta, or use local_mode 2)");
-    if (hmax > k) {
-      k_box_cap<<<nbk, 128, 0, c.stream>>>(c.box_cnt.as<int>(), nbk, k, S_knn, c.S.as<int32_t>());
+    if (hmax > k && b1 > b0) {
+      k_box_cap<<<b1 - b0, 128, 0, c.stream>>>(c.box_cnt.as<int>(), nbk, k, S_knn, c.S.as<int32_t>(), b0);
       ++c.n_launch;
       CK(cudaGetLastError());
-      std::vector<int> hc(nbk);
-      CK(cudaMemcpyAsync(hc.data(), c.box_cnt.p, sizeof(int) * (size_t)nbk, cudaMemcpyDeviceToHost, c.stream));
+      std::vector<int> hc(b1 - b0);
+      CK(cudaMemcpyAsync(hc.data(), c.box_cnt.as<int>() + b0, sizeof(int) * (size_t)(b1 - b0),
+                         cudaMemcpyDeviceToHost, c.stream));
       CK(cudaStreamSynchronize(c.stream));
       for (int v : hc) c.n_capped += v > k;
     }
@@ -1157,14 +1172,16 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
     k_check_finite<<<std::min<int64_t>(((int64_t)m * m + 255) / 256, 4 * (int64_t)c.sm_count * 8), 256, 0,
                      c.stream>>>(c.sgpr_A.as<double>(), (int64_t)m * m, c.derr.as<int>());
     ++c.n_launch;
-    int grid_f = std::min(nbk, c.sm_count * 2);
+    int grid_f = std::max(1, std::min(b1 - b0, c.sm_count * 2));
     CK(c.fscratch.ensure(sizeof(double) * 5 * (size_t)k * k * grid_f));
     size_t smem = sizeof(double) * 4 * (size_t)k;
-    k_bucket_factor_sgpr<<<grid_f, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.sgpr_A.as<double>(),
-                                                                   m, c.S.as<int32_t>(), c.bdata.as<double>(),
-                                                                   c.bstride, c.fscratch.as<double>(), nbk,
-                                                                   c.derr.as<int>());
-    ++c.n_launch;
+    if (b1 > b0) {
+      k_bucket_factor_sgpr<<<grid_f, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(),
+                                                                     c.sgpr_A.as<double>(), m, c.S.as<int32_t>(),
+                                                                     c.bdata.as<double>(), c.bstride,
+                                                                     c.fscratch.as<double>(), b1, c.derr.as<int>(), b0);
+      ++c.n_launch;
+    }
     CK(cudaGetLastError());
   } else {
     size_t head = sizeof(double) * 5 * (size_t)k;
@@ -1193,38 +1210,78 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
       const bool gm = !(smem_variant && bucket_factor_blk_smem(k, false) <= 220 * 1024);
       const size_t sb = bucket_factor_blk_smem(k, gm);
       const int KPf = (k + FB - 1) & ~(FB - 1);
-      unsigned gridf = (unsigned)nbk;
+      const int nfb = b1 - b0;
+      unsigned gridf = (unsigned)std::max(1, nfb);
       double* gsf = nullptr;
-      if (gm) {
+      if (nfb <= 0) {
+      } else if (gm) {
         // many buckets (k <= 256): 4 CTAs of <= 64 registers per SM; otherwise 2 unconstrained
-        const bool four = KPf <= 256 && nbk >= 2 * (int64_t)c.sm_count;
-        gridf = (unsigned)std::min<int64_t>(nbk, (four ? 4 : 2) * (int64_t)c.sm_count);
+        const bool four = KPf <= 256 && nfb >= 2 * (int64_t)c.sm_count;
+        gridf = (unsigned)std::min<int64_t>(nfb, (four ? 4 : 2) * (int64_t)c.sm_count);
         CK(c.fscratch.ensure(sizeof(double) * (size_t)gridf * KPf * (KPf + 4)));
         gsf = c.fscratch.as<double>();
         auto kf = four ? k_bucket_factor_blk<true, 4> : k_bucket_factor_blk<true, 1>;
         CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-        kf<<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(), c.S.as<int32_t>(),
-                                                  c.bdata.as<double>(), c.bstride, gsf, c.derr.as<int>());
+        kf<<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, b1, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                  c.bdata.as<double>(), c.bstride, gsf, c.derr.as<int>(), b0);
+        ++c.n_launch;
       } else {
         CK(cudaFuncSetAttribute(k_bucket_factor_blk<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb));
-        k_bucket_factor_blk<false, 1><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, nbk, X, c.y.as<double>(),
+        k_bucket_factor_blk<false, 1><<<gridf, FACT_THREADS, sb, c.stream>>>(kp, k, b1, X, c.y.as<double>(),
                                                                              c.S.as<int32_t>(), c.bdata.as<double>(),
-                                                                             c.bstride, nullptr, c.derr.as<int>());
+                                                                             c.bstride, nullptr, c.derr.as<int>(), b0);
+        ++c.n_launch;
       }
+    } else if (b1 <= b0) {
     } else if (use_smem) {
       CK(cudaFuncSetAttribute(k_bucket_factor<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_bucket_factor<true><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
-                                                                   c.bdata.as<double>(), c.bstride, gs,
-                                                                   c.derr.as<int>());
+      k_bucket_factor<true><<<b1 - b0, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                                       c.bdata.as<double>(), c.bstride, gs,
+                                                                       c.derr.as<int>(), b0);
+      ++c.n_launch;
     } else {
       CK(cudaFuncSetAttribute(k_bucket_factor<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_bucket_factor<false><<<nbk, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
-                                                                    c.bdata.as<double>(), c.bstride, gs,
-                                                                    c.derr.as<int>());
+      k_bucket_factor<false><<<b1 - b0, FACT_THREADS, smem, c.stream>>>(kp, k, X, c.y.as<double>(), c.S.as<int32_t>(),
+                                                                        c.bdata.as<double>(), c.bstride, gs,
+                                                                        c.derr.as<int>(), b0);
+      ++c.n_launch;
     }
-    ++c.n_launch;
     CK(cudaGetLastError());
   }
+  cudaEventRecord(e1, c.stream);
+  CK(cudaStreamSynchronize(c.stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  c.t.fit_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+#undef CK
+  if (shard) {   // the caller exchanges the bucket blocks, then lcp_fit_finish runs a4
+    lcp_status_t st = check_device_errors(c);
+    if (st != LCP_OK) return st;
+    c.fit_pending = true;
+    return LCP_OK;
+  }
+  return fit_finish_impl(c);
+}
+
+// a4 (observation marginals, every bucket factor present) and the context state after a fit
+lcp_status_t fit_finish_impl(Ctx& c) {
+  NvtxRange nvtx_("lcp_fit_finish");
+  cudaError_t e;
+#define CK(x)                                  \
+  do {                                         \
+    e = (x);                                   \
+    if (e != cudaSuccess) return cuda_err(c, e, #x); \
+  } while (0)
+  const Geom& g = c.g;
+  const int64_t m = c.m;
+  const double* X = c.X.as<double>();
+  const unsigned gm = (unsigned)((m + 255) / 256);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, c.stream);
   // a4: observation marginals (grouped by bucket)
   k_gather_i32<<<gm, 256, 0, c.stream>>>(c.obs_bucket.as<int32_t>(), c.obs_by_bucket.as<int64_t>(), m,
                                          c.cell_bucket.as<int32_t>());
@@ -1235,9 +1292,10 @@ lcp_status_t fit_impl(Ctx& c, const double* xyz, const double* yv, int64_t m, in
   CK(cudaStreamSynchronize(c.stream));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  c.t.fit_ms = ms;
+  c.t.fit_ms += ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  c.fit_pending = false;
   lcp_status_t st = check_device_errors(c);
   if (st != LCP_OK) return st;
   // the vertex cache covers every grid vertex

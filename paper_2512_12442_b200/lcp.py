@@ -29,7 +29,7 @@ EXPORTS = ["lcp_create", "lcp_destroy", "lcp_last_error", "lcp_fit_local", "lcp_
            "lcp_cell_posterior", "lcp_point_marginals", "lcp_bucket_sets", "lcp_get_info",
            "lcp_stats_json", "lcp_synchronize", "lcp_set_level_field", "lcp_fit_sgpr",
            "lcp_pmc_cells_multi", "lcp_run_field_multi", "lcp_union_cells", "lcp_slab_auto_level",
-           "lcp_slab_cuts"]
+           "lcp_slab_cuts", "lcp_fit_shard_buffers", "lcp_fit_finish"]
 
 
 class LcpError(RuntimeError):
@@ -52,7 +52,7 @@ class OptsT(C.Structure):
     _fields_ = [("bucket_log2", C.c_int32), ("h_full", C.c_int32), ("precision", C.c_int32),
                 ("slab_rank", C.c_int32), ("slab_count", C.c_int32), ("slab_level", C.c_int32),
                 ("keep_records", C.c_int32), ("extreme_iters", C.c_int32), ("brick_pass", C.c_int32),
-                ("local_mode", C.c_int32), ("pad1_", C.c_int32), ("beta", C.c_double)]
+                ("local_mode", C.c_int32), ("fit_shard", C.c_int32), ("beta", C.c_double)]
 
 
 class InfoT(C.Structure):
@@ -101,6 +101,8 @@ def load_library() -> C.CDLL:
     L.lcp_run_field_multi.argtypes = [P, P, i32, dbl, i32, i64, u64, u32, P, i32, P, C.POINTER(i64)]
     L.lcp_union_cells.argtypes = [P, C.POINTER(i64), C.POINTER(P), C.POINTER(P)]
     L.lcp_slab_auto_level.argtypes = [C.POINTER(GridT), i32, i32]
+    L.lcp_fit_shard_buffers.argtypes = [P, C.POINTER(P), C.POINTER(i64), C.POINTER(P), C.POINTER(i64)]
+    L.lcp_fit_finish.argtypes = [P]
     L.lcp_slab_cuts.argtypes = [P, i32, i32, P]
     for name in EXPORTS:
         if name not in ("lcp_destroy", "lcp_last_error"):
@@ -157,7 +159,7 @@ class Context:
     def fit_local(self, xyz, y, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,
                   h_full: int = 2, precision: int = FP64, slab_rank: int = 0, slab_count: int = 1,
                   slab_level: int = 0, keep_records=False, extreme_iters: int = 0, brick_pass: int = 0,
-                  local_mode: int = 0, beta: float = 6.0):
+                  local_mode: int = 0, beta: float = 6.0, fit_shard: int = 0):
         """xyz (m,3) / y (m,) float64, either torch CUDA tensors or numpy host arrays.
         kernel = (kind, variance, lengthscale[3], nugget, prior_mean); grid = (lo, hi, cells).
         keep_records: True = every level, int L = levels < L (parity tap)."""
@@ -169,7 +171,8 @@ class Context:
         lo, hi, cells = grid
         gt = GridT((C.c_double * 3)(*lo), (C.c_double * 3)(*hi), (C.c_int32 * 3)(*cells), 0)
         ot = OptsT(bucket_log2, h_full, precision, slab_rank, slab_count, slab_level,
-                   int(keep_records), int(extreme_iters), int(brick_pass), int(local_mode), 0, float(beta))
+                   int(keep_records), int(extreme_iters), int(brick_pass), int(local_mode), int(fit_shard),
+                   float(beta))
         if isinstance(xyz, np.ndarray):
             xyz = np.ascontiguousarray(xyz, np.float64)
             y = np.ascontiguousarray(y, np.float64)
@@ -180,6 +183,32 @@ class Context:
                                    _is_dev(xyz), C.byref(kt), int(k), C.byref(gt), C.byref(ot))
         self._check(st, "lcp_fit_local")
         self.grid = (tuple(lo), tuple(hi), tuple(cells))
+        self._slab_count = slab_count
+        return self
+
+    def fit_shard_buffers(self):
+        """Sharded fit: (bdata, sets) as uint8 CUDA tensor views of the ctx-owned arrays (no
+        copy) and their per-rank chunk sizes in bytes, for an in-place all-gather."""
+        pb, ps = C.c_void_p(), C.c_void_p()
+        nb, ns = C.c_int64(), C.c_int64()
+        self._check(self._L.lcp_fit_shard_buffers(self._h, C.byref(pb), C.byref(nb), C.byref(ps), C.byref(ns)),
+                    "lcp_fit_shard_buffers")
+        return self._view_dev(pb.value, nb.value), nb.value, self._view_dev(ps.value, ns.value), ns.value
+
+    def _view_dev(self, ptr, chunk):
+        """uint8 CUDA tensor aliasing slab_count x chunk bytes of a ctx-owned device array."""
+        torch = self._torch
+        n = chunk * self._slab_count
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                        "strides": None, "stream": None}
+
+        with torch.cuda.device(self.device):
+            return torch.as_tensor(_View(), device=f"cuda:{self.device}")
+
+    def fit_finish(self):
+        self._check(self._L.lcp_fit_finish(self._h), "lcp_fit_finish")
         return self
 
     def fit_sgpr(self, xyz_M, mu_M, A_M, kernel: Tuple, k: int, grid: Tuple, bucket_log2: int = 0,

@@ -34,12 +34,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,world", [("c2", 2), ("c2", 8), ("c4", 2), ("c4", 8), ("c5", 8)])
-def test_torchrun_gather_equals_single_gpu(name, world, tmp_path):
+@pytest.mark.parametrize("name,world,shard", [("c2", 2, False), ("c2", 8, False), ("c4", 2, False),
+                                              ("c4", 8, False), ("c5", 8, False), ("c2", 3, True), ("c4", 8, True)])
+def test_torchrun_gather_equals_single_gpu(name, world, shard, tmp_path):
+    # shard: the bucket factors split across the ranks and all-gathered (dist.fit_sharded)
     out = tmp_path / "res.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "dist_check.py"),
-           "--workload", name, "--out", str(out)]
+           "--workload", name, "--out", str(out)] + (["--fit-shard"] if shard else [])
     env = dict(os.environ, OMP_NUM_THREADS="1")
     p = subprocess.run(cmd, cwd=ROOT, env=env, timeout=1200, capture_output=True, text=True)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]

@@ -30,12 +30,13 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--out", required=True)
     ap.add_argument("--n-samples", type=int, default=0, help="override N (0 = the config's)")
+    ap.add_argument("--fit-shard", action="store_true", help="shard the bucket factors (dist.fit_sharded)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
 
     from paper_2512_12442_b200 import Context, config_args
-    from paper_2512_12442_b200.dist import gather_fields, plan_z_cuts
+    from paper_2512_12442_b200.dist import fit_sharded, gather_fields, plan_z_cuts
     from workloads import generate
 
     world = int(os.environ["WORLD_SIZE"])
@@ -74,8 +75,11 @@ def main():
         del r_, ref_ctx
         torch.cuda.empty_cache()
     dist.barrier()
-    ctx = Context(local).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=rank,
-                                   slab_count=world)
+    if args.fit_shard:
+        ctx = fit_sharded(Context(local), X, y, kernel, k, grid, rank, world, bucket_log2=b, h_full=hf)
+    else:
+        ctx = Context(local).fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=rank,
+                                       slab_count=world)
     if T > 1:
         fields, nl, nu = ctx.run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, N, cfg.mc_seed, 0)
         nleaf = [int(v) for v in nl]
@@ -94,6 +98,7 @@ def main():
     if rank == 0:
         got = fields.cpu()
         res = {"workload": args.workload, "world": world, "backend": backend, "gpus": ngpu,
+               "fit_shard": bool(args.fit_shard),
                "bitexact": bool(torch.equal(got, ref)),
                "max_abs_diff": float((got - ref).abs().max()),
                "leaves_n1": nl_ref, "leaves_per_rank": [g["leaves"] for g in gathered],

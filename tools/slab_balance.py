@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fit-shard", action="store_true",
+                    help="the bucket factors split across the ranks (dist.fit_sharded); the all-gather is "
+                         "emulated by copies between the ranks' contexts and its NVLink time modelled")
     args = ap.parse_args()
     import torch
 
@@ -63,6 +66,63 @@ def main():
                 best = t if best is None else min(best, t)
             return n, best, ctx.stats()
 
+        def sharded(N):
+            """Every rank's sharded fit (timed), the in-place all-gather emulated by device copies
+            between the ranks' contexts (not timed; modelled as 7/8 of the blocks over NVLink at
+            700 GB/s), then each rank's lcp_fit_finish + run_field (timed)."""
+            ctxs = [Context(0) for _ in range(N)]
+            for rnd in range(2):               # round 0 warms the contexts (allocations), round 1 is timed
+                t_fit = []
+                for r in range(N):
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    ctxs[r].fit_local(X, y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=r, slab_count=N,
+                                      fit_shard=1)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    t_fit.append(e0.elapsed_time(e1))
+                bufs = [c_.fit_shard_buffers() for c_ in ctxs]
+                for r in range(N):             # the all-gather
+                    for dst in range(N):
+                        if dst != r:
+                            for which in (0, 2):
+                                ch = bufs[r][which + 1]
+                                bufs[dst][which][r * ch:(r + 1) * ch].copy_(bufs[r][which][r * ch:(r + 1) * ch])
+                torch.cuda.synchronize()
+                gather_bytes = (N - 1) * (bufs[0][1] + bufs[0][3])
+                t_gather = gather_bytes / 700e9 * 1e3
+                del bufs
+                leaves, times = [], []
+                for r in range(N):
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    ctxs[r].fit_finish()
+                    if T > 1:
+                        _, nl, _ = ctxs[r].run_field_multi(list(w.thetas), cfg.alpha, cfg.max_depth, cfg.n_samples,
+                                                           cfg.mc_seed, 0)
+                        n = int(np.sum(nl))
+                    else:
+                        n = ctxs[r].run_field(w.thetas[0], cfg.alpha, cfg.max_depth, cfg.n_samples, cfg.mc_seed)[1]
+                    e1.record()
+                    torch.cuda.synchronize()
+                    leaves.append(n)
+                    times.append(t_fit[r] + e0.elapsed_time(e1) + t_gather)
+            del ctxs
+            torch.cuda.empty_cache()
+            assert sum(leaves) == n1, (name, N, leaves, n1)
+            L = np.array(leaves, float)
+            tm = np.array(times)
+            print(f"{name} N={N} sharded fit: fit ms {[round(x, 2) for x in t_fit]}, modelled all-gather "
+                  f"{t_gather:.2f} ms ({gather_bytes / 1e9:.2f} GB per rank); step ms {[round(x, 1) for x in times]} "
+                  f"(T1 {t1:.1f}) -> projected efficiency {t1 / (N * tm.max()):.3f}", flush=True)
+            return {"fit_shard": True, "fit_ms_per_rank": [round(x, 3) for x in t_fit],
+                    "modelled_allgather_ms": t_gather, "allgather_bytes_per_rank": gather_bytes,
+                    "leaves_per_rank": leaves, "leaf_max_over_mean": float(L.max() / L.mean()),
+                    "step_ms_per_rank": [round(x, 3) for x in times],
+                    "projected_efficiency": float(t1 / (N * tm.max()))}
+
         one = Context(0)
         step(one, {})
         n1, t1, _ = timed(one, {})
@@ -71,6 +131,9 @@ def main():
         del one
         out = {"leaves_n1": n1, "t1_ms": t1, "ranks": {}}
         for N in args.ranks:
+            if args.fit_shard:
+                out["ranks"][N] = sharded(N)
+                continue
             leaves, times, plan = [], [], None
             for r in range(N):
                 ctx = Context(0)
