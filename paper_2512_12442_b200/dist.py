@@ -1,14 +1,16 @@
 """z-slab decomposition of the octree across GPUs.
 
-Every rank fits the same bucket-local GP (observations replicated: the halo),
-refines octree levels 0 .. slab_level redundantly, and the first refine after
+Every rank holds the same bucket-local GP (observations replicated: the halo;
+with `fit_sharded` each rank factors 1/N of the buckets and the blocks are
+all-gathered in place), refines octree levels 0 .. slab_level redundantly, and the first refine after
 the fit cuts the z-layers of level `slab_level` into contiguous per-rank ranges
 by prefix sums of the refined nodes per layer -- computed identically on every
 rank, so no communication is needed (liblcp, octree.cu).  Each rank then
 finishes refine + PMC on its own subtrees.  Results are bit-identical to one GPU:
 Philox counters are keyed by the global cell id and every node decision is local
-to the node.  The only collective is the final gather of the per-slab slices of
-the dense field(s) to rank 0 (point-to-point: only rank 0 receives).
+to the node.  The collectives: the all-gather of the sharded bucket factors
+after the fit, and the final gather of the per-slab slices of the dense field(s)
+to rank 0 (point-to-point: only rank 0 receives).
 
 This module is plumbing only (range arithmetic and torch.distributed calls); the
 slab plan itself is liblcp's (lcp_slab_auto_level / lcp_slab_cuts, host-only).

@@ -18,8 +18,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2512_12442_b200.dist import (cell_ranges, cell_z_cuts, equal_z_cuts, gather_fields, layers_at,
-                                        lfull_of)
+from paper_2512_12442_b200.dist import (_allgather_inplace, cell_ranges, cell_z_cuts, equal_z_cuts, gather_fields,
+                                        layers_at, lfull_of)
 from paper_2512_12442_b200.lcp import slab_auto_level, slab_cuts
 
 GRIDS = [(16, 16, 16), (23, 17, 11), (40, 9, 33), (64, 64, 64), (128, 128, 128), (256, 256, 128), (512, 512, 512),
@@ -138,6 +138,36 @@ def test_gather_fields_gloo(world, cells, T):
     w = np.random.default_rng(nz + world).integers(0, 50, nz)
     zc = cell_z_cuts(cells, lv, slab_cuts(w, world))
     procs = [ctx.Process(target=_worker, args=(r, world, port, cells, zc, T, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    oks = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(oks)
+
+
+def _ag_worker(rank, world, port, chunk, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    buf = torch.zeros(world * chunk, dtype=torch.uint8)
+    buf[rank * chunk:(rank + 1) * chunk] = torch.arange(chunk, dtype=torch.int64).remainder(251).to(torch.uint8) + rank
+    _allgather_inplace(buf, chunk)
+    want = torch.cat([torch.arange(chunk, dtype=torch.int64).remainder(251).to(torch.uint8) + r for r in range(world)])
+    q.put(bool(torch.equal(buf, want)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_fit_allgather_gloo(world):
+    # the in-place all-gather of dist.fit_sharded: rank r's chunk of the ctx-owned bucket
+    # blocks is sent, the others' are received in place
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ag_worker, args=(r, world, port, 1000 + 7 * world, q)) for r in range(world)]
     for p in procs:
         p.start()
     oks = [q.get(timeout=120) for _ in range(world)]
