@@ -130,7 +130,7 @@ const char* lcp_last_error(const lcp_ctx_t* ctx);
  * local GP), and the observation marginals.
  *   xyz: m x 3 row-major, y: m; host pointers if on_device == 0 (copied inside,
  *   synchronously), else device pointers (read before return).
- *   opts may be NULL (bucket_log2 = 0, h_full = 2, FP64, one slab, level 3, no records).
+ *   opts may be NULL (bucket_log2 = 0, h_full = 2, FP64, one slab, automatic slab level, no records).
  * Errors: EINVAL (k < 1, k > m, variance <= 0, nugget < 0, lengthscale <= 0,
  * cells < 1, bucket_log2 > Lfull, a non-finite coordinate or value), EFACTOR,
  * ENUMERIC, ENOMEM, ECUDA. */
