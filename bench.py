@@ -35,6 +35,10 @@ UNIT = "cells/s"
 #                           decision 3, queue store + load 14                              =  93
 OPS_PHASE1 = 114
 OPS_PHASE2 = 93
+# each further isovalue of a fused pass (k_pmc<T>, cuobjdump -sass: 271 vs 210 instructions per
+# two-sample phase-1 iteration at T = 3 vs 1): + 15 per sample; its crossing test in phase 2: + 4
+OPS_PHASE1_PER_EXTRA_ISO = 15
+OPS_PHASE2_PER_EXTRA_ISO = 4
 # SURVEY.md §8(d) per-unit figure of the leaf MC ("minimal op mix", fixed before any kernel):
 # 170-210 CUDA-core issue slots + 16 MUFU per sample; the lower end, 186, is used, and each
 # further isovalue of a fused multi-isovalue pass adds the crossing-test row (21 slots).
@@ -484,9 +488,10 @@ def run_ours(args):
     mc_s = float(t[1]) / args.steps / 1000.0
     peak = SM_COUNT * LANES_PER_SM_CLK * 1965e6 / 1e12          # T lane-op/s at the max SM clock
     p2_step = float(lv[2]) / args.steps
-    ops_step = samples_step * OPS_PHASE1 + p2_step * OPS_PHASE2
-    impl_mix = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
     fused_t = len(w.thetas) if len(w.thetas) > 1 and not args.dense and not args.separate_iso else 1
+    ops_step = (samples_step * (OPS_PHASE1 + OPS_PHASE1_PER_EXTRA_ISO * (fused_t - 1))
+                + p2_step * (OPS_PHASE2 + OPS_PHASE2_PER_EXTRA_ISO * (fused_t - 1)))
+    impl_mix = (ops_step / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
     ops_survey = samples_step * (OPS_SURVEY + OPS_SURVEY_PER_EXTRA_ISO * (fused_t - 1))
     achieved = (ops_survey / max(world, 1)) / mc_s / 1e12 if mc_s > 0 else None
     launches_per_step = 1 if fused_t > 1 else len(w.thetas)      # k_pmc launches per step
