@@ -35,7 +35,8 @@ def _port():
 
 
 @pytest.mark.parametrize("name,world,shard", [("c2", 2, False), ("c2", 8, False), ("c4", 2, False),
-                                              ("c4", 8, False), ("c5", 8, False), ("c2", 3, True), ("c4", 8, True)])
+                                              ("c4", 8, False), ("c5", 8, False), ("c2", 3, True), ("c4", 8, True),
+                                              ("c1", 8, True)])
 def test_torchrun_gather_equals_single_gpu(name, world, shard, tmp_path):
     # shard: the bucket factors split across the ranks and all-gathered (dist.fit_sharded)
     out = tmp_path / "res.json"
@@ -50,8 +51,10 @@ def test_torchrun_gather_equals_single_gpu(name, world, shard, tmp_path):
                                           "leaves_per_rank", "record_cells_per_rank")}))
     assert res["bitexact"], res["max_abs_diff"]
     assert res["leaves_sum"] == res["leaves_n1"]
-    # no empty rank, the same plan on every rank
-    assert all(sum(lv) > 0 for lv in res["leaves_per_rank"]), res["leaves_per_rank"]
+    # no empty rank (c1: 16^3 cells, 2 slab layers for 8 ranks -- more ranks than layers, and
+    # more ranks than buckets for the sharded fit), the same plan on every rank
+    if name != "c1":
+        assert all(sum(lv) > 0 for lv in res["leaves_per_rank"]), res["leaves_per_rank"]
     assert all(c == res["layer_cuts"][0] for c in res["layer_cuts"])
     assert len(res["layer_cuts"][0]) == world + 1
     # slab-local record tables, used by every rank's leaf pass
