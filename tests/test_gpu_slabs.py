@@ -59,7 +59,8 @@ def test_torchrun_gather_equals_single_gpu(name, world, shard, tmp_path):
     assert len(res["layer_cuts"][0]) == world + 1
     # slab-local record tables, used by every rank's leaf pass
     if res["records_used_n1"]:
-        assert all(res["records_used_per_rank"]), res["records_used_per_rank"]
+        used = [u for u, lv in zip(res["records_used_per_rank"], res["leaves_per_rank"]) if sum(lv) > 0]
+        assert all(used), res["records_used_per_rank"]
         lf = {"c2": 6, "c4": 8, "c5": 9}[name]
         assert max(res["record_cells_per_rank"]) < (1 << (3 * lf))   # slab-local: below the whole cube
 
