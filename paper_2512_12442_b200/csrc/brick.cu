@@ -30,6 +30,16 @@ constexpr int NVP = 128;                    // padded vertex columns
 constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
 constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
+// k_brick's CTA: BT threads = 4 column blocks x NRS row sets of warps; mu / variance dots
+// split over DOTP threads per vertex column
+#ifndef BRICK_NT
+#define BRICK_NT 512
+#endif
+constexpr int BT = BRICK_NT;
+constexpr int NRS = BT / 128;               // row sets (4 or 8)
+constexpr int TPW = 16 / NRS;               // row tiles per warp (4 or 2)
+constexpr int DOTP = BT / NVP;              // threads per column in the mu / variance dots
+constexpr int P1_UNROLL = BT >= 1024 ? 2 : 4;
 
 // kernel value from r^2 (Matern-5/2 per BASELINE c4/c5) with exp_neg_fast
 __device__ __forceinline__ double kern_from_r2_fast(const KernParams& p, double r2) {
@@ -97,7 +107,7 @@ struct BrickOut {
 };
 
 template <bool FUSED>
-__global__ void __launch_bounds__(BRICK_THREADS, 1)
+__global__ void __launch_bounds__(BT, 1)
     k_brick(BrickArgs a, const int64_t* __restrict__ cells, const int64_t* __restrict__ run_start, int64_t nruns,
             unsigned long long* __restrict__ work, BrickOut o) {
   extern __shared__ double smem[];
@@ -156,14 +166,14 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       if (b != staged) {
         const double2* src = reinterpret_cast<const double2*>(a.bdata + (int64_t)b * a.bstride);
         double2* dst = reinterpret_cast<double2*>(smem);
-        for (int64_t t = tid; t < (a.bstride >> 1); t += BRICK_THREADS) dst[t] = __ldg(src + t);
+        for (int64_t t = tid; t < (a.bstride >> 1); t += BT) dst[t] = __ldg(src + t);
         staged = b;
       }
       __syncthreads();
       // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding.
       // r^2 is separable over the lattice: T[j][5d + t] = ((x_jd - v_d(t)) / l_d)^2 for the
       // 5 lattice positions t per axis d, then r^2 = (T_x + T_y) + T_z per element.
-      for (int e = tid; e < 15 * k; e += BRICK_THREADS) {
+      for (int e = tid; e < 15 * k; e += BT) {
         const int j = e / 15, col = e - 15 * j, d = col / 5, t = col - 5 * d;
         const int c0 = d == 0 ? i0 : (d == 1 ? j0 : k0);
         const double diff = (sX[d * k + j] - vpos(g, d, min(c0 + t, g.cells[d]))) * a.kp.inv_ls[d];
@@ -177,8 +187,8 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         // straight-line body (clamped indices, 0/1 mask) so that the unrolled copies
         // interleave: the Horner chains of exp are latency-bound one at a time
         const int ta = vok ? va : 0, tb = vok ? 5 + vb : 5, tc = vok ? 10 + vc : 10;
-#pragma unroll 4
-        for (int j = tid >> 7; j < KP; j += BRICK_THREADS / NVP) {
+#pragma unroll P1_UNROLL
+        for (int j = tid >> 7; j < KP; j += BT / NVP) {
           const double* tj = sT + 16 * min(j, k - 1);
           const double val = kern_from_r2_tab(a.kp, (tj[ta] + tj[tb]) + tj[tc], sExp);
           KV[(int64_t)j * VSTR + v] = (j < k && vok) ? val : 0.0;
@@ -188,28 +198,28 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       {
         // mu_v = m0 + sum_j K[j][v] alpha_j: 4 threads per vertex column (rows j = part
         // mod 4, conflict-free), combined as ((s0 + s1) + (s2 + s3))
-        const int v = tid >> 2, part = tid & 3;
+        const int v = tid / DOTP, part = tid % DOTP;
         double s = 0.0;
-        for (int j = part; j < k; j += 4) s = fma(KV[(int64_t)j * VSTR + v], sAlpha[j], s);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        for (int j = part; j < k; j += DOTP) s = fma(KV[(int64_t)j * VSTR + v], sAlpha[j], s);
+#pragma unroll
+        for (int o = 1; o < DOTP; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (part == 0) sMu[v] = a.kp.m0 + s;
       }
       // phase 2: V = L^-1 K with DMMA; warp = (row set rs, column block cb)
       const int rs = wid >> 2, cb = wid & 3;
       const int nrt = KP >> 3;
-      double acc[4][4][2];
+      double acc[TPW][4][2];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < TPW; ++t)
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
       const int lr = lane >> 2, lc = lane & 3;
-      // row tiles rt(t) zig-zag over the 4 row sets so that every warp gets the same
-      // triangular work (rs = 0: 0, 7, 8, 15; rs = 3: 3, 4, 11, 12)
-      auto rtile = [&](int t) { return (t & 1) ? (3 - rs) + 4 * t : rs + 4 * t; };
+      // row tiles rt(t) zig-zag over the NRS row sets so that every warp gets the same
+      // triangular work (NRS = 4: rs = 0: 0, 7, 8, 15; rs = 3: 3, 4, 11, 12)
+      auto rtile = [&](int t) { return (t & 1) ? (NRS - 1 - rs) + NRS * t : rs + NRS * t; };
       int last_rt = -1;
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int t = 0; t < TPW; ++t)
         if (rtile(t) < nrt) last_rt = max(last_rt, rtile(t));
       const int jend = last_rt < 0 ? 0 : min(KP, 8 * last_rt + 8);
       for (int j = 0; j < jend; j += 4) {
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
 #pragma unroll
         for (int u = 0; u < 4; ++u) bf[u] = KV[(int64_t)jj * VSTR + 32 * cb + 8 * u + lr];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < TPW; ++t) {
           const int rt = rtile(t);
           if (rt >= nrt || 8 * rt + 7 < j) continue;   // warp-uniform: zero block of L^-1
           const double af = sLA[la_block(rt, j >> 2) + lane];
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       }
       __syncthreads();   // every warp has read K
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < TPW; ++t) {
         const int rt = rtile(t);
         if (rt >= nrt) continue;
 #pragma unroll
@@ -242,15 +252,15 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
         // vertex marginals (R10) of the brick's vertices whose own bucket is b:
         // var = k(v,v) - ||V_{:,v}||^2 (4 threads per column as for mu), cached as
         // (mu, 1 / (sigma sqrt 2))
-        const int v = tid >> 2, part = tid & 3;
+        const int v = tid / DOTP, part = tid % DOTP;
         double s2 = 0.0;
         if (v < NVB)
-          for (int j = part; j < k; j += 4) {
+          for (int j = part; j < k; j += DOTP) {
             const double x = KV[(int64_t)j * VSTR + v];
             s2 = fma(x, x, s2);
           }
-        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
-        s2 += __shfl_xor_sync(0xffffffffu, s2, 2);
+#pragma unroll
+        for (int o = 1; o < DOTP; o <<= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
         if (part == 0 && v < NVB) {
           const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
           const int vi = i0 + va, vj = j0 + vb, vk = k0 + vc;
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(BRICK_THREADS, 1)
       }
       // phase 3: Sigma_C = K_CC - V_C^T V_C per cell (warp per cell)
       const int64_t nq = FUSED ? BK * BK * BK : q1 - q0;
-      for (int64_t qq = wid; qq < nq; qq += BRICK_THREADS / 32) {
+      for (int64_t qq = wid; qq < nq; qq += BT / 32) {
         int xi, xj, xk;
         int64_t slot;
         if (FUSED) {
@@ -409,7 +419,7 @@ cudaError_t launch_brick_pass(Ctx& c, const uint64_t* bricks, int64_t nb, double
   o.var_floor = 1e-12 * c.kp.var;
   o.derr = c.derr.as<int>();
   unsigned grid = (unsigned)std::min<int64_t>((nb + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count);
-  k_brick<true><<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), nullptr, nullptr, nb, dcnt + 13, o);
+  k_brick<true><<<grid, BT, smem, c.stream>>>(brick_args(c), nullptr, nullptr, nb, dcnt + 13, o);
   ++c.n_launch;
   return cudaGetLastError();
 }
@@ -684,7 +694,7 @@ bool brick_posterior(Ctx& c, const int64_t* cells, int64_t n, double* post, cuda
   o.derr = c.derr.as<int>();
   int blocks_per_sm = smem <= 110 * 1024 ? 2 : 1;
   unsigned grid = (unsigned)std::min<int64_t>((nruns + BRICK_CHUNK - 1) / BRICK_CHUNK, (int64_t)c.sm_count * blocks_per_sm);
-  k_brick<false><<<grid, BRICK_THREADS, smem, c.stream>>>(brick_args(c), cells, start, nruns, dcnt + 13, o);
+  k_brick<false><<<grid, BT, smem, c.stream>>>(brick_args(c), cells, start, nruns, dcnt + 13, o);
   ++c.n_launch;
   err = cudaGetLastError();
   c.last_brick_runs = nruns;
