@@ -61,7 +61,7 @@ def test_torchrun_gather_equals_single_gpu(name, world, shard, tmp_path):
     if res["records_used_n1"]:
         used = [u for u, lv in zip(res["records_used_per_rank"], res["leaves_per_rank"]) if sum(lv) > 0]
         assert all(used), res["records_used_per_rank"]
-        lf = {"c2": 6, "c4": 8, "c5": 9}[name]
+        lf = {"c1": 4, "c2": 6, "c4": 8, "c5": 9}[name]
         assert max(res["record_cells_per_rank"]) < (1 << (3 * lf))   # slab-local: below the whole cube
 
 
