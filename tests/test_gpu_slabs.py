@@ -120,3 +120,39 @@ def test_slab_refine_shallower_than_plan(dev):
         allp = np.concatenate(parts)
         assert len(allp) == len(np.unique(allp))
         assert np.array_equal(np.sort(allp), ref), depth
+
+
+def test_sharded_fit_state_machine(dev):
+    # lcp_fit_shard_buffers / lcp_fit_finish only while a sharded fit is pending; every other
+    # call returns ESTATE in between; an unsharded fit has nothing pending
+    from paper_2512_12442_b200 import Context, LcpError, config_args
+    from paper_2512_12442_b200.lcp import LCP_ESTATE
+    w = generate("t2")
+    cfg = w.cfg
+    kernel, grid, k, b, hf = config_args(cfg)
+    ctx = Context(0).fit_local(w.X, w.y, kernel, k, grid, bucket_log2=b, h_full=hf)
+    for call in (ctx.fit_shard_buffers, ctx.fit_finish):
+        with pytest.raises(LcpError) as e:
+            call()
+        assert e.value.status == LCP_ESTATE
+    ctx.fit_local(w.X, w.y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=0, slab_count=2, fit_shard=1)
+    with pytest.raises(LcpError) as e:
+        ctx.octree_refine(w.thetas[0], cfg.alpha, cfg.max_depth)
+    assert e.value.status == LCP_ESTATE
+    bd, nb, sets, ns = ctx.fit_shard_buffers()
+    assert bd.numel() == 2 * nb and sets.numel() == 2 * ns
+    # stand-in for the other rank's chunk: a second context's own sharded fit
+    other = Context(0).fit_local(w.X, w.y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=1, slab_count=2,
+                                 fit_shard=1)
+    obd, _, osets, _ = other.fit_shard_buffers()
+    bd[nb:].copy_(obd[nb:])
+    sets[ns:].copy_(osets[ns:])
+    ctx.fit_finish()
+    with pytest.raises(LcpError):
+        ctx.fit_finish()
+    # the completed model equals an unsharded one (same refine, same slab plan)
+    ref = Context(0).fit_local(w.X, w.y, kernel, k, grid, bucket_log2=b, h_full=hf, slab_rank=0, slab_count=2)
+    a = ctx.run_field(w.thetas[0], cfg.alpha, cfg.max_depth, 500, 3)[0]
+    r = ref.run_field(w.thetas[0], cfg.alpha, cfg.max_depth, 500, 3)[0]
+    assert torch.equal(a, r)
+    assert torch.equal(ctx.bucket_sets(), ref.bucket_sets())
