@@ -281,7 +281,9 @@ lcp_status_t lcp_synchronize(lcp_ctx_t* ctx);
  * caller (e.g. NCCL allgather with sendbuff = recvbuff + rank x chunk); then
  * lcp_fit_finish computes the observation marginals (a4) and completes the fit.
  * Every other call returns ESTATE in between.  The fitted model is the one an
- * unsharded fit builds, bit for bit (per-bucket arithmetic does not depend on the split). */
+ * unsharded fit builds, bit for bit (per-bucket arithmetic does not depend on the split).
+ * Errors: EINVAL on a null pointer; ESTATE when no sharded fit is pending; lcp_fit_finish
+ * as lcp_fit_local's a4 (ENUMERIC, ECUDA). */
 lcp_status_t lcp_fit_shard_buffers(lcp_ctx_t* ctx, void** bdata_dev, int64_t* bdata_chunk_bytes,
                                    void** sets_dev, int64_t* sets_chunk_bytes);
 lcp_status_t lcp_fit_finish(lcp_ctx_t* ctx);
