@@ -139,6 +139,29 @@ def _opts(seed, d):
     return o, d
 
 
+def _fp32_mean_scale(d, M, cell):
+    """sum_j |k(x_c, x_j) alpha_j| for the 8 corners c of `cell`, alpha = K_SS^-1 (y_S - m0):
+    the scale of the FP32 posterior's mean error (R17: the kernel values k_j are rounded to
+    FP32, relative error a few eps32, so |d mu| ~ eps32 sum_j |k_j alpha_j|, whatever the
+    accumulation precision).  Tolerance arithmetic only (numpy), not an expected value."""
+    S = np.asarray(M.bucket_set(M.cell_bucket(cell)))
+    S = S[(S >= 0) & (S < len(d["y"]))]
+    ls = np.asarray(d["ls"])
+
+    def kern(A, B):
+        r = np.sqrt((((A[:, None, :] - B[None]) / ls) ** 2).sum(-1))
+        if d["kind"] == 0:
+            return d["var"] * np.exp(-0.5 * r * r)
+        return d["var"] * (1 + math.sqrt(5) * r + 5.0 / 3.0 * r * r) * np.exp(-math.sqrt(5) * r)
+
+    X = d["X"][S]
+    al = np.linalg.solve(kern(X, X) + d["nug"] * np.eye(len(S)), d["y"][S] - d["m0"])
+    lo, hi, n = (np.asarray(d[key], np.float64) for key in ("lo", "hi", "cells"))
+    ijk = np.array([cell % n[0], (cell // n[0]) % n[1], cell // (n[0] * n[1])], np.float64)
+    Q = np.array([lo + (ijk + [(c & 1), (c >> 1) & 1, c >> 2]) * (hi - lo) / n for c in range(8)])
+    return np.abs(kern(Q, X) * al).sum(1)
+
+
 @pytest.mark.parametrize("seed", _seeds(30))
 def test_fuzz_options(seed):
     from paper_2512_12442_b200 import Context, LcpError
@@ -197,7 +220,13 @@ def test_fuzz_options(seed):
             for q, c in enumerate(lv[sel]):
                 mu_o, cov_o = M.cell_posterior(int(c))
                 em, ec = posterior_close(mu_g[q], mu_o, cov_g[q], cov_o, d["var"], tol)
-                assert em <= tol and ec <= tol, (o, int(c), em, ec)
+                tol_mu = tol
+                if o["precision"] and em > tol:
+                    # FP32 mean: 1e-4 (R18) or, for an ill-conditioned K_SS (large sum |alpha|),
+                    # twice its rounding scale (R17; measured <= 0.24x on the worst of 3897 draws)
+                    sc = _fp32_mean_scale(d, M, int(c)) / np.maximum(np.abs(mu_o), math.sqrt(d["var"]))
+                    tol_mu = max(tol, 2 * float(np.finfo(np.float32).eps) * float(sc.max()))
+                assert em <= tol_mu and ec <= tol, (o, int(c), em, ec, tol_mu)
     fields, nls, nu = ctx.run_field_multi(thetas, alpha, md, N, d["seed"], 5)
     cells_u, mask_u = ctx.union_cells()
     cells_u, mask_u = cells_u.cpu().numpy(), mask_u.cpu().numpy()
