@@ -118,6 +118,23 @@ def test_octree_node_sets(name, dev):
             assert np.array_equal(np.sort(leaves_g), leaves_o)
 
 
+@pytest.mark.parametrize("name", ["t2", "c2"])
+def test_octree_shallow_max_depth(name, dev):
+    # a leaf level above the cells (max_depth < Lfull): every cell of a surviving node of
+    # level max_depth is a leaf (k_emit_cells writes whole node boxes); leaf sets equal
+    w, ctx, M = _ctx(name, dev)
+    cfg = w.cfg
+    th = w.thetas[0]
+    for depth in range(0, cfg.max_depth):
+        leaves_g = ctx.octree_refine(th, cfg.alpha, depth).cpu().numpy()
+        rec_o, leaves_o = M.octree(th, cfg.alpha, depth)
+        res = compare_node_sets(ctx.node_records(), rec_o, cfg.alpha)
+        assert not res["unexcused"], (depth, res["unexcused"][:10])
+        if res["excused"] == 0:
+            assert np.array_equal(np.sort(leaves_g), leaves_o), depth
+        assert len(np.unique(leaves_g)) == len(leaves_g)
+
+
 @pytest.mark.parametrize("name", ["t1", "t2", "c2", "c3"])
 def test_octree_node_sets_continuous_extremes(name, dev):
     # NEXT-1 (R26): the deterministic continuous extreme search at coarse nodes,

@@ -123,18 +123,24 @@ def main():
                     "step_ms_per_rank": [round(x, 3) for x in times],
                     "projected_efficiency": float(t1 / (N * tm.max()))}
 
+        phase_keys = ("fit_ms", "refine_ms", "brick_pass_ms", "posterior_ms", "chol_ms", "mc_ms", "scatter_ms",
+                      "launches", "vertex_marginals")
+
+        def phases(st):
+            return {key: st[key] for key in phase_keys if key in st}
+
         one = Context(0)
         step(one, {})
-        n1, t1, _ = timed(one, {})
+        n1, t1, st1 = timed(one, {})
         one_leaves = [one.octree_refine(th, cfg.alpha, cfg.max_depth).cpu().numpy() for th in w.thetas[:1]]
         lf = one.info()["lfull"]
         del one
-        out = {"leaves_n1": n1, "t1_ms": t1, "ranks": {}}
+        out = {"leaves_n1": n1, "t1_ms": t1, "phases_n1": phases(st1), "ranks": {}}
         for N in args.ranks:
             if args.fit_shard:
                 out["ranks"][N] = sharded(N)
                 continue
-            leaves, times, plan = [], [], None
+            leaves, times, plan, ph = [], [], None, []
             for r in range(N):
                 ctx = Context(0)
                 step(ctx, dict(slab_rank=r, slab_count=N))   # warm-up
@@ -142,6 +148,7 @@ def main():
                 leaves.append(n)
                 times.append(t)
                 plan = st["slab"]
+                ph.append(phases(st))
                 del ctx
                 torch.cuda.empty_cache()
             assert sum(leaves) == n1, (name, N, leaves, n1)
@@ -156,7 +163,7 @@ def main():
                                "leaves_per_rank": leaves, "leaf_max_over_mean": float(L.max() / L.mean()),
                                "step_ms_per_rank": [round(x, 3) for x in times],
                                "projected_efficiency": float(t1 / (N * tm.max())),
-                               "empty_ranks": int((L == 0).sum())}
+                               "empty_ranks": int((L == 0).sum()), "phases_per_rank": ph}
             print(f"{name} N={N}: level {plan['level']} ({plan['layers']} layers) cuts {plan['layer_cuts']} "
                   f"leaves {leaves} max/mean {L.max() / L.mean():.3f}; step ms {[round(x, 1) for x in times]} "
                   f"(T1 {t1:.1f}) -> projected efficiency {t1 / (N * tm.max()):.3f}", flush=True)
