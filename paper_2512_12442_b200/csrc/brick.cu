@@ -29,7 +29,10 @@ constexpr int NVP = 128;                    // padded vertex columns
 // fall on disjoint bank octets within each half-warp phase (conflict-free).
 constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
-constexpr int BRICK_CHUNK = 4;              // runs grabbed per atomic
+#ifndef BRICK_CHUNK_N
+#define BRICK_CHUNK_N 4
+#endif
+constexpr int BRICK_CHUNK = BRICK_CHUNK_N;  // runs grabbed per atomic
 // k_brick's CTA: BT threads = 4 column blocks x NRS row sets of warps; mu / variance dots
 // split over DOTP threads per vertex column
 #ifndef BRICK_NT
@@ -40,6 +43,33 @@ constexpr int NRS = BT / 128;               // row sets (4 or 8)
 constexpr int TPW = 16 / NRS;               // row tiles per warp (4 or 2)
 constexpr int DOTP = BT / NVP;              // threads per column in the mu / variance dots
 constexpr int P1_UNROLL = BT >= 1024 ? 2 : 4;
+// Timing-decomposition knobs (tools/brick_variants.py only; the records they produce are
+// wrong): BRICK_DIAG_K = 1 replaces the kernel evaluation by one FMA on r^2,
+// BRICK_DIAG_SOLVE = 0 / BRICK_DIAG_SIGMA = 0 skip the DMMA loops of phases 2 / 3.
+#ifndef BRICK_DIAG_K
+#define BRICK_DIAG_K 0
+#endif
+#ifndef BRICK_DIAG_SOLVE
+#define BRICK_DIAG_SOLVE 1
+#endif
+#ifndef BRICK_DIAG_SIGMA
+#define BRICK_DIAG_SIGMA 1
+#endif
+#ifndef BRICK_SOLVE_V2      // the DMMA solve with precomputed 32-bit shared addresses
+#define BRICK_SOLVE_V2 2
+#endif
+#ifndef BRICK_P1_V2         // branch-free phase-1 kernel values
+#define BRICK_P1_V2 1
+#endif
+#ifndef BRICK_DIAG_MU       // 0: skip the mu dot
+#define BRICK_DIAG_MU 1
+#endif
+#ifndef BRICK_DIAG_MARG     // 0: skip the vertex marginals
+#define BRICK_DIAG_MARG 1
+#endif
+#ifndef BRICK_DIAG_REC      // 0: skip phase 3 (the per-cell records)
+#define BRICK_DIAG_REC 1
+#endif
 
 // kernel value from r^2 (Matern-5/2 per BASELINE c4/c5) with exp_neg_fast
 __device__ __forceinline__ double kern_from_r2_fast(const KernParams& p, double r2) {
@@ -70,6 +100,12 @@ __device__ __forceinline__ void dmma(double a, double b, double& d0, double& d1)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ int64_t brick_key(const Geom& g, int64_t cell) {
@@ -126,6 +162,9 @@ __global__ void __launch_bounds__(BT, 1)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geom& g = a.g;
   if (tid < 64) sExp[tid] = c_exp2_64[tid];   // read after the loop's first barrier
+#if BRICK_P1_V2
+  for (int64_t e = tid; e < (int64_t)KP * VSTR; e += BT) KV[e] = 0.0;   // padding rows / columns
+#endif
   int staged = -1;
   for (;;) {
     if (tid == 0) s_r0 = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
@@ -180,6 +219,49 @@ __global__ void __launch_bounds__(BT, 1)
         sT[16 * j + col] = diff * diff;
       }
       __syncthreads();
+#if BRICK_P1_V2
+      {
+        // branch-free kernel values (the kernel kind hoisted out of the loop, exp_neg_tab_bf
+        // without the underflow branch, sqrt of r^2 + 1e-300 without the zero select) so
+        // that the unrolled evaluations interleave; rows j >= k and the padding columns
+        // v >= 125 are never written here: zeroed at kernel start, and the V write-back
+        // (L^-1 times zero columns, zero rows of L^-1) keeps them zero
+        const int v = tid & (NVP - 1);
+        const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
+        const bool vok = v < NVB;
+        const int ta = vok ? va : 0, tb = vok ? 5 + vb : 5, tc = vok ? 10 + vc : 10;
+        const double var = a.kp.var;
+        // P1_UNROLL rows per step evaluated unconditionally (rows past k clamped, not
+        // stored): a straight-line block the scheduler can interleave
+        auto p1 = [&](auto kval) {
+          constexpr int RS = BT / NVP;   // row stride of a thread
+          for (int jb = tid >> 7; jb < k; jb += RS * P1_UNROLL) {
+            double val[P1_UNROLL];
+#pragma unroll
+            for (int u = 0; u < P1_UNROLL; ++u) {
+              const double* tj = sT + 16 * min(jb + RS * u, k - 1);
+              val[u] = kval((tj[ta] + tj[tb]) + tj[tc]);
+            }
+#pragma unroll
+            for (int u = 0; u < P1_UNROLL; ++u)
+              if (vok && jb + RS * u < k) KV[(int64_t)(jb + RS * u) * VSTR + v] = val[u];
+          }
+        };
+#if BRICK_DIAG_K
+        p1([&](double r2) { return fma(r2, -1e-3, var); });
+#else
+        if (a.kp.kind == LCP_K_SE) {
+          p1([&](double r2) { return var * exp_neg_tab_bf(0.5 * r2, sExp); });
+        } else {
+          p1([&](double r2) {
+            const double r = sqrt_pos(r2 + 1e-300);
+            const double s5 = SQRT5 * r;
+            return var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_tab_bf(s5, sExp);
+          });
+        }
+#endif
+      }
+#else
       {
         const int v = tid & (NVP - 1);
         const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
@@ -190,17 +272,22 @@ __global__ void __launch_bounds__(BT, 1)
 #pragma unroll P1_UNROLL
         for (int j = tid >> 7; j < KP; j += BT / NVP) {
           const double* tj = sT + 16 * min(j, k - 1);
+#if BRICK_DIAG_K
+          const double val = fma((tj[ta] + tj[tb]) + tj[tc], -1e-3, a.kp.var);
+#else
           const double val = kern_from_r2_tab(a.kp, (tj[ta] + tj[tb]) + tj[tc], sExp);
+#endif
           KV[(int64_t)j * VSTR + v] = (j < k && vok) ? val : 0.0;
         }
       }
+#endif
       __syncthreads();
       {
         // mu_v = m0 + sum_j K[j][v] alpha_j: 4 threads per vertex column (rows j = part
         // mod 4, conflict-free), combined as ((s0 + s1) + (s2 + s3))
         const int v = tid / DOTP, part = tid % DOTP;
         double s = 0.0;
-        for (int j = part; j < k; j += DOTP) s = fma(KV[(int64_t)j * VSTR + v], sAlpha[j], s);
+        for (int j = part; j < (BRICK_DIAG_MU ? k : 0); j += DOTP) s = fma(KV[(int64_t)j * VSTR + v], sAlpha[j], s);
 #pragma unroll
         for (int o = 1; o < DOTP; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (part == 0) sMu[v] = a.kp.m0 + s;
@@ -221,7 +308,53 @@ __global__ void __launch_bounds__(BT, 1)
 #pragma unroll
       for (int t = 0; t < TPW; ++t)
         if (rtile(t) < nrt) last_rt = max(last_rt, rtile(t));
-      const int jend = last_rt < 0 ? 0 : min(KP, 8 * last_rt + 8);
+      const int jend = (last_rt < 0 || !BRICK_DIAG_SOLVE) ? 0 : min(KP, 8 * last_rt + 8);
+#if BRICK_SOLVE_V2 == 2
+      // row tile by row tile: one A pointer live at a time (the accumulators of all four
+      // tiles stay in registers until the write-back), B fragments re-read per tile
+      const uint32_t kv_s = (uint32_t)__cvta_generic_to_shared(KV) + 8u * (lc * VSTR + 32 * cb + lr);
+      const uint32_t la_s = (uint32_t)__cvta_generic_to_shared(sLA) + 8u * lane;
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const int rt = rtile(t);
+        const int je = (rt < nrt && BRICK_DIAG_SOLVE) ? 8 * rt + 8 : 0;
+        const uint32_t pa = la_s + 8u * (uint32_t)la_block(rt < nrt ? rt : 0, 0);
+#pragma unroll 2
+        for (int j = 0; j < je; j += 4) {
+          const uint32_t kb = kv_s + 8u * VSTR * j;
+          const double af = lds_f64(pa + 64u * j);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(af, lds_f64(kb + 64u * u), acc[t][u][0], acc[t][u][1]);
+        }
+      }
+#elif BRICK_SOLVE_V2
+      // 32-bit shared addresses computed once: the A fragment of (rt, js) sits at
+      // la_block(rt, 0) + 32 js doubles, the B fragments of k-step j at row j + lc; a row
+      // tile takes part while j < 8 rt + 8 (the nonzero blocks of L^-1)
+      const uint32_t kv_s = (uint32_t)__cvta_generic_to_shared(KV) + 8u * (lc * VSTR + 32 * cb + lr);
+      const uint32_t la_s = (uint32_t)__cvta_generic_to_shared(sLA) + 8u * lane;
+      uint32_t pa[TPW];
+      int jlim[TPW];
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const int rt = rtile(t);
+        jlim[t] = rt < nrt ? 8 * rt + 8 : 0;
+        pa[t] = la_s + 8u * (uint32_t)la_block(rt < nrt ? rt : 0, 0);
+      }
+      for (int j = 0; j < jend; j += 4) {
+        const uint32_t kb = kv_s + 8u * VSTR * j;
+        double bf[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) bf[u] = lds_f64(kb + 64u * u);
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          if (j >= jlim[t]) continue;   // warp-uniform: zero block of L^-1
+          const double af = lds_f64(pa[t] + 64u * j);   // + 32 js doubles, js = j / 4
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
+        }
+      }
+#else
       for (int j = 0; j < jend; j += 4) {
         const int jj = j + lc;
         double bf[4];
@@ -236,6 +369,7 @@ __global__ void __launch_bounds__(BT, 1)
           for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
         }
       }
+#endif
       __syncthreads();   // every warp has read K
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
@@ -248,7 +382,7 @@ __global__ void __launch_bounds__(BT, 1)
         }
       }
       __syncthreads();
-      if (FUSED) {
+      if (FUSED && BRICK_DIAG_MARG) {
         // vertex marginals (R10) of the brick's vertices whose own bucket is b:
         // var = k(v,v) - ||V_{:,v}||^2 (4 threads per column as for mu), cached as
         // (mu, 1 / (sigma sqrt 2))
@@ -278,7 +412,7 @@ __global__ void __launch_bounds__(BT, 1)
         }
       }
       // phase 3: Sigma_C = K_CC - V_C^T V_C per cell (warp per cell)
-      const int64_t nq = FUSED ? BK * BK * BK : q1 - q0;
+      const int64_t nq = !BRICK_DIAG_REC ? 0 : FUSED ? BK * BK * BK : q1 - q0;
       for (int64_t qq = wid; qq < nq; qq += BT / 32) {
         int xi, xj, xk;
         int64_t slot;
@@ -293,7 +427,7 @@ __global__ void __launch_bounds__(BT, 1)
         const int cr = lr;   // corner of this lane's A row / B column
         const int lv = (xi - i0 + (cr & 1)) + (BK + 1) * ((xj - j0 + ((cr >> 1) & 1)) + (BK + 1) * (xk - k0 + (cr >> 2)));
         double d0 = 0.0, d1 = 0.0;
-        for (int s = 0; s < KP; s += 4) {
+        for (int s = 0; s < (BRICK_DIAG_SIGMA ? KP : 0); s += 4) {
           double v = KV[(int64_t)(s + lc) * VSTR + lv];
           dmma(v, v, d0, d1);
         }

@@ -73,6 +73,41 @@ __device__ __forceinline__ double exp_neg_tab(double x, const double* __restrict
   return (m < -1022 || x > 745.0) ? 0.0 : (tab[ni & 63] * p) * scale;
 }
 
+// exp_neg_tab without branches (k_brick's phase 1): x clamped to 745 (e^-745 is below the
+// smallest subnormal), 2^m applied as 2^(m >> 1) 2^(m - (m >> 1)) so that m < -1022 gives
+// the subnormal (or zero) product instead of a branch to 0; identical to exp_neg_tab
+// whenever that one returns a normal number.  The degree-3..5 Taylor coefficients come
+// from the constant bank (DFMA c[] operands instead of UMOV pairs).
+__constant__ double c_exp_tab_poly[3] = {0x1.1111111111111p-7, 0x1.5555555555555p-5, 0x1.5555555555555p-3};
+
+__device__ __forceinline__ double exp_neg_tab_bf(double x, const double* __restrict__ tab) {
+  x = x < 745.0 ? x : 745.0;
+  const double t = fma(-x, c_exp_tab_consts[0], c_exp_tab_consts[1]);
+  const double n = t - c_exp_tab_consts[1];
+  double gg = fma(n, -c_exp_tab_consts[2], -x);
+  gg = fma(n, -c_exp_tab_consts[3], gg);
+  double p = fma(gg, c_exp_tab_poly[0], c_exp_tab_poly[1]);
+  p = fma(p, gg, c_exp_tab_poly[2]);
+  p = fma(p, gg, 0.5);
+  p = fma(p, gg, 1.0);
+  p = fma(p, gg, 1.0);
+  const int ni = __double2loint(t);
+  const int m = ni >> 6, m1 = m >> 1, m2 = m - m1;
+  const double s1 = __hiloint2double((m1 + 1023) << 20, 0), s2 = __hiloint2double((m2 + 1023) << 20, 0);
+  return ((tab[ni & 63] * p) * s1) * s2;
+}
+
+// sqrt of x > 0 (no zero select: callers pass r^2 + 1e-300, which equals r^2 for every
+// r^2 above ~1e-284 and keeps rsqrt finite at r = 0)
+__device__ __forceinline__ double sqrt_pos(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  y = y * fma(-0.5 * x, y * y, 1.5);
+  const double r = x * y;
+  return fma(0.5 * y, fma(-r, r, x), r);
+}
+
 // branch-free sqrt: MUFU.RSQ64H seed, two Newton steps on 1/sqrt, one on sqrt (~1 ulp);
 // sqrt(0) = 0 by a select (libm sqrt branches to a slow path per element)
 __device__ __forceinline__ double sqrt_fast(double x) {
