@@ -155,8 +155,9 @@ __global__ void __launch_bounds__(BT, 1)
   double* sX = sAlpha + k;
   double* KV = smem + head;                     // KP x VSTR
   double* sMu = KV + (int64_t)KP * VSTR;        // NVP
-  double* sT = sMu + NVP;                       // k x 16: separable squared offsets (phase 1)
-  double* sExp = sT + 16 * (int64_t)k;          // 64: 2^(j/64) for exp_neg_tab
+  const int k16 = (k + 15) & ~15;               // sT rows: k rounded up to 16 (zero padding)
+  double* sT = sMu + NVP;                       // k16 x 16: separable squared offsets (phase 1)
+  double* sExp = sT + 16 * (int64_t)k16;        // 64: 2^(j/64) for exp_neg_tab
   __shared__ int64_t s_r0;
   __shared__ int s_skip;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -212,10 +213,10 @@ __global__ void __launch_bounds__(BT, 1)
       // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding.
       // r^2 is separable over the lattice: T[j][5d + t] = ((x_jd - v_d(t)) / l_d)^2 for the
       // 5 lattice positions t per axis d, then r^2 = (T_x + T_y) + T_z per element.
-      for (int e = tid; e < 15 * k; e += BT) {
+      for (int e = tid; e < 15 * k16; e += BT) {
         const int j = e / 15, col = e - 15 * j, d = col / 5, t = col - 5 * d;
         const int c0 = d == 0 ? i0 : (d == 1 ? j0 : k0);
-        const double diff = (sX[d * k + j] - vpos(g, d, min(c0 + t, g.cells[d]))) * a.kp.inv_ls[d];
+        const double diff = j < k ? (sX[d * k + j] - vpos(g, d, min(c0 + t, g.cells[d]))) * a.kp.inv_ls[d] : 0.0;
         sT[16 * j + col] = diff * diff;
       }
       __syncthreads();
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(BT, 1)
             double val[P1_UNROLL];
 #pragma unroll
             for (int u = 0; u < P1_UNROLL; ++u) {
-              const double* tj = sT + 16 * min(jb + RS * u, k - 1);
+              const double* tj = sT + 16 * (jb + RS * u);   // rows up to k16: padding zeros
               val[u] = kval((tj[ta] + tj[tb]) + tj[tc]);
             }
 #pragma unroll
@@ -468,7 +469,7 @@ static BrickArgs brick_args(const Ctx& c) {
 static size_t brick_smem(int k) {
   const int kp8 = (k + 7) & ~7;
   const int64_t head = (la_size(k) + 4 * (int64_t)k + 1) & ~1ll;
-  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP + 16 * (int64_t)k + 64);
+  return sizeof(double) * (head + (int64_t)kp8 * VSTR + NVP + 16 * (int64_t)((k + 15) & ~15) + 64);
 }
 
 bool fused_brick_supported(const Ctx& c) {
