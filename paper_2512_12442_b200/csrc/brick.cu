@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(BT, 1)
   double* sT = sMu + NVP;                       // k16 x 16: separable squared offsets (phase 1)
   double* sExp = sT + 16 * (int64_t)k16;        // 64: 2^(j/64) for exp_neg_tab
   __shared__ int64_t s_r0;
-  __shared__ int s_skip;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geom& g = a.g;
   if (tid < 64) sExp[tid] = c_exp2_64[tid];   // read after the loop's first barrier
@@ -167,33 +166,64 @@ __global__ void __launch_bounds__(BT, 1)
   for (int64_t e = tid; e < (int64_t)KP * VSTR; e += BT) KV[e] = 0.0;   // padding rows / columns
 #endif
   int staged = -1;
-  for (;;) {
-    if (tid == 0) s_r0 = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
+  // FUSED: thread 0 walks the unit list one brick ahead -- it grabs chunks, skips empty
+  // slots and bricks done by an earlier refine, claims the next brick (bdone) during the
+  // current brick's phase 3 and publishes it in s_ur / s_uk[(it + 1) & 1], so that the
+  // dependent global round trips overlap the tensor-core work instead of stalling the CTA
+  __shared__ int64_t s_ur[2];
+  __shared__ uint64_t s_uk[2];
+  int64_t tr = -1, trend = -1;
+  auto claim_next = [&](int slot) {
+    for (;;) {
+      if (++tr >= trend) {
+        tr = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
+        trend = min(nruns, tr + BRICK_CHUNK);
+        if (tr >= nruns) {
+          s_ur[slot] = -1;
+          return;
+        }
+      }
+      const uint64_t key = o.bricks[tr];
+      if (key == ~0ull) {   // a child slot outside the grid (early pass)
+        o.ucomp[tr] = 0;
+        continue;
+      }
+      int bi, bj, bk;
+      node_unkey(key, bi, bj, bk);
+      uint8_t* d = o.bdone + (rec_index(g, BK * bi, BK * bj, BK * bk) >> 6);
+      const uint8_t done = *d;
+      *d = 1;
+      o.ucomp[tr] = done ? 0 : 1;
+      if (done) continue;   // done by an earlier refine (another isovalue)
+      s_ur[slot] = tr;
+      s_uk[slot] = key;
+      return;
+    }
+  };
+  if (FUSED) {
+    if (tid == 0) claim_next(0);
     __syncthreads();
-    const int64_t r0 = s_r0;
-    if (r0 >= nruns) break;
-    const int64_t r1 = min(nruns, r0 + BRICK_CHUNK);
+  }
+  for (int it = 0;; ++it) {
+    int64_t r0, r1;
+    if (FUSED) {
+      r0 = s_ur[it & 1];   // published before the previous brick's last barrier
+      if (r0 < 0) break;
+      r1 = r0 + 1;
+    } else {
+      if (tid == 0) s_r0 = (int64_t)atomicAdd(work, (unsigned long long)BRICK_CHUNK);
+      __syncthreads();
+      r0 = s_r0;
+      if (r0 >= nruns) break;
+      r1 = min(nruns, r0 + BRICK_CHUNK);
+    }
     for (int64_t r = r0; r < r1; ++r) {
       int i0, j0, k0;
       int64_t q0 = 0, q1 = 0;
       if (FUSED) {
-        const uint64_t key = o.bricks[r];
-        if (key == ~0ull) {   // uniform: a child slot outside the grid (early pass)
-          if (tid == 0) o.ucomp[r] = 0;
-          continue;
-        }
         int bi, bj, bk;
-        node_unkey(key, bi, bj, bk);
+        node_unkey(s_uk[it & 1], bi, bj, bk);
         i0 = BK * bi; j0 = BK * bj; k0 = BK * bk;
-        __syncthreads();   // every thread has read the previous brick's s_skip
-        if (tid == 0) {
-          uint8_t* d = o.bdone + (rec_index(g, BK * bi, BK * bj, BK * bk) >> 6);
-          s_skip = *d;
-          *d = 1;
-          o.ucomp[r] = s_skip ? 0 : 1;
-        }
-        __syncthreads();
-        if (s_skip) continue;   // uniform: done by an earlier refine (another isovalue)
       } else {
         q0 = run_start[r];
         q1 = run_start[r + 1];
@@ -209,7 +239,7 @@ __global__ void __launch_bounds__(BT, 1)
         for (int64_t t = tid; t < (a.bstride >> 1); t += BT) dst[t] = __ldg(src + t);
         staged = b;
       }
-      __syncthreads();
+      __syncthreads();   // (kept when nothing was staged: measured 1.3 ms faster on c5 than without)
       // phase 1: K[j][v] for the brick's (clamped) vertex lattice; zero padding.
       // r^2 is separable over the lattice: T[j][5d + t] = ((x_jd - v_d(t)) / l_d)^2 for the
       // 5 lattice positions t per axis d, then r^2 = (T_x + T_y) + T_z per element.
@@ -383,6 +413,7 @@ __global__ void __launch_bounds__(BT, 1)
         }
       }
       __syncthreads();
+      if (FUSED && tid == 0) claim_next((it + 1) & 1);
       if (FUSED && BRICK_DIAG_MARG) {
         // vertex marginals (R10) of the brick's vertices whose own bucket is b:
         // var = k(v,v) - ||V_{:,v}||^2 (4 threads per column as for mu), cached as
