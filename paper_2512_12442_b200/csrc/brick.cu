@@ -55,15 +55,6 @@ constexpr int P1_UNROLL = BT >= 1024 ? 2 : 4;
 #ifndef BRICK_DIAG_SIGMA
 #define BRICK_DIAG_SIGMA 1
 #endif
-#ifndef BRICK_SOLVE_V2      // the DMMA solve with precomputed 32-bit shared addresses
-#define BRICK_SOLVE_V2 2
-#endif
-#ifndef BRICK_SIGMA_CHAINS  // accumulator chains per cell in the Sigma products
-#define BRICK_SIGMA_CHAINS 2
-#endif
-#ifndef BRICK_P1_V2         // branch-free phase-1 kernel values
-#define BRICK_P1_V2 1
-#endif
 #ifndef BRICK_DIAG_MU       // 0: skip the mu dot
 #define BRICK_DIAG_MU 1
 #endif
@@ -81,14 +72,6 @@ __device__ __forceinline__ double kern_from_r2_fast(const KernParams& p, double 
   const double s5 = SQRT5 * r;
   return p.var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_fast(s5);
 }
-// the same with the table exp (k_brick: the table sits in its shared memory)
-__device__ __forceinline__ double kern_from_r2_tab(const KernParams& p, double r2, const double* __restrict__ tab) {
-  if (p.kind == LCP_K_SE) return p.var * exp_neg_tab(0.5 * r2, tab);
-  const double r = sqrt_fast(r2);
-  const double s5 = SQRT5 * r;
-  return p.var * (1.0 + s5 + (5.0 / 3.0) * r2) * exp_neg_tab(s5, tab);
-}
-
 struct BrickArgs {
   KernParams kp;
   Geom g;
@@ -165,9 +148,7 @@ __global__ void __launch_bounds__(BT, 1)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const Geom& g = a.g;
   if (tid < 64) sExp[tid] = c_exp2_64[tid];   // read after the loop's first barrier
-#if BRICK_P1_V2
   for (int64_t e = tid; e < (int64_t)KP * VSTR; e += BT) KV[e] = 0.0;   // padding rows / columns
-#endif
   int staged = -1;
   // FUSED: thread 0 walks the unit list one brick ahead -- it grabs chunks, skips empty
   // slots and bricks done by an earlier refine, claims the next brick (bdone) during the
@@ -253,7 +234,6 @@ __global__ void __launch_bounds__(BT, 1)
         sT[16 * j + col] = diff * diff;
       }
       __syncthreads();
-#if BRICK_P1_V2
       {
         // branch-free kernel values (the kernel kind hoisted out of the loop, exp_neg_tab_bf
         // without the underflow branch, sqrt of r^2 + 1e-300 without the zero select) so
@@ -295,26 +275,6 @@ __global__ void __launch_bounds__(BT, 1)
         }
 #endif
       }
-#else
-      {
-        const int v = tid & (NVP - 1);
-        const int va = v % (BK + 1), vb = (v / (BK + 1)) % (BK + 1), vc = v / ((BK + 1) * (BK + 1));
-        const bool vok = v < NVB;
-        // straight-line body (clamped indices, 0/1 mask) so that the unrolled copies
-        // interleave: the Horner chains of exp are latency-bound one at a time
-        const int ta = vok ? va : 0, tb = vok ? 5 + vb : 5, tc = vok ? 10 + vc : 10;
-#pragma unroll P1_UNROLL
-        for (int j = tid >> 7; j < KP; j += BT / NVP) {
-          const double* tj = sT + 16 * min(j, k - 1);
-#if BRICK_DIAG_K
-          const double val = fma((tj[ta] + tj[tb]) + tj[tc], -1e-3, a.kp.var);
-#else
-          const double val = kern_from_r2_tab(a.kp, (tj[ta] + tj[tb]) + tj[tc], sExp);
-#endif
-          KV[(int64_t)j * VSTR + v] = (j < k && vok) ? val : 0.0;
-        }
-      }
-#endif
       __syncthreads();
       {
         // mu_v = m0 + sum_j K[j][v] alpha_j: 4 threads per vertex column (rows j = part
@@ -343,7 +303,6 @@ __global__ void __launch_bounds__(BT, 1)
       for (int t = 0; t < TPW; ++t)
         if (rtile(t) < nrt) last_rt = max(last_rt, rtile(t));
       const int jend = (last_rt < 0 || !BRICK_DIAG_SOLVE) ? 0 : min(KP, 8 * last_rt + 8);
-#if BRICK_SOLVE_V2 == 2
       // row tile by row tile: one A pointer live at a time (the accumulators of all four
       // tiles stay in registers until the write-back), B fragments re-read per tile
       const uint32_t kv_s = (uint32_t)__cvta_generic_to_shared(KV) + 8u * (lc * VSTR + 32 * cb + lr);
@@ -361,49 +320,6 @@ __global__ void __launch_bounds__(BT, 1)
           for (int u = 0; u < 4; ++u) dmma(af, lds_f64(kb + 64u * u), acc[t][u][0], acc[t][u][1]);
         }
       }
-#elif BRICK_SOLVE_V2
-      // 32-bit shared addresses computed once: the A fragment of (rt, js) sits at
-      // la_block(rt, 0) + 32 js doubles, the B fragments of k-step j at row j + lc; a row
-      // tile takes part while j < 8 rt + 8 (the nonzero blocks of L^-1)
-      const uint32_t kv_s = (uint32_t)__cvta_generic_to_shared(KV) + 8u * (lc * VSTR + 32 * cb + lr);
-      const uint32_t la_s = (uint32_t)__cvta_generic_to_shared(sLA) + 8u * lane;
-      uint32_t pa[TPW];
-      int jlim[TPW];
-#pragma unroll
-      for (int t = 0; t < TPW; ++t) {
-        const int rt = rtile(t);
-        jlim[t] = rt < nrt ? 8 * rt + 8 : 0;
-        pa[t] = la_s + 8u * (uint32_t)la_block(rt < nrt ? rt : 0, 0);
-      }
-      for (int j = 0; j < jend; j += 4) {
-        const uint32_t kb = kv_s + 8u * VSTR * j;
-        double bf[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) bf[u] = lds_f64(kb + 64u * u);
-#pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          if (j >= jlim[t]) continue;   // warp-uniform: zero block of L^-1
-          const double af = lds_f64(pa[t] + 64u * j);   // + 32 js doubles, js = j / 4
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
-        }
-      }
-#else
-      for (int j = 0; j < jend; j += 4) {
-        const int jj = j + lc;
-        double bf[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) bf[u] = KV[(int64_t)jj * VSTR + 32 * cb + 8 * u + lr];
-#pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          const int rt = rtile(t);
-          if (rt >= nrt || 8 * rt + 7 < j) continue;   // warp-uniform: zero block of L^-1
-          const double af = sLA[la_block(rt, j >> 2) + lane];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dmma(af, bf[u], acc[t][u][0], acc[t][u][1]);
-        }
-      }
-#endif
       __syncthreads();   // every warp has read K
 #pragma unroll
       for (int t = 0; t < TPW; ++t) {
@@ -462,7 +378,6 @@ __global__ void __launch_bounds__(BT, 1)
         const int cr = lr;   // corner of this lane's A row / B column
         const int lv = (xi - i0 + (cr & 1)) + (BK + 1) * ((xj - j0 + ((cr >> 1) & 1)) + (BK + 1) * (xk - k0 + (cr >> 2)));
         double d0 = 0.0, d1 = 0.0;
-#if BRICK_SIGMA_CHAINS == 2
         {
           // two independent accumulator chains (even / odd k-steps), summed at the end
           // (c5 brick pass 401.8 -> 394.9 ms; four chains: 407 ms)
@@ -482,12 +397,6 @@ __global__ void __launch_bounds__(BT, 1)
           d0 += e0;
           d1 += e1;
         }
-#else
-        for (int s = 0; s < (BRICK_DIAG_SIGMA ? KP : 0); s += 4) {
-          double v = KV[(int64_t)(s + lc) * VSTR + lv];
-          dmma(v, v, d0, d1);
-        }
-#endif
         double* rec = o.post + 44 * slot;
         // lane holds D[cr][2 lc], D[cr][2 lc + 1]
         const int c0 = 2 * lc, c1 = 2 * lc + 1;
