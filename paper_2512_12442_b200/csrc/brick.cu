@@ -29,8 +29,8 @@ constexpr int NVP = 128;                    // padded vertex columns
 // fall on disjoint bank octets within each half-warp phase (conflict-free).
 constexpr int VSTR = 132;
 constexpr int BRICK_THREADS = 512;          // 16 warps = 4 row sets x 4 column blocks of 32
-#ifndef BRICK_CHUNK_N
-#define BRICK_CHUNK_N 4
+#ifndef BRICK_CHUNK_N   // 8: a bucket block is staged once per 8 bricks (c5 brick pass 389.3 -> 387.2 ms; 16: 388.5)
+#define BRICK_CHUNK_N 8
 #endif
 constexpr int BRICK_CHUNK = BRICK_CHUNK_N;  // runs grabbed per atomic
 // k_brick's CTA: BT threads = 4 column blocks x NRS row sets of warps; mu / variance dots

@@ -18,6 +18,9 @@
 
 namespace lcp {
 
+#ifndef PMC_SCALAR_LZ   // 1: scalar FFMA chains for the phase-1 L'z instead of FFMA2
+#define PMC_SCALAR_LZ 0
+#endif
 #ifndef PMC_ABS_LG2
 #define PMC_ABS_LG2 1
 #endif
@@ -386,6 +389,31 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     float z[4];
     upk(zA, z[0], z[1]);
     upk(zB, z[2], z[3]);
+    float y[4], lo[4], hi[4];
+#if PMC_SCALAR_LZ
+    // scalar FFMA chains, the same roundings in the same order as the FFMA2 form
+    y[0] = fmaf(L[0], z[0], m[0]);
+    y[1] = fmaf(L[2], z[1], fmaf(L[1], z[0], m[1]));
+    y[2] = m[2];
+    y[3] = m[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      y[2] = fmaf(L[3 + d], z[d], y[2]);
+      y[3] = fmaf(L[6 + d], z[d], y[3]);
+    }
+    y[3] = fmaf(L33, z[3], y[3]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) lo[c] = mB[c];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      lo[0] = fmaf(L[10 + d], z[d], lo[0]);
+      lo[1] = fmaf(L[15 + d], z[d], lo[1]);
+      lo[2] = fmaf(L[21 + d], z[d], lo[2]);
+      lo[3] = fmaf(L[28 + d], z[d], lo[3]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) hi[c] = fmaf(2.0f, B[c], lo[c]);
+#else
     f2_t A01 = ffma2(P01, pk(z[0], z[0]), M01);
     f2_t A23 = M23, A45 = MB45, A67 = MB67;
 #pragma unroll
@@ -395,7 +423,6 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
       A45 = ffma2(P45[d], zd, A45);
       A67 = ffma2(P67[d], zd, A67);
     }
-    float y[4], lo[4], hi[4];
     upk(A01, y[0], y[1]);
     upk(A23, y[2], y[3]);
     y[1] = fmaf(L11, z[1], y[1]);
@@ -404,6 +431,7 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     upk(A67, lo[2], lo[3]);
     upk(ffma2(TWO, B45, A45), hi[0], hi[1]);
     upk(ffma2(TWO, B67, A67), hi[2], hi[3]);
+#endif
     // 3-input chains (FMNMX3)
     const float mx03 = fmaxf(fmaxf(fmaxf(y[0], y[1]), y[2]), y[3]);
     const float mn03 = fminf(fminf(fminf(y[0], y[1]), y[2]), y[3]);
