@@ -29,11 +29,13 @@ sys.path.insert(0, ROOT)
 METRIC = "PMC LCP cells/sec"
 UNIT = "cells/s"
 # minimal op mix of the two-phase k_pmc, in issue slots (lane-ops):
-#   phase 1, every sample : Philox4x32-10 40, 2 Box-Muller pairs 20 (8 MUFU),
-#                           partial L z 26 FFMA, bounds 8, min/max 12, decision 5, queue 3  = 114
+#   phase 1, every sample : 3/4 of a Philox4x32-10 block 30 (R13c: 3 blocks per 4 samples),
+#                           top-byte gather 2 PRMT, 2 Box-Muller pairs 20 (8 MUFU),
+#                           partial L z 26 FFMA, bounds 8, min/max 12, decision 5, queue 3  = 106
+#                           (cuobjdump -sass of k_pmc<1>: 429 instructions per 128-sample group)
 #   phase 2, queued sample: Philox 40, 2 Box-Muller pairs 20, 10 FFMA, min/max 6,
 #                           decision 3, queue store + load 14                              =  93
-OPS_PHASE1 = 114
+OPS_PHASE1 = 106
 OPS_PHASE2 = 93
 # each further isovalue of a fused pass (k_pmc<T>, cuobjdump -sass: 271 vs 210 instructions per
 # two-sample phase-1 iteration at T = 3 vs 1): + 15 per sample; its crossing test in phase 2: + 4
@@ -501,7 +503,7 @@ def run_ours(args):
                 "ops_per_sample": ops_survey / samples_step if samples_step else None,
                 "ops_note": ("achieved = samples x SURVEY.md 8(d) minimal op mix (186 issue slots per "
                              "sample, +21 per extra fused isovalue) / summed k_pmc time; the two-phase "
-                             "kernel executes fewer: frac_impl_mix uses its own fixed mix (114 per "
+                             "kernel executes fewer: frac_impl_mix uses its own fixed mix (106 per "
                              "sample + 93 per phase-2 sample)"),
                 "frac_impl_mix": (impl_mix / peak) if impl_mix else None,
                 "impl_ops_per_sample": ops_step / samples_step if samples_step else None,

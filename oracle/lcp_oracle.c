@@ -638,23 +638,44 @@ void orc_philox4x32_10(const uint32_t* ctr, const uint32_t* key, uint32_t* out) 
 /* uniform from the low 23 bits: u = (r mod 2^23 + 1/2) 2^-23 in [2^-24, 1 - 2^-24] (R13) */
 static double u23(uint32_t r) { return ((double)(r & 0x7FFFFFu) + 0.5) * (1.0 / 8388608.0); }
 
-/* counter = (cell lo32, iso_index, cell hi32, 2s + j), key = (seed lo32, seed hi32)
- * (R13; the paper fixes no RNG); Box-Muller pairs (u_a, u_b):
- * R = sqrt(-2 ln u_a), (R cos 2 pi u_b, R sin 2 pi u_b). */
+static void bm_pair(uint32_t ra, uint32_t rb, double* z) {
+    double ua = u23(ra), ub = u23(rb);
+    double R = sqrt(-2.0 * log(ua));
+    z[0] = R * cos(2.0 * ORC_PI * ub);
+    z[1] = R * sin(2.0 * ORC_PI * ub);
+}
+
+/* key = (seed lo32, seed hi32); counters (cell lo32, iso_index, cell hi32, w) (R13; the paper
+ * fixes no RNG).  Box-Muller pairs (u_a, u_b): R = sqrt(-2 ln u_a),
+ * (R cos 2 pi u_b, R sin 2 pi u_b).
+ * z0..z3 (R13c): sample s belongs to group g = 32 floor(s / 128) + (s mod 32) at position
+ * t = floor(s / 32) mod 4; the group's word stream is the 12 words of the Philox blocks with
+ * w = 2 (3 g + j), j = 0, 1, 2 (word i = word i mod 4 of block floor(i / 4)), and the sample
+ * takes stream words 3t, 3t+1, 3t+2 = (A, B, C): (z0, z1) from (u(A), u(C)), (z2, z3) from
+ * (u(B), u(D)), D = (A >> 24) | (B >> 24) << 8 | (C >> 24) << 16 -- four 23-bit uniforms from
+ * disjoint bits of three words.
+ * z4..z7: the block with w = 2s + 1, pairs (word 0, word 1) and (word 2, word 3).          */
 void orc_normals8(uint64_t seed, int64_t cell, uint32_t iso_index, int64_t s, double* z) {
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-    for (int j = 0; j < 2; ++j) {
+    const int64_t g = 32 * (s / 128) + s % 32, t = (s / 32) % 4;
+    uint32_t w3[3];
+    for (int i = 0; i < 3; ++i) {
+        const int64_t wi = 3 * t + i;   /* stream word index */
         uint32_t ctr[4] = {(uint32_t)(uint64_t)cell, iso_index, (uint32_t)((uint64_t)cell >> 32),
-                           (uint32_t)(2 * s + j)};
+                           (uint32_t)(2 * (3 * g + wi / 4))};
         uint32_t r[4];
         orc_philox4x32_10(ctr, key, r);
-        for (int p = 0; p < 2; ++p) {
-            double ua = u23(r[2 * p]), ub = u23(r[2 * p + 1]);
-            double R = sqrt(-2.0 * log(ua));
-            z[4 * j + 2 * p] = R * cos(2.0 * ORC_PI * ub);
-            z[4 * j + 2 * p + 1] = R * sin(2.0 * ORC_PI * ub);
-        }
+        w3[i] = r[wi % 4];
     }
+    const uint32_t d = (w3[0] >> 24) | ((w3[1] >> 24) << 8) | ((w3[2] >> 24) << 16);
+    bm_pair(w3[0], w3[2], z);
+    bm_pair(w3[1], d, z + 2);
+    uint32_t ctr[4] = {(uint32_t)(uint64_t)cell, iso_index, (uint32_t)((uint64_t)cell >> 32),
+                       (uint32_t)(2 * s + 1)};
+    uint32_t r[4];
+    orc_philox4x32_10(ctr, key, r);
+    bm_pair(r[0], r[1], z + 4);
+    bm_pair(r[2], r[3], z + 6);
 }
 
 /* ----------------------------------------------------------------- C11 --- */

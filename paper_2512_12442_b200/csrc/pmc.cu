@@ -3,8 +3,10 @@
 //  a7  cell posterior (marginals.cu: k_cell_posterior), cells grouped by bucket
 //  a8  k_chol8 : 8x8 Cholesky of Sigma in FP64 with the PSD pivot clamp (R14)
 //      k_pmc   : warp per cell; lane l draws samples s = l, l+32, ...:
-//                Philox4x32-10 on counter (cell lo, iso, cell hi, 2s+j), key =
-//                seed (R13); uniforms from the low 23 bits; Box-Muller; y = mu +
+//                Philox4x32-10, key = seed, counter (cell lo, iso, cell hi, w) (R13):
+//                z0..z3 from three words of the lane group's stream (w = 2 (3g + j),
+//                R13c), z4..z7 from w = 2s + 1; uniforms from the low 23 bits
+//                (and the top bytes); Box-Muller; y = mu +
 //                L z in FP32; crossing = not all y < th and not all y > th
 //                (R5, R24).  LCP = count / N.
 //  a9  k_scatter : dense field, zero off the leaves.
@@ -12,6 +14,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "chol8.cuh"
 #include "ctx.h"
@@ -250,10 +253,10 @@ constexpr float ZMAX = 5.7684f;
 #ifndef PMC_WARPS
 #define PMC_WARPS 1
 #endif
-#ifndef PMC_ILP
+#ifndef PMC_ILP   // 2: two samples per lane in flight (T <= 4); 1: one (T > 4 always)
 #define PMC_ILP 2
 #endif
-constexpr int QCAP = PMC_ILP >= 4 ? 160 : 96;   // pending samples per warp (< 32 + ILP pushes of 32)
+constexpr int QCAP = 96;            // pending samples per warp (< 32 + 2 pushes of 32)
 constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are branch-free
 
 // k_pmc<T>: exact two-phase evaluation of the PMC count for
@@ -261,7 +264,8 @@ constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are 
 // Corner values are taken relative to the first isovalue, m_c = mu_c - th_0
 // (FP64 difference rounded once); isovalue t is the offset dl_t = th_t - th_0
 // (dl_0 = 0), and a sample crosses t iff min_c y_c <= dl_t <= max_c y_c.
-// Phase 1 draws the first Philox block (normals z0..z3) of sample s and forms
+// Phase 1 takes the sample's three words of its lane group's phase-1 word stream
+// (normals z0..z3, R13c: three Philox blocks serve four samples) and forms
 // y_c exactly for the first four corners and y_c - R_c for the other four,
 // where |R_c| = |sum_{d>=4} L_cd z_d| <= B_c = ZMAX sum_{d>=4} |L_cd| (+ rounding
 // slack).  That brackets max_c y_c in [LMX, UMX] and min_c y_c in [LMN, UMN].
@@ -271,8 +275,11 @@ constexpr int QROWS = QCAP + 32;    // + a trash row per lane: queue stores are 
 // block (z4..z7), finishes the sample and counts every isovalue exactly.  Every
 // sample is decided exactly as the one-pass FP32 evaluation decides it; the
 // count is the same estimator.
+// register bound: at least PMC_MINBLOCKS one-warp CTAs per SM for T <= 8 (70 registers, 28 warps;
+// with R13c's packed words: 79.0 ms per c5 chunk against 81.3 at 94 registers and 79.9 at 80),
+// 8 for T = 12, 16 (whose isovalue counters would spill at 70)
 #ifndef PMC_MINBLOCKS
-#define PMC_MINBLOCKS 8
+#define PMC_MINBLOCKS 26
 #endif
 #ifndef PMC_QUEUE_PRED
 #define PMC_QUEUE_PRED 0
@@ -288,7 +295,7 @@ struct IsoOffsets {
 };
 
 template <int T>
-__global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
+__global__ void __launch_bounds__(PMC_WARPS * 32, (T <= 8 ? PMC_MINBLOCKS : 8))
     k_pmc(const Geom g, const int64_t* __restrict__ cells, const double* __restrict__ post, int64_t rec_stride,
           int rec_by_morton,
           int64_t n, double theta, const IsoOffsets D, uint32_t N, const PhiloxKeys K, uint32_t iso, const uint32_t* __restrict__ mask,
@@ -380,12 +387,12 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
   // phase 1 of sample s: returns true (and the stash) if the sample is undecided.
   // y_c for c < 4 exactly; lo_c = y_c - B_c - R_c and hi_c = lo_c + 2 B_c for c >= 4.
   // Same FP32 operations in the same order as the scalar chains y = fma(L'_cd, z_d, y).
-  auto phase1 = [&](uint32_t s, float4& st0, float4& st1) -> bool {
-    uint32_t r0, r1, r2, r3;
-    // counter (cell lo, iso, cell hi, 2s + j) (R13): the sample word enters round 1
-    // only through an XOR, so rounds 1-3 need 2 varying IMAD.WIDE instead of 4
-    philox4x32_10(c1, iso, c2, 2u * s, K, r0, r1, r2, r3);
-    const f2_t zA = box_muller2(r0, r1, ONE), zB = box_muller2(r2, r3, ONE);
+  // phase 1 of sample s from its three words (A, B, C) of the group's word stream (R13c):
+  // (z0, z1) = BM(u(A), u(C)), (z2, z3) = BM(u(B), u(A[24..31] | B[24..31] << 8 | C[24..31] << 16))
+  auto phase1w = [&](uint32_t s, uint32_t wa, uint32_t wb, uint32_t wc, bool valid, float4& st0,
+                     float4& st1) -> bool {
+    const uint32_t wd = __byte_perm(__byte_perm(wa, wb, 0x0073), wc, 0x0710);
+    const f2_t zA = box_muller2(wa, wc, ONE), zB = box_muller2(wb, wd, ONE);
     float z[4];
     upk(zA, z[0], z[1]);
     upk(zB, z[2], z[3]);
@@ -447,13 +454,13 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
       cross[t] = lo_max >= d && hi_min <= d;
       decided = decided && (hi_max < d || lo_min > d || cross[t]);
     }
-    if (decided) {
+    if (decided && valid) {
 #pragma unroll
       for (int t = 0; t < T; ++t) cnt[t] += cross[t] ? 1u : 0u;
     }
     st0 = make_float4(lo[0], lo[1], lo[2], lo[3]);
     st1 = make_float4(mx03, mn03, __uint_as_float(s), 0.0f);
-    return !decided;
+    return !decided && valid;
   };
   // phase-2 operands: columns 4..7 of corners 4..7
   const f2_t Q45[1] = {pk(L[14], L[19])};
@@ -537,36 +544,53 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, PMC_MINBLOCKS)
     }
   };
   uint32_t base = 0;
-  // four / two samples per lane per iteration (instruction-level parallelism)
-  for (; ILP == 4 && base + 128u <= Nl; base += 128u) {
-    float4 a0, a1, b0, b1, c0, c1_, d0, d1;
-    const bool pa = phase1(base + lane, a0, a1);
-    const bool pb = phase1(base + 32u + lane, b0, b1);
-    const bool pc = phase1(base + 64u + lane, c0, c1_);
-    const bool pd = phase1(base + 96u + lane, d0, d1);
-    push2(pa, a0, a1, pb, b0, b1);
-    push2(pc, c0, c1_, pd, d0, d1);
-    drain();
-    drain();
-    drain();
-    drain();
-  }
-  for (; ILP >= 2 && base + 64u <= Nl; base += 64u) {
-    float4 a0, a1, b0, b1;
-    const bool pa = phase1(base + lane, a0, a1);
-    const bool pb = phase1(base + 32u + lane, b0, b1);
-    push2(pa, a0, a1, pb, b0, b1);
-    drain();
-    drain();
-  }
-  for (; base < Nl; base += 32u) {
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
-    const uint32_t s = base + lane;
-    bool pa = false;
-    if (s < Nl) pa = phase1(s, a0, a1);
-    push(pa, a0, a1);
-    drain();
-  }
+  // R13c: lane l takes the samples s = 128 h + l + 32 t, t = 0..3, of its group g = 32 h + l;
+  // the group's phase-1 words are the 12 words of three Philox blocks with counters
+  // (cell lo, iso, cell hi, 2 (3 g + j)), j = 0, 1, 2, and sample t takes words 3t..3t+2
+  // (3 words = 4 uniforms of 23 bits: 3 Philox blocks per 4 samples instead of 4)
+  auto group = [&](auto FULL) {
+    constexpr bool full = decltype(FULL)::value;
+    const uint32_t g = (base >> 2) + lane;   // 32 (base / 128) + lane
+    uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+    philox4x32_10(c1, iso, c2, 2u * (3u * g), K, a0, a1, a2, a3);
+    philox4x32_10(c1, iso, c2, 2u * (3u * g + 1u), K, b0, b1, b2, b3);
+    float4 x0, x1, y0, y1;
+    {
+      const uint32_t sa = base + lane, sb = sa + 32u;
+      const bool pa = phase1w(sa, a0, a1, a2, full || sa < Nl, x0, x1);
+      const bool pb = phase1w(sb, a3, b0, b1, full || sb < Nl, y0, y1);
+      if (ILP >= 2) {
+        push2(pa, x0, x1, pb, y0, y1);
+        drain();
+        drain();
+      } else {
+        push(pa, x0, x1);
+        drain();
+        push(pb, y0, y1);
+        drain();
+      }
+    }
+    if (!full && base + 64u >= Nl) return;
+    uint32_t e0, e1, e2, e3;
+    philox4x32_10(c1, iso, c2, 2u * (3u * g + 2u), K, e0, e1, e2, e3);
+    {
+      const uint32_t sc = base + 64u + lane, sd = sc + 32u;
+      const bool pc = phase1w(sc, b2, b3, e0, full || sc < Nl, x0, x1);
+      const bool pd = phase1w(sd, e1, e2, e3, full || sd < Nl, y0, y1);
+      if (ILP >= 2) {
+        push2(pc, x0, x1, pd, y0, y1);
+        drain();
+        drain();
+      } else {
+        push(pc, x0, x1);
+        drain();
+        push(pd, y0, y1);
+        drain();
+      }
+    }
+  };
+  for (; base + 128u <= Nl; base += 128u) group(std::true_type{});
+  if (base < Nl) group(std::false_type{});   // a partial group: samples s >= N neither count nor queue
   if (qn > 0) {
     __syncwarp();
     phase2(lane, lane < qn);

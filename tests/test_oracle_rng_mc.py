@@ -66,18 +66,43 @@ def test_philox_vs_curand_host(tmp_path):
     assert n == 200
 
 
-def test_normals_layout_and_uniform_map():
-    # counter = (cell lo, iso, cell hi, 2s + j), key = (seed lo, seed hi); u from low 23 bits
-    seed, cell, iso, s = 0x1234567890ABCDEF, (7 << 32) + 99, 2, 5
+def _bm(ra, rb):
+    ua, ub = [((int(x) & 0x7FFFFF) + 0.5) / 2 ** 23 for x in (ra, rb)]
+    R = math.sqrt(-2 * math.log(ua))
+    return R * math.cos(2 * math.pi * ub), R * math.sin(2 * math.pi * ub)
+
+
+@pytest.mark.parametrize("s", [0, 5, 37, 70, 101, 127, 128, 300, 4095])
+def test_normals_layout_and_uniform_map(s):
+    # DESIGN R13 / R13c, written out from the text: key = (seed lo, seed hi); u from the low 23
+    # bits.  z0..z3: group g = 32 (s div 128) + s mod 32, position t = (s div 32) mod 4; the
+    # group's word stream = the 12 words of the blocks with counter word 3 = 2 (3g + j), j < 3;
+    # the sample takes stream words 3t..3t+2 = (A, B, C): (z0, z1) = BM(A, C),
+    # (z2, z3) = BM(B, top bytes of A, B, C).  z4..z7: block 2s + 1, pairs (0, 1), (2, 3).
+    seed, cell, iso = 0x1234567890ABCDEF, (7 << 32) + 99, 2
     z = O.normals8(seed, cell, iso, s)
     key = [seed & 0xFFFFFFFF, seed >> 32]
-    for j in range(2):
-        r = O.philox4x32_10([cell & 0xFFFFFFFF, iso, cell >> 32, 2 * s + j], key)
-        u = [((int(x) & 0x7FFFFF) + 0.5) / 2 ** 23 for x in r]
-        for p in range(2):
-            R = math.sqrt(-2 * math.log(u[2 * p]))
-            assert abs(z[4 * j + 2 * p] - R * math.cos(2 * math.pi * u[2 * p + 1])) < 1e-15
-            assert abs(z[4 * j + 2 * p + 1] - R * math.sin(2 * math.pi * u[2 * p + 1])) < 1e-15
+    ctr = lambda w: [cell & 0xFFFFFFFF, iso, cell >> 32, w]
+    g, t = 32 * (s // 128) + s % 32, (s // 32) % 4
+    stream = [int(x) for j in range(3) for x in O.philox4x32_10(ctr(2 * (3 * g + j)), key)]
+    A, B, C = stream[3 * t:3 * t + 3]
+    D = (A >> 24) | ((B >> 24) << 8) | ((C >> 24) << 16)
+    r = [int(x) for x in O.philox4x32_10(ctr(2 * s + 1), key)]
+    want = [*_bm(A, C), *_bm(B, D), *_bm(r[0], r[1]), *_bm(r[2], r[3])]
+    assert np.abs(np.asarray(z) - np.asarray(want)).max() < 1e-15
+
+
+def test_normals_words_not_shared():
+    # every phase-1 word of a 128-sample block of a lane group is used by exactly one sample,
+    # and no counter of phase 1 (even) meets one of phase 2 (odd)
+    seen = {}
+    for s in range(1024):
+        g, t = 32 * (s // 128) + s % 32, (s // 32) % 4
+        for i in range(3 * t, 3 * t + 3):
+            w = (2 * (3 * g + i // 4), i % 4)
+            assert w not in seen, (s, seen.get(w))
+            seen[w] = s
+    assert len(seen) == 3 * 1024 and all(w % 2 == 0 for w, _ in seen)
 
 
 def test_normals_statistics():
