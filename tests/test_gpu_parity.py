@@ -926,3 +926,27 @@ def test_sgpr_beta_box(name, mode, beta, k, dev):
     lcp_o = M.pmc_cells(sel, th, 1000, cfg.mc_seed)
     frac, mean, mx = lcp_parity(lcp_g, lcp_o, 1000)
     assert frac >= 0.999 and mean <= 1e-4, (frac, mean, mx)
+
+
+@pytest.mark.parametrize("N", [1, 5, 31, 33, 100, 129, 191, 300])
+def test_pmc_partial_lane_groups(dev, N):
+    # R13c: a lane draws its phase-1 words in groups of 128 samples (3 Philox blocks per 4
+    # samples); sample counts that end inside a group (N mod 128 != 0, N < 32: idle lanes)
+    # must count exactly the oracle's samples -- single isovalue (k_pmc<1>, two samples per
+    # lane in flight) and a fused 6-isovalue pass (k_pmc<6>, one in flight)
+    w, ctx, M = _ctx("c1", dev)
+    cfg = w.cfg
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    lv = leaves.cpu().numpy()
+    sel = np.linspace(0, len(lv) - 1, 300).astype(int)
+    cells = torch.from_numpy(lv[sel]).to(dev)
+    got = np.rint(ctx.pmc_cells(cells, th, N, 17).cpu().numpy().astype(np.float64) * N)
+    want = np.rint(M.pmc_cells(lv[sel], th, N, 17) * N)
+    d = np.abs(got - want)
+    assert d.max() <= 1 and np.mean(d == 0) >= 0.99, (N, d.max(), np.mean(d == 0))
+    ths = list(th + np.linspace(-0.3, 0.3, 6))
+    got6 = np.rint(ctx.pmc_cells_multi(cells, ths, N, 17, 2).cpu().numpy().astype(np.float64) * N)
+    want6 = np.rint(M.pmc_cells_multi(lv[sel], ths, N, 17, 2) * N)
+    d6 = np.abs(got6 - want6)
+    assert d6.max() <= 1 and np.mean(d6 == 0) >= 0.99, (N, d6.max(), np.mean(d6 == 0))
