@@ -21,9 +21,6 @@
 
 namespace lcp {
 
-#ifndef PMC_PAIR   // 1: phase 1 of two samples at once, FFMA2 across the samples
-#define PMC_PAIR 0
-#endif
 #ifndef PMC_SCALAR_LZ   // 1: scalar FFMA chains for the phase-1 L'z instead of FFMA2
 #define PMC_SCALAR_LZ 0
 #endif
@@ -244,21 +241,6 @@ __device__ __forceinline__ f2_t box_muller2(uint32_t ra, uint32_t rb, uint32_t o
   float s, co;
   __sincosf(fmaf(6.283185307179586f, fb, -9.424777586727f), &s, &co);
   return fmul2(pk(co, s), pk(r, r));
-}
-
-// Box-Muller of two samples a, b at once: zc = (r_a cos_a, r_b cos_b), zs = (r_a sin_a, r_b sin_b)
-// -- the products of box_muller2, paired across the samples instead of within one
-__device__ __forceinline__ void box_muller_x2(uint32_t ra_a, uint32_t rb_a, uint32_t ra_b, uint32_t rb_b,
-                                              uint32_t one, f2_t& zc, f2_t& zs) {
-  const float ua_a = u23(ra_a, one), ua_b = u23(ra_b, one);
-  const float fb_a = __uint_as_float(mant1(rb_a, one)), fb_b = __uint_as_float(mant1(rb_b, one));
-  const float r_a = sqrt_approx(fabsf(lg2_approx(ua_a))), r_b = sqrt_approx(fabsf(lg2_approx(ua_b)));
-  float s_a, c_a, s_b, c_b;
-  __sincosf(fmaf(6.283185307179586f, fb_a, -9.424777586727f), &s_a, &c_a);
-  __sincosf(fmaf(6.283185307179586f, fb_b, -9.424777586727f), &s_b, &c_b);
-  const f2_t R = pk(r_a, r_b);
-  zc = fmul2(pk(c_a, c_b), R);
-  zs = fmul2(pk(s_a, s_b), R);
 }
 
 // Largest |z| Box-Muller can produce: u_a >= 2^-24 gives R <= sqrt(48 ln 2) = 5.7668;
@@ -485,50 +467,6 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, (T <= 8 ? PMC_MINBLOCKS : 8))
 #endif
     return decide(s, y, lo, hi, valid, st0, st1);
   };
-  // two samples a, b at once with FFMA2 across the samples: lane pair (value of a, value of b)
-  // times a uniform scalar operand (L', B from uniform registers), so no per-use copies of
-  // the coefficients into vector registers; the same FP32 operations per sample as phase1w
-  auto phase1pair = [&](uint32_t sa, uint32_t a0, uint32_t a1, uint32_t a2, bool va, float4& xa0, float4& xa1,
-                        uint32_t sb, uint32_t b0, uint32_t b1, uint32_t b2, bool vb, float4& xb0,
-                        float4& xb1, bool& pa, bool& pb) {
-    const uint32_t ad = __byte_perm(__byte_perm(a0, a1, 0x0073), a2, 0x0710);
-    const uint32_t bd = __byte_perm(__byte_perm(b0, b1, 0x0073), b2, 0x0710);
-    f2_t Z[4];   // Z[d] = (z_d of a, z_d of b)
-    box_muller_x2(a0, a2, b0, b2, ONE, Z[0], Z[1]);
-    box_muller_x2(a1, ad, b1, bd, ONE, Z[2], Z[3]);
-    auto bc = [](float v) { return pk(v, v); };
-    f2_t Y[4], LO[4], HI[4];
-    Y[0] = ffma2(Z[0], bc(L[0]), bc(m[0]));
-    Y[1] = ffma2(Z[1], bc(L[2]), ffma2(Z[0], bc(L[1]), bc(m[1])));
-    Y[2] = bc(m[2]);
-    Y[3] = bc(m[3]);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      Y[2] = ffma2(Z[d], bc(L[3 + d]), Y[2]);
-      Y[3] = ffma2(Z[d], bc(L[6 + d]), Y[3]);
-    }
-    Y[3] = ffma2(Z[3], bc(L33), Y[3]);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) LO[c] = bc(mB[c]);
-#pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      LO[0] = ffma2(Z[d], bc(L[10 + d]), LO[0]);
-      LO[1] = ffma2(Z[d], bc(L[15 + d]), LO[1]);
-      LO[2] = ffma2(Z[d], bc(L[21 + d]), LO[2]);
-      LO[3] = ffma2(Z[d], bc(L[28 + d]), LO[3]);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) HI[c] = ffma2(TWO, bc(B[c]), LO[c]);
-    float ya[4], yb[4], la[4], lb[4], ha[4], hb[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      upk(Y[c], ya[c], yb[c]);
-      upk(LO[c], la[c], lb[c]);
-      upk(HI[c], ha[c], hb[c]);
-    }
-    pa = decide(sa, ya, la, ha, va, xa0, xa1);
-    pb = decide(sb, yb, lb, hb, vb, xb0, xb1);
-  };
   // phase-2 operands: columns 4..7 of corners 4..7
   const f2_t Q45[1] = {pk(L[14], L[19])};
   const f2_t Q67[3] = {pk(L[25], L[32]), pk(L[26], L[33]), pk(L[27], L[34])};
@@ -624,13 +562,8 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, (T <= 8 ? PMC_MINBLOCKS : 8))
     float4 x0, x1, y0, y1;
     {
       const uint32_t sa = base + lane, sb = sa + 32u;
-      bool pa, pb;
-      if constexpr (PMC_PAIR && ILP >= 2) {
-        phase1pair(sa, a0, a1, a2, full || sa < Nl, x0, x1, sb, a3, b0, b1, full || sb < Nl, y0, y1, pa, pb);
-      } else {
-        pa = phase1w(sa, a0, a1, a2, full || sa < Nl, x0, x1);
-        pb = phase1w(sb, a3, b0, b1, full || sb < Nl, y0, y1);
-      }
+      const bool pa = phase1w(sa, a0, a1, a2, full || sa < Nl, x0, x1);
+      const bool pb = phase1w(sb, a3, b0, b1, full || sb < Nl, y0, y1);
       if (ILP >= 2) {
         push2(pa, x0, x1, pb, y0, y1);
         drain();
@@ -647,13 +580,8 @@ __global__ void __launch_bounds__(PMC_WARPS * 32, (T <= 8 ? PMC_MINBLOCKS : 8))
     philox4x32_10(c1, iso, c2, 2u * (3u * g + 2u), K, e0, e1, e2, e3);
     {
       const uint32_t sc = base + 64u + lane, sd = sc + 32u;
-      bool pc, pd;
-      if constexpr (PMC_PAIR && ILP >= 2) {
-        phase1pair(sc, b2, b3, e0, full || sc < Nl, x0, x1, sd, e1, e2, e3, full || sd < Nl, y0, y1, pc, pd);
-      } else {
-        pc = phase1w(sc, b2, b3, e0, full || sc < Nl, x0, x1);
-        pd = phase1w(sd, e1, e2, e3, full || sd < Nl, y0, y1);
-      }
+      const bool pc = phase1w(sc, b2, b3, e0, full || sc < Nl, x0, x1);
+      const bool pd = phase1w(sd, e1, e2, e3, full || sd < Nl, y0, y1);
       if (ILP >= 2) {
         push2(pc, x0, x1, pd, y0, y1);
         drain();
