@@ -115,6 +115,24 @@ def test_normals_statistics():
     assert np.abs(C - np.eye(8)).max() < 5 / math.sqrt(30000)
 
 
+def test_normals_pairwise_independence():
+    # R13c draws (z2, z3) from the low 23 bits of word B and the top bytes of A, B, C, while
+    # (z0, z1) use the low 23 bits of A and C: a 2-D chi-square over 8 x 8 cells of the
+    # probability-integral transform finds no dependence between any two of the eight normals,
+    # across samples of all four group positions t
+    Z = np.array([O.normals8(99, 12345, 1, s) for s in range(32000)])
+    U = stats.norm.cdf(Z)
+    for i in range(8):
+        for j in range(i + 1, 8):
+            H, _, _ = np.histogram2d(U[:, i], U[:, j], bins=8, range=[[0, 1], [0, 1]])
+            chi2 = ((H - len(U) / 64) ** 2 / (len(U) / 64)).sum()
+            assert stats.chi2.sf(chi2, 63) > 1e-4, (i, j, chi2)
+    # and the four positions t of a lane group draw the same distribution
+    t = (np.arange(len(Z)) // 32) % 4
+    for q in range(4):
+        assert stats.kstest(Z[t == q].ravel(), "norm").pvalue > 1e-4, q
+
+
 # ----------------------------------------------------------------- P5 chol8
 def test_chol8_matches_numpy_on_pd():
     g = np.random.default_rng(7)
