@@ -171,7 +171,7 @@ lcp_status_t lcp_octree_refine(lcp_ctx_t* ctx, double isovalue, double threshold
 
 /* a7-a8: for each cell id, the 8-corner posterior of the cell's bucket local
  * GP, its 8x8 Cholesky (R14), and an N-sample Philox MC count
- * of samples whose corners straddle `isovalue` (R13, R24).
+ * of samples whose corners straddle `isovalue` (R13, R13c, R24).
  *   cells: n_cells ids (device pointer if cells_on_device, else host);
  *   lcp_out: n_cells floats = count / n_samples (device pointer if
  *   out_on_device, else host: the call then synchronizes).
