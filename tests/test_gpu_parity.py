@@ -950,3 +950,19 @@ def test_pmc_partial_lane_groups(dev, N):
     want6 = np.rint(M.pmc_cells_multi(lv[sel], ths, N, 17, 2) * N)
     d6 = np.abs(got6 - want6)
     assert d6.max() <= 1 and np.mean(d6 == 0) >= 0.99, (N, d6.max(), np.mean(d6 == 0))
+
+
+def test_pmc_large_sample_count(dev):
+    # R13c counters at a large, odd N (lane groups up to g ~ N/4, counter words up to ~1.5 N):
+    # the sample counts equal the oracle's within one sample per cell
+    w, ctx, M = _ctx("c1", dev)
+    cfg = w.cfg
+    th = w.thetas[0]
+    leaves = ctx.octree_refine(th, cfg.alpha, cfg.max_depth)
+    lv = leaves.cpu().numpy()
+    sel = np.linspace(0, len(lv) - 1, 3).astype(int)
+    N = 1_000_003
+    cells = torch.from_numpy(lv[sel]).to(dev)
+    got = np.rint(ctx.pmc_cells(cells, th, N, 23).cpu().numpy().astype(np.float64) * N)
+    want = np.rint(M.pmc_cells(lv[sel], th, N, 23) * N)
+    assert np.abs(got - want).max() <= 2, (got, want)
