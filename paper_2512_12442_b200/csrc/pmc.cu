@@ -121,10 +121,57 @@ __global__ void __launch_bounds__(64) k_chol8_rec(Geom g, const uint64_t* __rest
   for (int e = q; e < 64 * (int)(sizeof(CellRec) / 16); e += 64) dst[e] = s4[e];
 }
 
+// The same conversion without shared-memory staging, thread per cell (one-warp CTAs, two per
+// brick): each thread reads its own 352-B slot with 16-B loads and writes its 208-B record with
+// 16-B stores.  0.92 ms per 131 072-brick chunk against 1.13 ms for the staged kernel above
+// (CHOL8_REC_DIRECT = 0).  Run beside the next chunk's k_brick on a second stream it would slow
+// k_brick by more than it hides (c5 pass 386.7 -> 396.8 ms with a matching carve-out; without
+// one the two never share an SM).  Records bit-identical.
+#ifndef CHOL8_REC_DIRECT
+#define CHOL8_REC_DIRECT 1
+#endif
+__global__ void __launch_bounds__(32) k_chol8_rec_direct(Geom g, const uint64_t* __restrict__ bricks, int64_t nb,
+                                                         const uint8_t* __restrict__ ucomp,
+                                                         const double* __restrict__ post, CellRec* __restrict__ recs) {
+  const int64_t u = blockIdx.x >> 1;
+  if (u >= nb || !ucomp[u]) return;   // brick done by an earlier refine: its records stand
+  const int q = ((blockIdx.x & 1) << 5) | threadIdx.x;   // local cell of the brick (x fastest)
+  const double2* src = reinterpret_cast<const double2*>(post + 44 * (64 * u + q));
+  double mu[8], sig[36];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const double2 v = src[t];
+    mu[2 * t] = v.x;
+    mu[2 * t + 1] = v.y;
+  }
+#pragma unroll
+  for (int t = 0; t < 18; ++t) {
+    const double2 v = src[4 + t];
+    sig[2 * t] = v.x;
+    sig[2 * t + 1] = v.y;
+  }
+  double mo[8];
+  float Lf[36];
+  chol8_factor(mu, sig, mo, Lf);
+  int bi, bj, bk;
+  node_unkey(bricks[u], bi, bj, bk);
+  CellRec* r = recs + rec_index(g, 4 * bi, 4 * bj, 4 * bk) + morton3(q & 3, (q >> 2) & 3, q >> 4);
+  double2* m2 = reinterpret_cast<double2*>(r->mu);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) m2[t] = make_double2(mo[2 * t], mo[2 * t + 1]);
+  float4* l4 = reinterpret_cast<float4*>(r->L);
+#pragma unroll
+  for (int t = 0; t < 9; ++t) l4[t] = make_float4(Lf[4 * t], Lf[4 * t + 1], Lf[4 * t + 2], Lf[4 * t + 3]);
+}
+
 cudaError_t launch_chol8_rec(Ctx& c, const uint64_t* bricks, int64_t nb, const double* post) {
   if (nb <= 0) return cudaSuccess;
-  k_chol8_rec<<<(unsigned)nb, 64, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(), post,
-                                                  c.crec.as<CellRec>());
+  if (CHOL8_REC_DIRECT)
+    k_chol8_rec_direct<<<(unsigned)(2 * nb), 32, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(), post,
+                                                                 c.crec.as<CellRec>());
+  else
+    k_chol8_rec<<<(unsigned)nb, 64, 0, c.stream>>>(c.g, bricks, nb, c.brick_unit.as<uint8_t>(), post,
+                                                   c.crec.as<CellRec>());
   ++c.n_launch;
   return cudaGetLastError();
 }
